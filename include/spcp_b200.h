@@ -1,0 +1,185 @@
+/*
+ * spcp_b200.h — C ABI of the B200-native Split-SPCP hot path.
+ *
+ * The reference (arXiv:1702.02241, /root/reference/pkg/src/spcp) is a pure
+ * Python/numpy package, so its "FFI" for this path is the set of Python
+ * entry points listed below; each C entry point replaces the numpy/BLAS work
+ * behind one of them.  The Python host layer (paper_1702_02241_b200/) binds
+ * these symbols with ctypes and keeps the reference's Python signatures,
+ * argument meaning and exceptions.
+ *
+ *   spcp_problem_create      <- ProblemSpec(x, lambda_l, lambda_s, mask)
+ *                               objective.py:20-59 (+ validation.py:10-34)
+ *   spcp_eval / _partial /
+ *   spcp_eval_finish         <- split_objective(fp, spec)      solver.py:105-123
+ *                               via _flat_split_objective      solver.py:219-225
+ *                               called per line-search trial   lbfgs.py:55-61
+ *   spcp_split_objective_host<- split_objective with host (numpy) buffers
+ *   spcp_phi_dense_host      <- phi_value_grad(l, spec)        objective.py:90-117
+ *   spcp_apply               <- the m x n products of certificate.py:93-103,
+ *                               rand_svd linalg.py:97-105 and the growth
+ *                               power iteration solver.py:237-241
+ *   spcp_materialize         <- FactorPair.compose + phi_value_grad S*
+ *                               solver.py:313-320 (final L, S)
+ *   spcp_vec_*               <- the L-BFGS vector algebra  lbfgs.py:152-188
+ *   spcp_gram / spcp_matmul_small  <- thin_qr/factor_svd factor-space algebra
+ *                               linalg.py:43-59, certificate.py:50-67
+ *
+ * Conventions:
+ *   - every function returns an int status; 0 = SPCP_OK.  The Python layer
+ *     maps SPCP_ERR_VALUE -> ValueError, SPCP_ERR_DIMENSION -> DimensionError,
+ *     SPCP_ERR_NUMERICAL / SPCP_ERR_CUDA -> NumericalError (DeviceError);
+ *     spcp_last_error() holds the message (thread-local).
+ *   - matrices are row-major; the flat iterate is concat(U.ravel(), V.ravel())
+ *     in float64 exactly as FactorPair.flatten (solver.py:65-66).
+ *   - "dev" pointers are CUDA device pointers on the problem's device; work is
+ *     stream-ordered on the problem's stream; nothing allocates inside eval
+ *     once the workspace for a rank bound k has been created.
+ *   - inputs are never mutated; outputs are caller-owned buffers.
+ */
+#ifndef SPCP_B200_H
+#define SPCP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPCP_ABI_VERSION 1
+
+enum spcp_status {
+  SPCP_OK = 0,
+  SPCP_ERR_VALUE = 1,       /* ValueError        (validation.py:19-20, objective.py:40-43) */
+  SPCP_ERR_DIMENSION = 2,   /* DimensionError    (errors.py:8-9) */
+  SPCP_ERR_NUMERICAL = 3,   /* NumericalError    (errors.py:12-13) */
+  SPCP_ERR_CUDA = 4,        /* NumericalError subclass DeviceError: CUDA failure */
+  SPCP_ERR_UNSUPPORTED = 5, /* ValueError: option not built into this library */
+};
+
+enum spcp_dtype { SPCP_F32 = 0, SPCP_F64 = 1 };
+
+/* storage flags for spcp_problem_create */
+#define SPCP_STORE_F32 1u
+#define SPCP_STORE_F64 2u
+
+typedef struct spcp_problem spcp_problem;
+
+int spcp_abi_version(void);
+const char* spcp_last_error(void);
+int spcp_device_count(int* out);
+
+/* ---- ProblemSpec upload (objective.py:20-59) ------------------------------
+ * x: m x n row-major with leading dimension ldx (elements), float64 or
+ *    float32 (x_dtype), on the host (x_on_device = 0) or the device.
+ * mask: optional m x n bool bytes on the host (non-zero = observed), or NULL.
+ * store: SPCP_STORE_F32 | SPCP_STORE_F64 — which device copies of X to keep
+ *    (fp32 copy feeds the fp32 kernels, fp64 copy the fp64 kernels; an fp32
+ *    copy is also read exactly by the fp64 kernels when X is fp32-exact).
+ * n_total / col0: column-sharded mode; this problem holds
+ *    columns [col0, col0+n) of an m x n_total matrix.  Single GPU: n_total = n,
+ *    col0 = 0.
+ * stream: cudaStream_t to order all work on (NULL = legacy default stream).
+ */
+int spcp_problem_create(spcp_problem** out, int device, int64_t m, int64_t n,
+                        const void* x, int64_t ldx, int x_dtype, int x_on_device,
+                        const uint8_t* mask, unsigned store, double lambda_l,
+                        double lambda_s, int64_t n_total, int64_t col0, void* stream);
+int spcp_problem_destroy(spcp_problem* p);
+int spcp_problem_set_stream(spcp_problem* p, void* stream);
+/* info[0] = 0.5*||P_Omega X||_F^2 (local shard), info[1] = #observed entries,
+ * info[2] = stored dtypes mask, info[3] = device bytes held */
+int spcp_problem_info(spcp_problem* p, double* info);
+
+/* ---- objective + gradient (solver.py:105-123) ------------------------------
+ * Evaluates F and grad F at the trial point w = z + alpha*dz (dz may be NULL),
+ * z, dz, g_out: device float64 vectors of length (m + n)*k, flat [U | V].
+ * dtype: SPCP_F32 runs the fused fp32 streaming kernel (fp64 accumulation of
+ * the objective, fp64 regulariser and trial point); SPCP_F64 runs it in fp64.
+ * out (host, 8 doubles): [0] f, [1] phi, [2] lambda/2(|U|^2+|V|^2),
+ *   [3] g . dz (0 when dz == NULL), [4] |g|^2, [5] |g_U|^2, [6] g_U . dz_U,
+ *   [7] reserved.  The call synchronises the problem's stream. */
+int spcp_eval(spcp_problem* p, int64_t k, int dtype, const double* z, const double* dz,
+              double alpha, double* g_out, double* out);
+
+/* Sharded evaluation split around the grad_U all-reduce:
+ * _partial writes the shard's G_p V_p (m x k, `dtype` elements) into gu_part
+ * (device), 4 shard scalars [phi_p, lambda/2|V_p|^2, g_V.dz_V, |g_V|^2] into
+ * scal (device float64) and the shard-local grad_V into g_out's V block.
+ * The caller all-reduces gu_part and scal across ranks, then _finish adds
+ * lambda*U, writes g_out's U block and fills out[8] as spcp_eval (synchronous). */
+int spcp_eval_partial(spcp_problem* p, int64_t k, int dtype, const double* z,
+                      const double* dz, double alpha, void* gu_part, double* scal,
+                      double* g_out);
+int spcp_eval_finish(spcp_problem* p, int64_t k, int dtype, const double* z,
+                     const double* dz, double alpha, const void* gu_sum,
+                     const double* scal_sum, double* g_out, double* out);
+
+/* Host-buffer drop-in for split_objective (the e2e path): u (m x k), v (n x k)
+ * float64 host arrays in, value and grad_u / grad_v float64 host arrays out. */
+int spcp_split_objective_host(spcp_problem* p, int64_t k, int dtype, const double* u,
+                              const double* v, double* value, double* grad_u,
+                              double* grad_v);
+
+/* Host-buffer drop-in for phi_value_grad(l, spec) (objective.py:90-117):
+ * l is m x n float64; grad / s_star outputs may be NULL. */
+int spcp_phi_dense_host(spcp_problem* p, const double* l, double* value, double* grad,
+                        double* s_star);
+
+/* ---- streaming operator products (certificate / rSVD / growth) -------------
+ * With G = grad phi(U V^T) (k >= 1, z = flat [U|V] float64 device) or, when
+ * k == 0, G = P_Omega(X) (the zero-filled observed matrix, ProblemSpec.observed
+ * objective.py:49-53), computes
+ *   left_out  (m x b) = G  @ w_right   (w_right: n x b)   if w_right != NULL
+ *   right_out (n x b) = G^T @ w_left   (w_left:  m x b)   if w_left  != NULL
+ * in float64 (all pointers device float64, row-major).  In sharded mode the
+ * left product is the shard's partial sum (caller all-reduces). */
+int spcp_apply(spcp_problem* p, int64_t k, const double* z, int64_t b,
+               const double* w_right, double* left_out, const double* w_left,
+               double* right_out);
+
+/* ---- final L and S (solver.py:313-320) --------------------------------------
+ * Rows [row0, row0+rows) of L = U V^T and S* = shrink(X - L) on Omega, float64,
+ * written to device or host buffers (row-major, n columns); either may be NULL. */
+int spcp_materialize(spcp_problem* p, int64_t k, const double* z, int64_t row0,
+                     int64_t rows, double* l_out, double* s_out, int out_on_host);
+
+/* Dense grad phi(U V^T) (m x n float64, device, row stride ldo) — the
+ * materialised D = -G/lambda of certificate.py:93-95, used only for small
+ * problems where the complement SVD is done densely like the reference. */
+int spcp_materialize_grad(spcp_problem* p, int64_t k, const double* z, double* g_out,
+                          int64_t ldo);
+
+/* ---- L-BFGS vector algebra (lbfgs.py:152-188, compact form) -----------------
+ * All device float64, length len.  Deterministic (fixed-order) reductions.
+ * multidot: out_host[i] = <a[i], b[i]> for i < count (a, b: host arrays of
+ *   device pointers).  lincomb: out = sum_i coef[i] * v[i] (out may alias v[0]).
+ */
+int spcp_vec_multidot(spcp_problem* p, int64_t len, int count, const double* const* a,
+                      const double* const* b, double* out_host);
+int spcp_vec_lincomb(spcp_problem* p, int64_t len, int count, const double* coef,
+                     const double* const* v, double* out);
+/* vec_gram: out_host[i*nb + j] = <a[i], b[j]>, i < na, j < nb (nb <= 4); every
+ * vector is read once (one pass for all dots of an L-BFGS iteration). */
+int spcp_vec_gram(spcp_problem* p, int64_t len, int na, const double* const* a, int nb,
+                  const double* const* b, double* out_host);
+
+/* ---- tall-skinny factor algebra (linalg.py:43-59, certificate.py:50-67) ----
+ * gram: out_host (p x q, float64) = A^T B, A: rows x p, B: rows x q (device).
+ * matmul_small: C (rows x q) = A (rows x p) @ M (p x q, host float64). */
+int spcp_gram(spcp_problem* p, int64_t rows, int64_t pa, const double* a, int64_t qb,
+              const double* b, double* out_host);
+int spcp_matmul_small(spcp_problem* p, int64_t rows, int64_t pa, const double* a,
+                      int64_t qb, const double* m_host, double* c);
+
+/* ---- profiling: CUDA-event time of the fused streaming kernel --------------
+ * When enabled, every eval records events around its main kernel; read
+ * returns the accumulated milliseconds and launch count, then resets. */
+int spcp_prof_enable(spcp_problem* p, int on);
+int spcp_prof_read(spcp_problem* p, double* ms_total, int64_t* launches,
+                   int64_t* kernels_launched);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPCP_B200_H */

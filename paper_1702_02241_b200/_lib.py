@@ -1,0 +1,84 @@
+"""ctypes binding of libspcp_b200.so (the C ABI declared in include/spcp_b200.h).
+
+The shared library is built in-tree by `__graft_entry__.build()` / `make`.
+There is no fallback: if the library is missing or does not export the ABI,
+importing the compute path raises immediately.
+"""
+
+import ctypes
+import os
+
+from .errors import DeviceError, DimensionError, NumericalError
+
+__all__ = ["lib", "check", "LIB_PATH", "SPCP_F32", "SPCP_F64", "STORE_F32", "STORE_F64",
+           "EXPORTS"]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libspcp_b200.so")
+
+SPCP_OK, SPCP_ERR_VALUE, SPCP_ERR_DIMENSION, SPCP_ERR_NUMERICAL, SPCP_ERR_CUDA, \
+    SPCP_ERR_UNSUPPORTED = range(6)
+SPCP_F32, SPCP_F64 = 0, 1
+STORE_F32, STORE_F64 = 1, 2
+
+_i64, _i32, _u32 = ctypes.c_int64, ctypes.c_int, ctypes.c_uint
+_vp, _dp, _d = ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_double
+_pp = ctypes.POINTER(ctypes.c_void_p)
+
+# name -> (argtypes); every function returns int status except the two noted
+EXPORTS = {
+    "spcp_abi_version": [],
+    "spcp_last_error": [],
+    "spcp_device_count": [ctypes.POINTER(_i32)],
+    "spcp_problem_create": [_pp, _i32, _i64, _i64, _vp, _i64, _i32, _i32, _vp, _u32, _d, _d,
+                            _i64, _i64, _vp],
+    "spcp_problem_destroy": [_vp],
+    "spcp_problem_set_stream": [_vp, _vp],
+    "spcp_problem_info": [_vp, _dp],
+    "spcp_eval": [_vp, _i64, _i32, _vp, _vp, _d, _vp, _dp],
+    "spcp_eval_partial": [_vp, _i64, _i32, _vp, _vp, _d, _vp, _vp, _vp],
+    "spcp_eval_finish": [_vp, _i64, _i32, _vp, _vp, _d, _vp, _vp, _vp, _dp],
+    "spcp_split_objective_host": [_vp, _i64, _i32, _vp, _vp, _dp, _vp, _vp],
+    "spcp_phi_dense_host": [_vp, _vp, _dp, _vp, _vp],
+    "spcp_apply": [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp],
+    "spcp_materialize": [_vp, _i64, _vp, _i64, _i64, _vp, _vp, _i32],
+    "spcp_materialize_grad": [_vp, _i64, _vp, _vp, _i64],
+    "spcp_vec_multidot": [_vp, _i64, _i32, _pp, _pp, _dp],
+    "spcp_vec_lincomb": [_vp, _i64, _i32, _dp, _pp, _vp],
+    "spcp_vec_gram": [_vp, _i64, _i32, _pp, _i32, _pp, _dp],
+    "spcp_gram": [_vp, _i64, _i64, _vp, _i64, _vp, _dp],
+    "spcp_matmul_small": [_vp, _i64, _i64, _vp, _i64, _dp, _vp],
+    "spcp_prof_enable": [_vp, _i32],
+    "spcp_prof_read": [_vp, _dp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)],
+}
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "or `make` (there is no CPU fallback for the compute path)")
+    so = ctypes.CDLL(LIB_PATH)
+    for name, argtypes in EXPORTS.items():
+        fn = getattr(so, name)  # AttributeError = ABI mismatch: fail loudly
+        fn.argtypes = argtypes
+        fn.restype = ctypes.c_char_p if name == "spcp_last_error" else ctypes.c_int
+    if so.spcp_abi_version() != 1:
+        raise ImportError("libspcp_b200.so ABI version mismatch")
+    return so
+
+
+lib = _load()
+
+
+def check(rc):
+    """Map a C status to the reference's exception types."""
+    if rc == SPCP_OK:
+        return
+    msg = (lib.spcp_last_error() or b"").decode(errors="replace")
+    if rc == SPCP_ERR_DIMENSION:
+        raise DimensionError(msg)
+    if rc in (SPCP_ERR_VALUE, SPCP_ERR_UNSUPPORTED):
+        raise ValueError(msg)
+    if rc == SPCP_ERR_CUDA:
+        raise DeviceError(msg)
+    raise NumericalError(msg)

@@ -1,0 +1,1055 @@
+// spcp_api.cu — C ABI (include/spcp_b200.h) over the sm_100a kernels.
+//
+// Owns the device copy of the problem (ProblemSpec, objective.py:20-59): X in
+// a padded row-major layout (rows to 128, columns to 64, zero pads so padded
+// entries contribute r = 0), the bit-packed observation mask and the
+// workspaces of the fused streaming pass.  Every call is stream-ordered on the
+// problem's stream; results that the reference returns as Python floats come
+// back through a pinned host buffer after one stream synchronisation.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "aux_kernels.cuh"
+#include "common.cuh"
+#include "stream_simt.cuh"
+
+namespace spcp {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+  g_last_error = std::string("CUDA error in ") + where + ": " + cudaGetErrorString(e);
+  return SPCP_ERR_CUDA;
+}
+
+// ------------------------------------------------------------------ buffers
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t want) {
+    if (want <= bytes) return SPCP_OK;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&ptr, want);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(workspace)");
+    bytes = want;
+    return SPCP_OK;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+  template <typename T>
+  T* as() const {
+    return reinterpret_cast<T*>(ptr);
+  }
+};
+
+}  // namespace spcp
+
+struct spcp_problem {
+  int device = 0;
+  int64_t m = 0, n = 0, n_total = 0, col0 = 0;
+  int64_t m_pad = 0, n_pad = 0, ldx = 0, ldm = 0;
+  bool masked = false;
+  double lambda_l = 1.0, lambda_s = 1.0;
+  cudaStream_t stream = nullptr;
+  double f_zero = 0.0, n_obs = 0.0;
+  unsigned stored = 0;
+  spcp::DevBuf x32, x64, mbits;
+  // workspaces
+  spcp::DevBuf uc, vc, wr, wl, pleft, pright, pphi, blk, out_dev, counter, scratch, scal,
+      gu_tmp, vec_part, small;
+  double* host_out = nullptr;  // pinned [64]
+  // profiling
+  bool prof = false;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool ev_pending = false;
+  double prof_ms = 0.0;
+  int64_t prof_count = 0;
+  int64_t launches = 0;
+};
+
+namespace spcp {
+
+// ------------------------------------------------------------------ dispatch
+template <typename T>
+struct DT;
+template <>
+struct DT<float> {
+  static constexpr int id = SPCP_F32;
+};
+template <>
+struct DT<double> {
+  static constexpr int id = SPCP_F64;
+};
+
+struct LaunchShape {
+  int nchunks = 1, nrb = 1;
+  int64_t chunk_cols = 0;
+};
+
+template <typename T, typename TX, int KR, int PW, int MODE, bool MASK>
+static int launch_stream(spcp_problem* p, StreamParams sp, LaunchShape& shape, bool prof) {
+  using G = StreamGeom<T>;
+  auto kern = stream_kernel<T, TX, KR, PW, MODE, MASK>;
+  constexpr size_t smem = stream_smem_bytes<T, TX, KR, PW, MODE, MASK>();
+  static int occ = -1;  // per instantiation
+  if (occ < 0) {
+    SPCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int o = 0;
+    SPCP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, G::NT, smem));
+    occ = std::max(o, 1);
+  }
+  const int64_t nrb = p->m_pad / G::BM;
+  const int64_t ntiles = p->n_pad / G::BN;
+  // enough CTAs for ~4 waves, but keep each chunk >= 4 tiles when possible
+  const int64_t target = int64_t(kSMs) * occ * 4;
+  int64_t nch = ceil_div(target, nrb);
+  nch = std::max<int64_t>(1, std::min<int64_t>(nch, std::max<int64_t>(1, ntiles / 4)));
+  const int64_t tiles_per = ceil_div(ntiles, nch);
+  nch = ceil_div(ntiles, tiles_per);
+  sp.chunk_cols = tiles_per * G::BN;
+  sp.nchunks = int(nch);
+  shape.nchunks = int(nch);
+  shape.nrb = int(nrb);
+  shape.chunk_cols = sp.chunk_cols;
+  // partial buffers
+  int rc;
+  if ((rc = p->pleft.ensure(size_t(nch) * p->m_pad * PW * sizeof(T)))) return rc;
+  if ((rc = p->pright.ensure(size_t(nrb) * p->n_pad * PW * sizeof(T)))) return rc;
+  if ((rc = p->pphi.ensure(size_t(nrb * nch) * sizeof(double)))) return rc;
+  sp.pleft = p->pleft.ptr;
+  sp.pright = p->pright.ptr;
+  sp.pphi = p->pphi.as<double>();
+  dim3 grid{unsigned(nch), unsigned(nrb), 1u};
+  if (prof) SPCP_CUDA(cudaEventRecord(p->ev0, p->stream));
+  kern<<<grid, G::NT, smem, p->stream>>>(sp);
+  SPCP_CHECK_LAUNCH("stream_kernel");
+  if (prof) SPCP_CUDA(cudaEventRecord(p->ev1, p->stream));
+  p->launches++;
+  return SPCP_OK;
+}
+
+// fused EVAL kernel widths
+#define SPCP_EVAL_F32_LIST(X) X(4) X(8) X(12) X(16) X(20) X(24) X(28) X(32) X(40) X(48) X(56) X(64)
+#define SPCP_EVAL_F64_LIST(X) X(4) X(8) X(12) X(16) X(20) X(24) X(28) X(32)
+
+static int eval_kp(int dtype, int64_t k) {
+  if (dtype == SPCP_F32) {
+    static const int l[] = {4, 8, 12, 16, 20, 24, 28, 32, 40, 48, 56, 64};
+    for (int v : l)
+      if (k <= v) return v;
+  } else {
+    static const int l[] = {4, 8, 12, 16, 20, 24, 28, 32};
+    for (int v : l)
+      if (k <= v) return v;
+  }
+  return 0;  // beyond the fused kernel: dense fallback
+}
+
+template <typename T, typename TX, bool MASK>
+static int dispatch_eval(spcp_problem* p, int kp, StreamParams sp, LaunchShape& sh) {
+  bool prof = p->prof;
+#define SPCP_CASE(K) \
+  case K:            \
+    return launch_stream<T, TX, K, K, MODE_EVAL, MASK>(p, sp, sh, prof);
+  if constexpr (sizeof(T) == 4) {
+    switch (kp) { SPCP_EVAL_F32_LIST(SPCP_CASE) }
+  } else {
+    switch (kp) { SPCP_EVAL_F64_LIST(SPCP_CASE) }
+  }
+#undef SPCP_CASE
+  return fail(SPCP_ERR_UNSUPPORTED, "no fused kernel for this rank bound");
+}
+
+// APPLY / RAW (float64 only)
+static int apply_kr(int64_t k) {
+  if (k == 0) return 0;
+  if (k <= 8) return 8;
+  if (k <= 16) return 16;
+  if (k <= 32) return 32;
+  return -1;
+}
+
+template <typename TX, bool MASK>
+static int dispatch_apply(spcp_problem* p, int kr, int pw, StreamParams sp, LaunchShape& sh) {
+#define SPCP_AP(KR, PW)                                                                 \
+  if (kr == KR && pw == PW)                                                           \
+    return KR == 0 ? launch_stream<double, TX, 0, PW, MODE_RAW, MASK>(p, sp, sh, false) \
+                   : launch_stream<double, TX, KR, PW, MODE_APPLY, MASK>(p, sp, sh, false);
+  SPCP_AP(0, 8)
+  SPCP_AP(0, 32)
+  SPCP_AP(8, 8)
+  SPCP_AP(8, 32)
+  SPCP_AP(16, 8)
+  SPCP_AP(16, 32)
+  SPCP_AP(32, 8)
+  SPCP_AP(32, 32)
+#undef SPCP_AP
+  return fail(SPCP_ERR_UNSUPPORTED, "no apply kernel for this width");
+}
+
+static inline int grid_for(int64_t total, int threads = 256, int64_t cap = 148 * 16) {
+  int64_t g = ceil_div(std::max<int64_t>(total, 1), threads);
+  return int(std::min<int64_t>(g, cap));
+}
+
+static int ensure_common(spcp_problem* p) {
+  int rc;
+  if ((rc = p->out_dev.ensure(64 * sizeof(double)))) return rc;
+  if ((rc = p->counter.ensure(64))) return rc;
+  if (!p->host_out) {
+    SPCP_CUDA(cudaMallocHost(&p->host_out, 64 * sizeof(double)));
+    SPCP_CUDA(cudaMemsetAsync(p->counter.ptr, 0, 64, p->stream));
+  }
+  return SPCP_OK;
+}
+
+static int prof_collect(spcp_problem* p) {
+  if (p->prof && p->ev_pending) {
+    float ms = 0.f;
+    SPCP_CUDA(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+    p->prof_ms += ms;
+    p->prof_count++;
+    p->ev_pending = false;
+  }
+  return SPCP_OK;
+}
+
+static int check_k(spcp_problem* p, int64_t k) {
+  if (k < 1 || k > std::min(p->m, p->n_total))
+    return fail(SPCP_ERR_DIMENSION, "rank bound k=" + std::to_string(k) + " out of range [1, " +
+                                        std::to_string(std::min(p->m, p->n_total)) + "]");
+  return SPCP_OK;
+}
+
+// Run prep + fused kernel; fills the partial buffers. kp == 0: dense fallback
+// (G materialised in float64, then RAW products), used for large rank bounds.
+static int run_stream_eval(spcp_problem* p, int64_t k, int dtype, const double* z,
+                           const double* dz, double alpha, int& kp_used, LaunchShape& sh,
+                           int& part_dtype);
+
+template <typename T>
+static int prep(spcp_problem* p, int64_t k, int kp, const double* z, const double* dz,
+                double alpha) {
+  int rc;
+  if ((rc = p->uc.ensure(size_t(p->m_pad) * kp * sizeof(T)))) return rc;
+  if ((rc = p->vc.ensure(size_t(p->n_pad) * kp * sizeof(T)))) return rc;
+  const int64_t total = (p->m_pad + p->n_pad) * kp;
+  prep_operands_kernel<T><<<grid_for(total), 256, 0, p->stream>>>(
+      z, dz, alpha, p->m, p->n, k, p->m_pad, p->n_pad, kp, p->uc.as<T>(), p->vc.as<T>());
+  SPCP_CHECK_LAUNCH("prep_operands");
+  p->launches++;
+  return SPCP_OK;
+}
+
+static StreamParams base_params(spcp_problem* p, bool want_f64) {
+  StreamParams sp{};
+  sp.m_pad = p->m_pad;
+  sp.n_pad = p->n_pad;
+  sp.ldx = p->ldx;
+  sp.x = want_f64 && p->x64.ptr ? p->x64.ptr : p->x32.ptr;
+  sp.mbits = p->masked ? p->mbits.as<uint32_t>() : nullptr;
+  sp.ldm = p->ldm;
+  sp.tau = p->lambda_s;
+  sp.do_left = 1;
+  sp.do_right = 1;
+  return sp;
+}
+
+static int dense_fallback_eval(spcp_problem* p, int64_t k, const double* z, const double* dz,
+                               double alpha, LaunchShape& sh);
+
+static int run_stream_eval(spcp_problem* p, int64_t k, int dtype, const double* z,
+                           const double* dz, double alpha, int& kp_used, LaunchShape& sh,
+                           int& part_dtype) {
+  int kp = eval_kp(dtype, k);
+  kp_used = kp;
+  if (dtype == SPCP_F32 && !p->x32.ptr)
+    return fail(SPCP_ERR_VALUE, "fp32 evaluation requested but no fp32 copy of X is stored");
+  if (kp == 0) {
+    part_dtype = SPCP_F64;
+    return dense_fallback_eval(p, k, z, dz, alpha, sh);
+  }
+  int rc;
+  if (dtype == SPCP_F32) {
+    part_dtype = SPCP_F32;
+    if ((rc = prep<float>(p, k, kp, z, dz, alpha))) return rc;
+    StreamParams sp = base_params(p, false);
+    sp.uc = p->uc.ptr;
+    sp.vc = p->vc.ptr;
+    return p->masked ? dispatch_eval<float, float, true>(p, kp, sp, sh)
+                     : dispatch_eval<float, float, false>(p, kp, sp, sh);
+  }
+  part_dtype = SPCP_F64;
+  if ((rc = prep<double>(p, k, kp, z, dz, alpha))) return rc;
+  StreamParams sp = base_params(p, true);
+  sp.uc = p->uc.ptr;
+  sp.vc = p->vc.ptr;
+  if (p->x64.ptr)
+    return p->masked ? dispatch_eval<double, double, true>(p, kp, sp, sh)
+                     : dispatch_eval<double, double, false>(p, kp, sp, sh);
+  return p->masked ? dispatch_eval<double, float, true>(p, kp, sp, sh)
+                   : dispatch_eval<double, float, false>(p, kp, sp, sh);
+}
+
+// ---- dense fallback: G (float64, m_pad x ldx scratch) then RAW products
+template <typename TX>
+static int launch_dense(spcp_problem* p, int mode, int64_t k, const double* z, int64_t row0,
+                        int64_t rows, double* l_out, double* s_out, int64_t ldo, double* pphi) {
+  dim3 grid(unsigned(ceil_div(p->n, 64)), unsigned(ceil_div(rows, 64)));
+  const TX* x = reinterpret_cast<const TX*>(sizeof(TX) == 8 ? p->x64.ptr : p->x32.ptr);
+  const uint32_t* mb = p->masked ? p->mbits.as<uint32_t>() : nullptr;
+  if (mode == 0)
+    dense_kernel<TX, 0><<<grid, 256, 0, p->stream>>>(z, p->m, p->n, k, x, p->ldx, mb, p->ldm,
+                                                    p->lambda_s, row0, rows, l_out, s_out, ldo,
+                                                    pphi);
+  else
+    dense_kernel<TX, 1><<<grid, 256, 0, p->stream>>>(z, p->m, p->n, k, x, p->ldx, mb, p->ldm,
+                                                    p->lambda_s, row0, rows, l_out, s_out, ldo,
+                                                    pphi);
+  SPCP_CHECK_LAUNCH("dense_kernel");
+  p->launches++;
+  return SPCP_OK;
+}
+
+static int dense_fallback_eval(spcp_problem* p, int64_t k, const double* z, const double* dz,
+                               double alpha, LaunchShape& sh) {
+  // trial point in float64
+  int rc;
+  const int64_t len = (p->m + p->n) * k;
+  if ((rc = p->scratch.ensure(size_t(len) * sizeof(double) +
+                              size_t(p->m_pad) * p->ldx * sizeof(double))))
+    return rc;
+  double* w = p->scratch.as<double>();
+  double* gmat = w + len;
+  {
+    VecPtrs vp{};
+    vp.a[0] = z;
+    vp.coef[0] = 1.0;
+    int cnt = 1;
+    if (dz) {
+      vp.a[1] = dz;
+      vp.coef[1] = alpha;
+      cnt = 2;
+    }
+    lincomb_kernel<<<grid_for(len), 256, 0, p->stream>>>(vp, cnt, len, w);
+    SPCP_CHECK_LAUNCH("lincomb");
+    p->launches++;
+  }
+  SPCP_CUDA(cudaMemsetAsync(gmat, 0, size_t(p->m_pad) * p->ldx * sizeof(double), p->stream));
+  const int64_t nbx = ceil_div(p->n, 64), nby = ceil_div(p->m, 64);
+  DevBuf& ph = p->pphi;
+  if ((rc = ph.ensure(size_t(nbx * nby) * sizeof(double)))) return rc;
+  rc = p->x64.ptr ? launch_dense<double>(p, 1, k, w, 0, p->m, gmat, nullptr, p->ldx,
+                                         ph.as<double>())
+                  : launch_dense<float>(p, 1, k, w, 0, p->m, gmat, nullptr, p->ldx,
+                                        ph.as<double>());
+  if (rc) return rc;
+  // products G V and G^T U through the RAW streaming kernel over gmat, in
+  // column blocks of 32 of the rank dimension
+  const int64_t nrb = p->m_pad / 128;
+  const int64_t ncb = ceil_div(k, 32);
+  // partial outputs laid out as the fused kernel's: pleft [1][m_pad][kp], pright [nrb][n_pad][kp]
+  const int kp = int(round_up(k, 2));
+  if ((rc = p->gu_tmp.ensure(size_t(p->m_pad) * kp * sizeof(double) +
+                             size_t(nrb) * p->n_pad * kp * sizeof(double))))
+    return rc;
+  double* pl = p->gu_tmp.as<double>();
+  double* pr = pl + p->m_pad * kp;
+  if ((rc = p->wr.ensure(size_t(p->n_pad) * 32 * sizeof(double)))) return rc;
+  if ((rc = p->wl.ensure(size_t(p->m_pad) * 32 * sizeof(double)))) return rc;
+  if ((rc = p->small.ensure(size_t(std::max(p->m_pad, p->n_pad)) * 32 * sizeof(double)))) return rc;
+  for (int64_t cb = 0; cb < ncb; ++cb) {
+    const int64_t c0 = cb * 32, bw = std::min<int64_t>(32, k - c0);
+    // operands: columns c0..c0+bw of V (for G V) and of U (for G^T U)
+    // gather via matmul_small with a selection matrix is overkill; use a strided copy
+    SPCP_CUDA(cudaMemsetAsync(p->wr.ptr, 0, size_t(p->n_pad) * 32 * sizeof(double), p->stream));
+    SPCP_CUDA(cudaMemsetAsync(p->wl.ptr, 0, size_t(p->m_pad) * 32 * sizeof(double), p->stream));
+    SPCP_CUDA(cudaMemcpy2DAsync(p->wr.ptr, 32 * sizeof(double), w + p->m * k + c0,
+                                k * sizeof(double), bw * sizeof(double), p->n,
+                                cudaMemcpyDeviceToDevice, p->stream));
+    SPCP_CUDA(cudaMemcpy2DAsync(p->wl.ptr, 32 * sizeof(double), w + c0, k * sizeof(double),
+                                bw * sizeof(double), p->m, cudaMemcpyDeviceToDevice, p->stream));
+    StreamParams sp{};
+    sp.m_pad = p->m_pad;
+    sp.n_pad = p->n_pad;
+    sp.ldx = p->ldx;
+    sp.x = gmat;
+    sp.mbits = nullptr;
+    sp.ldm = 0;
+    sp.tau = p->lambda_s;
+    sp.wr = p->wr.ptr;
+    sp.wl = p->wl.ptr;
+    sp.do_left = 1;
+    sp.do_right = 1;
+    LaunchShape s2;
+    if ((rc = launch_stream<double, double, 0, 32, MODE_RAW, false>(p, sp, s2, false))) return rc;
+    // fold partials of this column block into pl / pr column slots c0..c0+bw
+    // (pl: one chunk; pr: per row band) — reduce chunks now into pl
+    double* srcl = p->pleft.as<double>();
+    double* srcr = p->pright.as<double>();
+    // sum chunks of the left partial: use reduce_apply into small, then scatter
+    reduce_apply_kernel<double><<<grid_for(p->m * bw), 256, 0, p->stream>>>(
+        srcl, s2.nchunks, p->m, p->m_pad, 32, bw, p->small.as<double>());
+    SPCP_CHECK_LAUNCH("reduce_apply");
+    p->launches++;
+    SPCP_CUDA(cudaMemcpy2DAsync(pl + c0, kp * sizeof(double), p->small.ptr, bw * sizeof(double),
+                                bw * sizeof(double), p->m, cudaMemcpyDeviceToDevice, p->stream));
+    reduce_apply_kernel<double><<<grid_for(p->n * bw), 256, 0, p->stream>>>(
+        srcr, s2.nrb, p->n, p->n_pad, 32, bw, p->small.as<double>());
+    SPCP_CHECK_LAUNCH("reduce_apply");
+    p->launches++;
+    SPCP_CUDA(cudaMemcpy2DAsync(pr + c0, kp * sizeof(double), p->small.ptr, bw * sizeof(double),
+                                bw * sizeof(double), p->n, cudaMemcpyDeviceToDevice, p->stream));
+  }
+  // expose as a one-chunk / one-band partial set in pleft/pright
+  int rc2;
+  if ((rc2 = p->pleft.ensure(size_t(p->m_pad) * kp * sizeof(double)))) return rc2;
+  if ((rc2 = p->pright.ensure(size_t(p->n_pad) * kp * sizeof(double)))) return rc2;
+  SPCP_CUDA(cudaMemcpyAsync(p->pleft.ptr, pl, size_t(p->m_pad) * kp * sizeof(double),
+                            cudaMemcpyDeviceToDevice, p->stream));
+  SPCP_CUDA(cudaMemcpyAsync(p->pright.ptr, pr, size_t(p->n_pad) * kp * sizeof(double),
+                            cudaMemcpyDeviceToDevice, p->stream));
+  // pphi currently holds nbx*nby dense partials
+  sh.nchunks = 1;
+  sh.nrb = 1;
+  sh.chunk_cols = int64_t(nbx * nby);  // smuggle the phi partial count
+  return SPCP_OK;
+}
+
+static int run_reduce(spcp_problem* p, int64_t k, int kp, int part_dtype, const LaunchShape& sh,
+                      bool dense, const double* z, const double* dz, double alpha, int u_mode,
+                      int v_mode, const void* gu_sum, void* gu_part, const double* scal_sum,
+                      double* scal_out, double* g_out) {
+  int rc;
+  if ((rc = ensure_common(p))) return rc;
+  const int64_t work = std::max(p->m, p->n) * k;
+  const int nblk = grid_for(work, 256, 148 * 4);
+  if ((rc = p->blk.ensure(size_t(nblk) * 6 * sizeof(double)))) return rc;
+  ReduceParams rp{};
+  rp.m = p->m;
+  rp.n = p->n;
+  rp.k = k;
+  rp.m_pad = p->m_pad;
+  rp.n_pad = p->n_pad;
+  rp.kp = kp;
+  rp.z = z;
+  rp.dz = dz;
+  rp.alpha = alpha;
+  rp.lambda_l = p->lambda_l;
+  rp.pleft = p->pleft.ptr;
+  rp.nchunks = sh.nchunks;
+  rp.pright = p->pright.ptr;
+  rp.nrb = sh.nrb;
+  rp.gu_sum = gu_sum;
+  rp.gu_part = gu_part;
+  rp.g_out = g_out;
+  rp.u_mode = u_mode;
+  rp.v_mode = v_mode;
+  rp.blk = p->blk.as<double>();
+  rp.counter = p->counter.as<unsigned>();
+  rp.pphi = (u_mode == U_FROM_SUM) ? nullptr : p->pphi.as<double>();
+  rp.nphi = (u_mode == U_FROM_SUM) ? 0 : (dense ? int(sh.chunk_cols) : sh.nchunks * sh.nrb);
+  rp.scal_sum = scal_sum;
+  rp.scal_out = scal_out;
+  rp.out = p->out_dev.as<double>();
+  if (part_dtype == SPCP_F32)
+    reduce_kernel<float><<<nblk, 256, 0, p->stream>>>(rp);
+  else
+    reduce_kernel<double><<<nblk, 256, 0, p->stream>>>(rp);
+  SPCP_CHECK_LAUNCH("reduce_kernel");
+  p->launches++;
+  return SPCP_OK;
+}
+
+static int fetch_out(spcp_problem* p, double* out) {
+  SPCP_CUDA(cudaMemcpyAsync(p->host_out, p->out_dev.ptr, 8 * sizeof(double),
+                            cudaMemcpyDeviceToHost, p->stream));
+  SPCP_CUDA(cudaStreamSynchronize(p->stream));
+  if (p->prof && p->ev_pending) prof_collect(p);
+  std::memcpy(out, p->host_out, 8 * sizeof(double));
+  return SPCP_OK;
+}
+
+}  // namespace spcp
+
+using namespace spcp;
+
+// ====================================================================== ABI
+extern "C" {
+
+int spcp_abi_version(void) { return SPCP_ABI_VERSION; }
+const char* spcp_last_error(void) { return g_last_error.c_str(); }
+
+int spcp_device_count(int* out) {
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) {
+    *out = 0;
+    return cuda_fail(e, "cudaGetDeviceCount");
+  }
+  *out = c;
+  return SPCP_OK;
+}
+
+int spcp_problem_create(spcp_problem** out, int device, int64_t m, int64_t n, const void* x,
+                        int64_t ldx, int x_dtype, int x_on_device, const uint8_t* mask,
+                        unsigned store, double lambda_l, double lambda_s, int64_t n_total,
+                        int64_t col0, void* stream) {
+  if (!out) return fail(SPCP_ERR_VALUE, "null output handle");
+  *out = nullptr;
+  if (m < 1 || n < 1) return fail(SPCP_ERR_DIMENSION, "X must be a non-empty 2-D matrix");
+  if (ldx < n) return fail(SPCP_ERR_DIMENSION, "ldx < n");
+  if (!(lambda_l > 0.0)) return fail(SPCP_ERR_VALUE, "lambda_l must be positive");
+  if (!(lambda_s > 0.0)) return fail(SPCP_ERR_VALUE, "lambda_s must be positive");
+  if (x_dtype != SPCP_F32 && x_dtype != SPCP_F64) return fail(SPCP_ERR_VALUE, "bad x dtype");
+  if ((store & 3u) == 0) return fail(SPCP_ERR_VALUE, "store must keep fp32 and/or fp64 X");
+  if (n_total < n || col0 < 0 || col0 + n > n_total)
+    return fail(SPCP_ERR_DIMENSION, "bad column shard");
+  SPCP_CUDA(cudaSetDevice(device));
+  auto* p = new spcp_problem();
+  p->device = device;
+  p->m = m;
+  p->n = n;
+  p->n_total = n_total;
+  p->col0 = col0;
+  p->m_pad = round_up(m, 128);
+  p->n_pad = round_up(n, 64);
+  p->ldx = p->n_pad;
+  p->ldm = round_up(ceil_div(p->n_pad, 32), 2);
+  p->masked = mask != nullptr;
+  p->lambda_l = lambda_l;
+  p->lambda_s = lambda_s;
+  p->stream = reinterpret_cast<cudaStream_t>(stream);
+  p->stored = store & 3u;
+  auto bail = [&](int rc) {
+    spcp_problem_destroy(p);
+    return rc;
+  };
+  int rc;
+  const size_t xe = size_t(p->m_pad) * p->ldx;
+  if (store & SPCP_STORE_F32) {
+    if ((rc = p->x32.ensure(xe * sizeof(float)))) return bail(rc);
+    if (cudaMemsetAsync(p->x32.ptr, 0, xe * sizeof(float), p->stream) != cudaSuccess)
+      return bail(cuda_fail(cudaGetLastError(), "memset x32"));
+  }
+  if (store & SPCP_STORE_F64) {
+    if ((rc = p->x64.ensure(xe * sizeof(double)))) return bail(rc);
+    if (cudaMemsetAsync(p->x64.ptr, 0, xe * sizeof(double), p->stream) != cudaSuccess)
+      return bail(cuda_fail(cudaGetLastError(), "memset x64"));
+  }
+  if (p->masked) {
+    const size_t mb = size_t(p->m_pad) * p->ldm * sizeof(uint32_t);
+    if ((rc = p->mbits.ensure(mb))) return bail(rc);
+    if (cudaMemsetAsync(p->mbits.ptr, 0, mb, p->stream) != cudaSuccess)
+      return bail(cuda_fail(cudaGetLastError(), "memset mask"));
+  }
+  // upload in row chunks of <= 256 MiB of source
+  const size_t esz = x_dtype == SPCP_F64 ? 8 : 4;
+  int64_t chunk_rows = std::max<int64_t>(1, int64_t((size_t(256) << 20) / (size_t(n) * esz)));
+  chunk_rows = std::min(chunk_rows, m);
+  DevBuf stage, mstage, parts;
+  const int nblk = 296;
+  if ((rc = parts.ensure(2 * nblk * sizeof(double)))) return bail(rc);
+  if (cudaMemsetAsync(parts.ptr, 0, 2 * nblk * sizeof(double), p->stream) != cudaSuccess)
+    return bail(cuda_fail(cudaGetLastError(), "memset parts"));
+  if (!x_on_device && (rc = stage.ensure(size_t(chunk_rows) * n * esz))) return bail(rc);
+  if (p->masked && (rc = mstage.ensure(size_t(chunk_rows) * n))) return bail(rc);
+  for (int64_t r0 = 0; r0 < m; r0 += chunk_rows) {
+    const int64_t rows = std::min(chunk_rows, m - r0);
+    const void* src;
+    int64_t lds;
+    if (x_on_device) {
+      src = static_cast<const char*>(x) + size_t(r0) * ldx * esz;
+      lds = ldx;
+    } else {
+      cudaError_t e = cudaMemcpy2DAsync(stage.ptr, n * esz,
+                                        static_cast<const char*>(x) + size_t(r0) * ldx * esz,
+                                        ldx * esz, n * esz, rows, cudaMemcpyHostToDevice,
+                                        p->stream);
+      if (e != cudaSuccess) return bail(cuda_fail(e, "upload X"));
+      src = stage.ptr;
+      lds = n;
+    }
+    const uint8_t* mrows = nullptr;
+    if (p->masked) {
+      cudaError_t e = cudaMemcpyAsync(mstage.ptr, mask + size_t(r0) * n, size_t(rows) * n,
+                                      cudaMemcpyHostToDevice, p->stream);
+      if (e != cudaSuccess) return bail(cuda_fail(e, "upload mask"));
+      mrows = mstage.as<uint8_t>();
+      pack_mask_kernel<<<grid_for(rows * ceil_div(n, 32)), 256, 0, p->stream>>>(
+          mrows, rows, n, r0, p->mbits.as<uint32_t>(), p->ldm);
+    }
+    double* psq = parts.as<double>();
+    if (x_dtype == SPCP_F64)
+      convert_x_kernel<double><<<nblk, 256, 0, p->stream>>>(
+          static_cast<const double*>(src), lds, rows, n, r0, p->x32.as<float>(),
+          p->x64.as<double>(), p->ldx, mrows, psq, psq + nblk);
+    else
+      convert_x_kernel<float><<<nblk, 256, 0, p->stream>>>(
+          static_cast<const float*>(src), lds, rows, n, r0, p->x32.as<float>(),
+          p->x64.as<double>(), p->ldx, mrows, psq, psq + nblk);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return bail(cuda_fail(e, "convert_x"));
+    // stage buffers are reused next chunk: serialise
+    e = cudaStreamSynchronize(p->stream);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "upload sync"));
+  }
+  {
+    DevBuf res;
+    if ((rc = res.ensure(2 * sizeof(double)))) return bail(rc);
+    sum_partials_kernel<<<1, 256, 0, p->stream>>>(parts.as<double>(), nblk, res.as<double>());
+    sum_partials_kernel<<<1, 256, 0, p->stream>>>(parts.as<double>() + nblk, nblk,
+                                                  res.as<double>() + 1);
+    double h[2];
+    cudaError_t e = cudaMemcpyAsync(h, res.ptr, 2 * sizeof(double), cudaMemcpyDeviceToHost,
+                                    p->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "f_zero"));
+    p->f_zero = h[0];
+    p->n_obs = h[1];
+  }
+  SPCP_CUDA(cudaEventCreate(&p->ev0));
+  SPCP_CUDA(cudaEventCreate(&p->ev1));
+  *out = p;
+  return SPCP_OK;
+}
+
+int spcp_problem_destroy(spcp_problem* p) {
+  if (!p) return SPCP_OK;
+  cudaSetDevice(p->device);
+  if (p->stream) cudaStreamSynchronize(p->stream);
+  for (DevBuf* b : {&p->x32, &p->x64, &p->mbits, &p->uc, &p->vc, &p->wr, &p->wl, &p->pleft,
+                    &p->pright, &p->pphi, &p->blk, &p->out_dev, &p->counter, &p->scratch,
+                    &p->scal, &p->gu_tmp, &p->vec_part, &p->small})
+    b->release();
+  if (p->host_out) cudaFreeHost(p->host_out);
+  if (p->ev0) cudaEventDestroy(p->ev0);
+  if (p->ev1) cudaEventDestroy(p->ev1);
+  delete p;
+  return SPCP_OK;
+}
+
+int spcp_problem_set_stream(spcp_problem* p, void* stream) {
+  p->stream = reinterpret_cast<cudaStream_t>(stream);
+  return SPCP_OK;
+}
+
+int spcp_problem_info(spcp_problem* p, double* info) {
+  info[0] = p->f_zero;
+  info[1] = p->n_obs;
+  info[2] = double(p->stored);
+  info[3] = double(p->x32.bytes + p->x64.bytes + p->mbits.bytes);
+  return SPCP_OK;
+}
+
+static int eval_impl(spcp_problem* p, int64_t k, int dtype, const double* z, const double* dz,
+                     double alpha, double* g_out, int u_mode, void* gu_part, double* scal) {
+  int rc;
+  if ((rc = check_k(p, k))) return rc;
+  if (dtype != SPCP_F32 && dtype != SPCP_F64) return fail(SPCP_ERR_VALUE, "bad compute dtype");
+  SPCP_CUDA(cudaSetDevice(p->device));
+  int kp = 0, pdt = SPCP_F64;
+  LaunchShape sh;
+  if ((rc = run_stream_eval(p, k, dtype, z, dz, alpha, kp, sh, pdt))) return rc;
+  const bool dense = (kp == 0);
+  if (dense) kp = int(round_up(k, 2));
+  p->ev_pending = p->prof && !dense;
+  return run_reduce(p, k, kp, pdt, sh, dense, z, dz, alpha, u_mode, 1, nullptr, gu_part,
+                    nullptr, scal, g_out);
+}
+
+int spcp_eval(spcp_problem* p, int64_t k, int dtype, const double* z, const double* dz,
+              double alpha, double* g_out, double* out) {
+  int rc = eval_impl(p, k, dtype, z, dz, alpha, g_out, U_FULL, nullptr, nullptr);
+  if (rc) return rc;
+  return fetch_out(p, out);
+}
+
+int spcp_eval_partial(spcp_problem* p, int64_t k, int dtype, const double* z, const double* dz,
+                      double alpha, void* gu_part, double* scal, double* g_out) {
+  return eval_impl(p, k, dtype, z, dz, alpha, g_out, U_PARTIAL, gu_part, scal);
+}
+
+int spcp_eval_finish(spcp_problem* p, int64_t k, int dtype, const double* z, const double* dz,
+                     double alpha, const void* gu_sum, const double* scal_sum, double* g_out,
+                     double* out) {
+  int rc;
+  if ((rc = check_k(p, k))) return rc;
+  SPCP_CUDA(cudaSetDevice(p->device));
+  LaunchShape sh;
+  const int pdt = (dtype == SPCP_F32 && eval_kp(SPCP_F32, k) != 0) ? SPCP_F32 : SPCP_F64;
+  if ((rc = run_reduce(p, k, int(round_up(k, 2)), pdt, sh, false, z, dz, alpha, U_FROM_SUM, 0,
+                       gu_sum, nullptr, scal_sum, nullptr, g_out)))
+    return rc;
+  return fetch_out(p, out);
+}
+
+int spcp_split_objective_host(spcp_problem* p, int64_t k, int dtype, const double* u,
+                              const double* v, double* value, double* grad_u, double* grad_v) {
+  int rc;
+  if ((rc = check_k(p, k))) return rc;
+  SPCP_CUDA(cudaSetDevice(p->device));
+  const int64_t nu = p->m * k, nv = p->n * k;
+  if ((rc = p->scratch.ensure(size_t(nu + nv) * 2 * sizeof(double)))) return rc;
+  double* z = p->scratch.as<double>();
+  double* g = z + nu + nv;
+  SPCP_CUDA(cudaMemcpyAsync(z, u, size_t(nu) * sizeof(double), cudaMemcpyHostToDevice, p->stream));
+  SPCP_CUDA(cudaMemcpyAsync(z + nu, v, size_t(nv) * sizeof(double), cudaMemcpyHostToDevice,
+                            p->stream));
+  double out[8];
+  if (eval_kp(dtype, k) == 0) {
+    // dense fallback uses `scratch` itself: stage z elsewhere
+    if ((rc = p->vec_part.ensure(size_t(nu + nv) * 2 * sizeof(double)))) return rc;
+    double* z2 = p->vec_part.as<double>();
+    SPCP_CUDA(cudaMemcpyAsync(z2, z, size_t(nu + nv) * sizeof(double), cudaMemcpyDeviceToDevice,
+                              p->stream));
+    z = z2;
+    g = z2 + nu + nv;
+  }
+  if ((rc = spcp_eval(p, k, dtype, z, nullptr, 0.0, g, out))) return rc;
+  *value = out[0];
+  if (grad_u)
+    SPCP_CUDA(cudaMemcpyAsync(grad_u, g, size_t(nu) * sizeof(double), cudaMemcpyDeviceToHost,
+                              p->stream));
+  if (grad_v)
+    SPCP_CUDA(cudaMemcpyAsync(grad_v, g + nu, size_t(nv) * sizeof(double),
+                              cudaMemcpyDeviceToHost, p->stream));
+  SPCP_CUDA(cudaStreamSynchronize(p->stream));
+  return SPCP_OK;
+}
+
+int spcp_phi_dense_host(spcp_problem* p, const double* l, double* value, double* grad,
+                        double* s_star) {
+  int rc;
+  SPCP_CUDA(cudaSetDevice(p->device));
+  const int64_t mn = p->m * p->n;
+  const int nblk = grid_for(mn, 256, 148 * 8);
+  if ((rc = p->scratch.ensure(size_t(mn) * 3 * sizeof(double) + size_t(nblk) * sizeof(double))))
+    return rc;
+  double* dl = p->scratch.as<double>();
+  double* dg = dl + mn;
+  double* ds = dg + mn;
+  double* part = ds + mn;
+  SPCP_CUDA(cudaMemcpyAsync(dl, l, size_t(mn) * sizeof(double), cudaMemcpyHostToDevice, p->stream));
+  const uint32_t* mb = p->masked ? p->mbits.as<uint32_t>() : nullptr;
+  if (p->x64.ptr)
+    phi_dense_kernel<double><<<nblk, 256, 0, p->stream>>>(dl, p->m, p->n, p->x64.as<double>(),
+                                                          p->ldx, mb, p->ldm, p->lambda_s, dg,
+                                                          ds, part);
+  else
+    phi_dense_kernel<float><<<nblk, 256, 0, p->stream>>>(dl, p->m, p->n, p->x32.as<float>(),
+                                                         p->ldx, mb, p->ldm, p->lambda_s, dg, ds,
+                                                         part);
+  SPCP_CHECK_LAUNCH("phi_dense");
+  p->launches++;
+  if ((rc = ensure_common(p))) return rc;
+  sum_partials_kernel<<<1, 256, 0, p->stream>>>(part, nblk, p->out_dev.as<double>());
+  p->launches++;
+  SPCP_CUDA(cudaMemcpyAsync(p->host_out, p->out_dev.ptr, sizeof(double), cudaMemcpyDeviceToHost,
+                            p->stream));
+  if (grad)
+    SPCP_CUDA(cudaMemcpyAsync(grad, dg, size_t(mn) * sizeof(double), cudaMemcpyDeviceToHost,
+                              p->stream));
+  if (s_star)
+    SPCP_CUDA(cudaMemcpyAsync(s_star, ds, size_t(mn) * sizeof(double), cudaMemcpyDeviceToHost,
+                              p->stream));
+  SPCP_CUDA(cudaStreamSynchronize(p->stream));
+  *value = p->host_out[0];
+  return SPCP_OK;
+}
+
+int spcp_apply(spcp_problem* p, int64_t k, const double* z, int64_t b, const double* w_right,
+               double* left_out, const double* w_left, double* right_out) {
+  int rc;
+  if (k < 0 || b < 1) return fail(SPCP_ERR_DIMENSION, "bad apply shape");
+  SPCP_CUDA(cudaSetDevice(p->device));
+  const bool x64 = p->x64.ptr != nullptr;
+  int kr = apply_kr(k);
+  // residual operands (float64)
+  if (kr > 0) {
+    if ((rc = prep<double>(p, k, kr, z, nullptr, 0.0))) return rc;
+  } else if (kr < 0) {
+    // large rank bound: materialise G once, then RAW products over it
+    const int64_t len = (p->m + p->n) * k;
+    (void)len;
+    if ((rc = p->gu_tmp.ensure(size_t(p->m_pad) * p->ldx * sizeof(double)))) return rc;
+    double* gmat = p->gu_tmp.as<double>();
+    SPCP_CUDA(cudaMemsetAsync(gmat, 0, size_t(p->m_pad) * p->ldx * sizeof(double), p->stream));
+    const int64_t nbx = ceil_div(p->n, 64), nby = ceil_div(p->m, 64);
+    if ((rc = p->pphi.ensure(size_t(nbx * nby) * sizeof(double)))) return rc;
+    rc = x64 ? launch_dense<double>(p, 1, k, z, 0, p->m, gmat, nullptr, p->ldx, p->pphi.as<double>())
+             : launch_dense<float>(p, 1, k, z, 0, p->m, gmat, nullptr, p->ldx, p->pphi.as<double>());
+    if (rc) return rc;
+  }
+  for (int64_t c0 = 0; c0 < b; c0 += 32) {
+    const int64_t bw = std::min<int64_t>(32, b - c0);
+    const int pw = bw <= 8 ? 8 : 32;
+    if (w_right) {
+      if ((rc = p->wr.ensure(size_t(p->n_pad) * pw * sizeof(double)))) return rc;
+      SPCP_CUDA(cudaMemsetAsync(p->wr.ptr, 0, size_t(p->n_pad) * pw * sizeof(double), p->stream));
+      SPCP_CUDA(cudaMemcpy2DAsync(p->wr.ptr, pw * sizeof(double), w_right + c0, b * sizeof(double),
+                                  bw * sizeof(double), p->n, cudaMemcpyDeviceToDevice, p->stream));
+    }
+    if (w_left) {
+      if ((rc = p->wl.ensure(size_t(p->m_pad) * pw * sizeof(double)))) return rc;
+      SPCP_CUDA(cudaMemsetAsync(p->wl.ptr, 0, size_t(p->m_pad) * pw * sizeof(double), p->stream));
+      SPCP_CUDA(cudaMemcpy2DAsync(p->wl.ptr, pw * sizeof(double), w_left + c0, b * sizeof(double),
+                                  bw * sizeof(double), p->m, cudaMemcpyDeviceToDevice, p->stream));
+    }
+    StreamParams sp{};
+    sp.m_pad = p->m_pad;
+    sp.n_pad = p->n_pad;
+    sp.ldx = p->ldx;
+    sp.ldm = p->ldm;
+    sp.tau = p->lambda_s;
+    sp.uc = p->uc.ptr;
+    sp.vc = p->vc.ptr;
+    sp.wr = p->wr.ptr;
+    sp.wl = p->wl.ptr;
+    sp.do_left = w_right != nullptr;
+    sp.do_right = w_left != nullptr;
+    LaunchShape sh;
+    if (kr < 0) {
+      sp.x = p->gu_tmp.ptr;
+      sp.mbits = nullptr;
+      rc = pw == 8 ? launch_stream<double, double, 0, 8, MODE_RAW, false>(p, sp, sh, false)
+                   : launch_stream<double, double, 0, 32, MODE_RAW, false>(p, sp, sh, false);
+    } else {
+      sp.x = x64 ? p->x64.ptr : p->x32.ptr;
+      sp.mbits = p->masked ? p->mbits.as<uint32_t>() : nullptr;
+      if (x64)
+        rc = p->masked ? dispatch_apply<double, true>(p, kr, pw, sp, sh)
+                       : dispatch_apply<double, false>(p, kr, pw, sp, sh);
+      else
+        rc = p->masked ? dispatch_apply<float, true>(p, kr, pw, sp, sh)
+                       : dispatch_apply<float, false>(p, kr, pw, sp, sh);
+    }
+    if (rc) return rc;
+    if ((rc = p->small.ensure(size_t(std::max(p->m, p->n)) * 32 * sizeof(double)))) return rc;
+    if (w_right) {
+      reduce_apply_kernel<double><<<grid_for(p->m * bw), 256, 0, p->stream>>>(
+          p->pleft.as<double>(), sh.nchunks, p->m, p->m_pad, pw, bw, p->small.as<double>());
+      SPCP_CHECK_LAUNCH("reduce_apply");
+      p->launches++;
+      SPCP_CUDA(cudaMemcpy2DAsync(left_out + c0, b * sizeof(double), p->small.ptr,
+                                  bw * sizeof(double), bw * sizeof(double), p->m,
+                                  cudaMemcpyDeviceToDevice, p->stream));
+    }
+    if (w_left) {
+      reduce_apply_kernel<double><<<grid_for(p->n * bw), 256, 0, p->stream>>>(
+          p->pright.as<double>(), sh.nrb, p->n, p->n_pad, pw, bw, p->small.as<double>());
+      SPCP_CHECK_LAUNCH("reduce_apply");
+      p->launches++;
+      SPCP_CUDA(cudaMemcpy2DAsync(right_out + c0, b * sizeof(double), p->small.ptr,
+                                  bw * sizeof(double), bw * sizeof(double), p->n,
+                                  cudaMemcpyDeviceToDevice, p->stream));
+    }
+  }
+  SPCP_CUDA(cudaStreamSynchronize(p->stream));
+  return SPCP_OK;
+}
+
+int spcp_materialize(spcp_problem* p, int64_t k, const double* z, int64_t row0, int64_t rows,
+                     double* l_out, double* s_out, int out_on_host) {
+  int rc;
+  if (row0 < 0 || rows < 0 || row0 + rows > p->m) return fail(SPCP_ERR_DIMENSION, "bad row range");
+  SPCP_CUDA(cudaSetDevice(p->device));
+  const bool x64 = p->x64.ptr != nullptr;
+  int64_t step = rows;
+  if (out_on_host) {
+    step = std::max<int64_t>(1, int64_t((size_t(128) << 20) / (size_t(p->n) * 8)));
+    if ((rc = p->gu_tmp.ensure(size_t(step) * p->n * 2 * sizeof(double)))) return rc;
+  }
+  for (int64_t r = row0; r < row0 + rows; r += step) {
+    const int64_t nr = std::min(step, row0 + rows - r);
+    double* lo = l_out ? (out_on_host ? p->gu_tmp.as<double>() : l_out + (r - row0) * p->n) : nullptr;
+    double* so = s_out ? (out_on_host ? p->gu_tmp.as<double>() + step * p->n
+                                      : s_out + (r - row0) * p->n)
+                       : nullptr;
+    rc = x64 ? launch_dense<double>(p, 0, k, z, r, nr, lo, so, p->n, nullptr)
+             : launch_dense<float>(p, 0, k, z, r, nr, lo, so, p->n, nullptr);
+    if (rc) return rc;
+    if (out_on_host) {
+      if (l_out)
+        SPCP_CUDA(cudaMemcpyAsync(l_out + (r - row0) * p->n, lo, size_t(nr) * p->n * 8,
+                                  cudaMemcpyDeviceToHost, p->stream));
+      if (s_out)
+        SPCP_CUDA(cudaMemcpyAsync(s_out + (r - row0) * p->n, so, size_t(nr) * p->n * 8,
+                                  cudaMemcpyDeviceToHost, p->stream));
+      SPCP_CUDA(cudaStreamSynchronize(p->stream));
+    }
+  }
+  SPCP_CUDA(cudaStreamSynchronize(p->stream));
+  return SPCP_OK;
+}
+
+int spcp_materialize_grad(spcp_problem* p, int64_t k, const double* z, double* g_out,
+                          int64_t ldo) {
+  int rc;
+  if (k < 1) return fail(SPCP_ERR_DIMENSION, "k must be >= 1");
+  if (ldo < p->n) return fail(SPCP_ERR_DIMENSION, "ldo < n");
+  SPCP_CUDA(cudaSetDevice(p->device));
+  const int64_t nbx = ceil_div(p->n, 64), nby = ceil_div(p->m, 64);
+  if ((rc = p->pphi.ensure(size_t(nbx * nby) * sizeof(double)))) return rc;
+  rc = p->x64.ptr ? launch_dense<double>(p, 1, k, z, 0, p->m, g_out, nullptr, ldo,
+                                         p->pphi.as<double>())
+                  : launch_dense<float>(p, 1, k, z, 0, p->m, g_out, nullptr, ldo,
+                                        p->pphi.as<double>());
+  if (rc) return rc;
+  SPCP_CUDA(cudaStreamSynchronize(p->stream));
+  return SPCP_OK;
+}
+
+int spcp_vec_multidot(spcp_problem* p, int64_t len, int count, const double* const* a,
+                      const double* const* b, double* out_host) {
+  int rc;
+  SPCP_CUDA(cudaSetDevice(p->device));
+  if ((rc = ensure_common(p))) return rc;
+  const int nblk = grid_for(len, 256, 148 * 2);
+  for (int c0 = 0; c0 < count; c0 += kMaxVec) {
+    const int cnt = std::min(kMaxVec, count - c0);
+    VecPtrs vp{};
+    for (int i = 0; i < cnt; ++i) {
+      vp.a[i] = a[c0 + i];
+      vp.b[i] = b[c0 + i];
+    }
+    if ((rc = p->vec_part.ensure(size_t(cnt) * nblk * sizeof(double) + 64 * sizeof(double))))
+      return rc;
+    double* part = p->vec_part.as<double>();
+    multidot_kernel<<<dim3(nblk, cnt), 256, 0, p->stream>>>(vp, len, part, nblk);
+    SPCP_CHECK_LAUNCH("multidot");
+    fold_kernel<<<cnt, 256, 0, p->stream>>>(part, nblk, p->out_dev.as<double>());
+    SPCP_CHECK_LAUNCH("fold");
+    p->launches += 2;
+    SPCP_CUDA(cudaMemcpyAsync(p->host_out, p->out_dev.ptr, cnt * sizeof(double),
+                              cudaMemcpyDeviceToHost, p->stream));
+    SPCP_CUDA(cudaStreamSynchronize(p->stream));
+    std::memcpy(out_host + c0, p->host_out, cnt * sizeof(double));
+  }
+  return SPCP_OK;
+}
+
+int spcp_vec_lincomb(spcp_problem* p, int64_t len, int count, const double* coef,
+                     const double* const* v, double* out) {
+  SPCP_CUDA(cudaSetDevice(p->device));
+  if (count < 1) return fail(SPCP_ERR_VALUE, "lincomb needs >= 1 vector");
+  if (count > kMaxVec) return fail(SPCP_ERR_VALUE, "lincomb: too many vectors");
+  VecPtrs vp{};
+  for (int i = 0; i < count; ++i) {
+    vp.a[i] = v[i];
+    vp.coef[i] = coef[i];
+  }
+  lincomb_kernel<<<grid_for(len), 256, 0, p->stream>>>(vp, count, len, out);
+  SPCP_CHECK_LAUNCH("lincomb");
+  p->launches++;
+  return SPCP_OK;
+}
+
+int spcp_vec_gram(spcp_problem* p, int64_t len, int na, const double* const* a, int nb,
+                  const double* const* b, double* out_host) {
+  int rc;
+  SPCP_CUDA(cudaSetDevice(p->device));
+  if (nb < 1 || nb > 4 || na < 1) return fail(SPCP_ERR_VALUE, "vec_gram: need 1<=nb<=4, na>=1");
+  if ((rc = ensure_common(p))) return rc;
+  const int nblk = grid_for(len, 256, 148 * 2);
+  for (int a0 = 0; a0 < na; a0 += kGramNA) {
+    const int cnt = std::min(kGramNA, na - a0);
+    GramPtrs gp{};
+    for (int i = 0; i < cnt; ++i) gp.a[i] = a[a0 + i];
+    for (int j = 0; j < nb; ++j) gp.b[j] = b[j];
+    if ((rc = p->vec_part.ensure(size_t(nblk) * kGramNA * 4 * sizeof(double)))) return rc;
+    double* part = p->vec_part.as<double>();
+    switch (nb) {
+      case 1: vec_gram_kernel<1><<<nblk, 256, 0, p->stream>>>(gp, cnt, len, part); break;
+      case 2: vec_gram_kernel<2><<<nblk, 256, 0, p->stream>>>(gp, cnt, len, part); break;
+      case 3: vec_gram_kernel<3><<<nblk, 256, 0, p->stream>>>(gp, cnt, len, part); break;
+      default: vec_gram_kernel<4><<<nblk, 256, 0, p->stream>>>(gp, cnt, len, part); break;
+    }
+    SPCP_CHECK_LAUNCH("vec_gram");
+    vec_gram_fold_kernel<<<1, 256, 0, p->stream>>>(part, nblk, cnt, nb, p->out_dev.as<double>());
+    SPCP_CHECK_LAUNCH("vec_gram_fold");
+    p->launches += 2;
+    SPCP_CUDA(cudaMemcpyAsync(p->host_out, p->out_dev.ptr, size_t(cnt) * nb * sizeof(double),
+                              cudaMemcpyDeviceToHost, p->stream));
+    SPCP_CUDA(cudaStreamSynchronize(p->stream));
+    std::memcpy(out_host + size_t(a0) * nb, p->host_out, size_t(cnt) * nb * sizeof(double));
+  }
+  return SPCP_OK;
+}
+
+int spcp_gram(spcp_problem* p, int64_t rows, int64_t pa, const double* a, int64_t qb,
+              const double* b, double* out_host) {
+  int rc;
+  SPCP_CUDA(cudaSetDevice(p->device));
+  const int64_t rpb = std::max<int64_t>(256, round_up(ceil_div(rows, 296), 32));
+  const int64_t nrb = std::max<int64_t>(1, ceil_div(rows, rpb));
+  const int64_t pq = pa * qb;
+  if ((rc = p->vec_part.ensure(size_t(nrb * pq + pq) * sizeof(double)))) return rc;
+  double* part = p->vec_part.as<double>();
+  double* res = part + nrb * pq;
+  dim3 grid(unsigned(nrb), unsigned(ceil_div(pa, 32)), unsigned(ceil_div(qb, 32)));
+  gram_kernel<<<grid, 256, 0, p->stream>>>(a, pa, b, qb, rows, rpb, part);
+  SPCP_CHECK_LAUNCH("gram");
+  gram_fold_kernel<<<grid_for(pq), 256, 0, p->stream>>>(part, int(nrb), pq, res);
+  SPCP_CHECK_LAUNCH("gram_fold");
+  p->launches += 2;
+  SPCP_CUDA(cudaMemcpyAsync(out_host, res, size_t(pq) * sizeof(double), cudaMemcpyDeviceToHost,
+                            p->stream));
+  SPCP_CUDA(cudaStreamSynchronize(p->stream));
+  return SPCP_OK;
+}
+
+int spcp_matmul_small(spcp_problem* p, int64_t rows, int64_t pa, const double* a, int64_t qb,
+                      const double* m_host, double* c) {
+  int rc;
+  SPCP_CUDA(cudaSetDevice(p->device));
+  if ((rc = p->small.ensure(std::max(p->small.bytes, size_t(pa * qb) * sizeof(double))))) return rc;
+  DevBuf mm;
+  if ((rc = mm.ensure(size_t(pa * qb) * sizeof(double)))) return rc;
+  SPCP_CUDA(cudaMemcpyAsync(mm.ptr, m_host, size_t(pa * qb) * sizeof(double),
+                            cudaMemcpyHostToDevice, p->stream));
+  matmul_small_kernel<<<grid_for(rows * qb), 256, 0, p->stream>>>(a, rows, pa, mm.as<double>(), qb,
+                                                                   c);
+  SPCP_CHECK_LAUNCH("matmul_small");
+  p->launches++;
+  SPCP_CUDA(cudaStreamSynchronize(p->stream));
+  mm.release();
+  return SPCP_OK;
+}
+
+int spcp_prof_enable(spcp_problem* p, int on) {
+  p->prof = on != 0;
+  p->prof_ms = 0.0;
+  p->prof_count = 0;
+  p->ev_pending = false;
+  return SPCP_OK;
+}
+
+int spcp_prof_read(spcp_problem* p, double* ms_total, int64_t* launches, int64_t* kernels) {
+  *ms_total = p->prof_ms;
+  *launches = p->prof_count;
+  *kernels = p->launches;
+  p->prof_ms = 0.0;
+  p->prof_count = 0;
+  p->launches = 0;
+  return SPCP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,270 @@
+"""Device-resident problem (the GPU side of ProblemSpec, objective.py:20-59).
+
+`DeviceProblem` owns one `spcp_problem` handle of libspcp_b200.so: the padded
+fp32/fp64 copies of X in HBM, the bit-packed observation mask and the
+workspaces of the fused streaming kernel.  Device vectors are torch CUDA
+tensors (torch is plumbing here: allocation, streams, torch.distributed); all
+arithmetic on m x n data runs in this repo's sm_100a kernels.
+"""
+
+import ctypes
+
+import numpy as np
+
+from ._lib import SPCP_F32, SPCP_F64, STORE_F32, STORE_F64, check, lib
+
+__all__ = ["DeviceProblem", "torch_mod", "cuda_device", "dptr", "PRECISIONS"]
+
+PRECISIONS = ("fp32", "fp64", "mixed")
+
+_torch = None
+
+
+def torch_mod():
+    global _torch
+    if _torch is None:
+        import torch
+
+        _torch = torch
+    return _torch
+
+
+def cuda_device():
+    torch = torch_mod()
+    if not torch.cuda.is_available():
+        from .errors import DeviceError
+
+        raise DeviceError("no CUDA device: the Split-SPCP compute path runs only on the GPU "
+                          "(sm_100a); there is no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def dptr(t):
+    """Raw device pointer of a torch tensor (None -> NULL)."""
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _ptr_array(ts):
+    arr = (ctypes.c_void_p * len(ts))()
+    for i, t in enumerate(ts):
+        arr[i] = t.data_ptr()
+    return arr
+
+
+class DeviceProblem:
+    """One column shard (or the whole matrix) of X resident on a GPU.
+
+    x: host numpy array (float64 or float32) or a CUDA tensor, m x n.
+    store: iterable of "f32" / "f64": which device copies to keep.
+    n_total, col0: column-sharded mode.
+    """
+
+    def __init__(self, x, lambda_l, lambda_s, mask=None, store=("f32",), n_total=None,
+                 col0=0):
+        torch = torch_mod()
+        self.device = cuda_device()
+        self.stream = torch.cuda.current_stream(self.device)
+        on_dev = isinstance(x, torch.Tensor)
+        if on_dev:
+            xt = x if x.is_contiguous() else x.contiguous()
+            m, n = xt.shape
+            dt = SPCP_F64 if xt.dtype == torch.float64 else SPCP_F32
+            if xt.dtype not in (torch.float32, torch.float64):
+                raise ValueError("device X must be float32 or float64")
+            xptr, ldx = ctypes.c_void_p(xt.data_ptr()), n
+        else:
+            xa = np.asarray(x)
+            if xa.dtype not in (np.float32, np.float64):
+                xa = xa.astype(np.float64)
+            xa = np.ascontiguousarray(xa)
+            m, n = xa.shape
+            dt = SPCP_F64 if xa.dtype == np.float64 else SPCP_F32
+            xptr, ldx = ctypes.c_void_p(xa.ctypes.data), n
+            self._keep = xa
+        mptr = None
+        if mask is not None:
+            mk = np.ascontiguousarray(mask, dtype=np.bool_)
+            mptr = ctypes.c_void_p(mk.ctypes.data)
+            self._keep_mask = mk
+        flags = 0
+        for s in store:
+            flags |= STORE_F32 if s == "f32" else STORE_F64
+        self.m, self.n = int(m), int(n)
+        self.n_total = int(n_total if n_total is not None else n)
+        self.col0 = int(col0)
+        self.lambda_l, self.lambda_s = float(lambda_l), float(lambda_s)
+        self.masked = mask is not None
+        self.store = frozenset(store)
+        h = ctypes.c_void_p()
+        check(lib.spcp_problem_create(ctypes.byref(h), self.device.index, self.m, self.n, xptr,
+                                      ldx, dt, int(on_dev), mptr, flags, self.lambda_l,
+                                      self.lambda_s, self.n_total, self.col0,
+                                      ctypes.c_void_p(self.stream.cuda_stream)))
+        self.handle = h
+        self._keep = None
+        self._keep_mask = None
+        info = (ctypes.c_double * 4)()
+        check(lib.spcp_problem_info(self.handle, info))
+        self.f_zero = float(info[0])
+        self.n_obs = float(info[1])
+        self._out = (ctypes.c_double * 8)()
+
+    # ------------------------------------------------------------ lifecycle
+    def close(self):
+        if getattr(self, "handle", None):
+            lib.spcp_problem_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------ helpers
+    def empty(self, n, dtype=None):
+        torch = torch_mod()
+        return torch.empty(int(n), dtype=dtype or torch.float64, device=self.device)
+
+    def zeros(self, n, dtype=None):
+        torch = torch_mod()
+        return torch.zeros(int(n), dtype=dtype or torch.float64, device=self.device)
+
+    @staticmethod
+    def dtype_code(precision):
+        return SPCP_F32 if precision == "fp32" else SPCP_F64
+
+    # ------------------------------------------------------------ evaluation
+    def eval(self, k, dtype, z, dz, alpha, g_out):
+        """F and grad F at z + alpha*dz -> np.array([f, phi, reg, g.dz, |g|^2, |gU|^2,
+        gU.dzU, 0]); g_out (device float64) receives the gradient."""
+        check(lib.spcp_eval(self.handle, int(k), int(dtype), dptr(z), dptr(dz), float(alpha),
+                            dptr(g_out), self._out))
+        return np.frombuffer(self._out, dtype=np.float64).copy()
+
+    def eval_partial(self, k, dtype, z, dz, alpha, gu_part, scal, g_out):
+        check(lib.spcp_eval_partial(self.handle, int(k), int(dtype), dptr(z), dptr(dz),
+                                    float(alpha), dptr(gu_part), dptr(scal), dptr(g_out)))
+
+    def eval_finish(self, k, dtype, z, dz, alpha, gu_sum, scal_sum, g_out):
+        check(lib.spcp_eval_finish(self.handle, int(k), int(dtype), dptr(z), dptr(dz),
+                                   float(alpha), dptr(gu_sum), dptr(scal_sum), dptr(g_out),
+                                   self._out))
+        return np.frombuffer(self._out, dtype=np.float64).copy()
+
+    def split_objective_host(self, u, v, dtype):
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        k = u.shape[1]
+        gu = np.empty_like(u)
+        gv = np.empty_like(v)
+        val = ctypes.c_double()
+        check(lib.spcp_split_objective_host(self.handle, k, int(dtype),
+                                            ctypes.c_void_p(u.ctypes.data),
+                                            ctypes.c_void_p(v.ctypes.data), ctypes.byref(val),
+                                            ctypes.c_void_p(gu.ctypes.data),
+                                            ctypes.c_void_p(gv.ctypes.data)))
+        return float(val.value), gu, gv
+
+    def phi_dense_host(self, l, want_grad=True, want_s=True):
+        l = np.ascontiguousarray(l, dtype=np.float64)
+        g = np.empty_like(l) if want_grad else None
+        s = np.empty_like(l) if want_s else None
+        val = ctypes.c_double()
+        check(lib.spcp_phi_dense_host(self.handle, ctypes.c_void_p(l.ctypes.data),
+                                      ctypes.byref(val),
+                                      None if g is None else ctypes.c_void_p(g.ctypes.data),
+                                      None if s is None else ctypes.c_void_p(s.ctypes.data)))
+        return float(val.value), g, s
+
+    # ------------------------------------------------------------ operators
+    def apply(self, k, z, w_right=None, w_left=None):
+        """(G @ w_right, G^T @ w_left) as float64 device matrices; G = grad phi at
+        U V^T (k >= 1) or the zero-filled observed X (k == 0)."""
+        torch = torch_mod()
+        b = int((w_right if w_right is not None else w_left).shape[1])
+        left = right = None
+        if w_right is not None:
+            w_right = w_right.contiguous()
+            left = torch.empty((self.m, b), dtype=torch.float64, device=self.device)
+        if w_left is not None:
+            w_left = w_left.contiguous()
+            right = torch.empty((self.n, b), dtype=torch.float64, device=self.device)
+        check(lib.spcp_apply(self.handle, int(k), dptr(z), b, dptr(w_right), dptr(left),
+                             dptr(w_left), dptr(right)))
+        return left, right
+
+    def materialize(self, k, z, row0=0, rows=None, want_l=True, want_s=True):
+        rows = self.m - row0 if rows is None else rows
+        l = np.empty((rows, self.n)) if want_l else None
+        s = np.empty((rows, self.n)) if want_s else None
+        check(lib.spcp_materialize(self.handle, int(k), dptr(z), int(row0), int(rows),
+                                   None if l is None else ctypes.c_void_p(l.ctypes.data),
+                                   None if s is None else ctypes.c_void_p(s.ctypes.data), 1))
+        return l, s
+
+    def grad_dense(self, k, z):
+        """Dense grad phi(U V^T) as an (m x n) float64 device matrix."""
+        torch = torch_mod()
+        g = torch.empty((self.m, self.n), dtype=torch.float64, device=self.device)
+        check(lib.spcp_materialize_grad(self.handle, int(k), dptr(z), dptr(g), self.n))
+        return g
+
+    # ------------------------------------------------------------ vector algebra
+    def multidot(self, a_list, b_list):
+        cnt = len(a_list)
+        out = (ctypes.c_double * cnt)()
+        length = a_list[0].numel()
+        check(lib.spcp_vec_multidot(self.handle, length, cnt, _ptr_array(a_list),
+                                    _ptr_array(b_list), out))
+        return np.frombuffer(out, dtype=np.float64).copy()
+
+    def vec_gram(self, a_list, b_list):
+        """Host (len(a) x len(b)) matrix of dots, each device vector read once."""
+        na, nb = len(a_list), len(b_list)
+        out = (ctypes.c_double * (na * nb))()
+        check(lib.spcp_vec_gram(self.handle, a_list[0].numel(), na, _ptr_array(a_list), nb,
+                                _ptr_array(b_list), out))
+        return np.frombuffer(out, dtype=np.float64).reshape(na, nb).copy()
+
+    def lincomb(self, coefs, vecs, out):
+        cnt = len(vecs)
+        c = (ctypes.c_double * cnt)(*[float(x) for x in coefs])
+        check(lib.spcp_vec_lincomb(self.handle, out.numel(), cnt, c, _ptr_array(vecs),
+                                   dptr(out)))
+        return out
+
+    def gram(self, a, b):
+        """a^T b for tall float64 device matrices (rows x p), (rows x q) -> host p x q."""
+        a = a.contiguous()
+        b = b.contiguous()
+        rows, pa = a.shape
+        qb = b.shape[1]
+        out = np.empty((pa, qb))
+        check(lib.spcp_gram(self.handle, rows, pa, dptr(a), qb, dptr(b),
+                            out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        return out
+
+    def matmul_small(self, a, mat):
+        """a (rows x p, device) @ mat (p x q, host) -> device rows x q."""
+        torch = torch_mod()
+        a = a.contiguous()
+        rows, pa = a.shape
+        mat = np.ascontiguousarray(mat, dtype=np.float64)
+        qb = mat.shape[1]
+        c = torch.empty((rows, qb), dtype=torch.float64, device=self.device)
+        check(lib.spcp_matmul_small(self.handle, rows, pa, dptr(a), qb,
+                                    mat.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), dptr(c)))
+        return c
+
+    # ------------------------------------------------------------ profiling
+    def prof_enable(self, on=True):
+        check(lib.spcp_prof_enable(self.handle, int(bool(on))))
+
+    def prof_read(self):
+        ms = ctypes.c_double()
+        cnt = ctypes.c_int64()
+        kl = ctypes.c_int64()
+        check(lib.spcp_prof_read(self.handle, ctypes.byref(ms), ctypes.byref(cnt),
+                                 ctypes.byref(kl)))
+        return float(ms.value), int(cnt.value), int(kl.value)

@@ -1,0 +1,209 @@
+"""Generate golden fixtures by running the REAL reference package.
+
+Run in the build container (where `/root/reference` exists):
+
+    python tests/golden/make_golden.py
+
+It imports `spcp` from `/root/reference/pkg/src` (read-only; nothing is
+copied into this repo) and writes `tests/golden/*.npz`.  Those fixtures pin
+the oracle (`oracle/spcp_oracle.py`) and the CUDA path; the GPU box never
+needs `/root/reference`.
+"""
+
+import os
+import sys
+
+import numpy as np
+
+REF_SRC = "/root/reference/pkg/src"
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def _ref():
+    sys.dont_write_bytecode = True
+    if REF_SRC not in sys.path:
+        sys.path.insert(0, REF_SRC)
+    import spcp  # noqa: E402
+
+    return spcp
+
+
+def _records(recs):
+    return (np.array([r.iteration for r in recs], np.int64),
+            np.array([r.objective for r in recs], np.float64),
+            np.array([r.grad_norm for r in recs], np.float64))
+
+
+def gen_phi(spcp):
+    out = {}
+    rng = np.random.default_rng(1234)
+    for tag, masked in (("full", False), ("mask", True)):
+        x = rng.standard_normal((9, 7)) * 2.0
+        mask = rng.random((9, 7)) < 0.7 if masked else None
+        l = rng.standard_normal((9, 7))
+        spec = spcp.ProblemSpec(x=x, lambda_l=1.3, lambda_s=0.6, mask=mask)
+        val, g, s = spcp.phi_value_grad(l, spec)
+        out.update({f"{tag}_x": x, f"{tag}_l": l, f"{tag}_value": val, f"{tag}_grad": g,
+                    f"{tag}_s": s})
+        if mask is not None:
+            out[f"{tag}_mask"] = mask
+    spec = spcp.ProblemSpec(x=[[2.0]], lambda_l=1.0, lambda_s=1.0)
+    val, g, s = spcp.phi_value_grad(np.zeros((1, 1)), spec)
+    out.update(kat_value=val, kat_grad=g, kat_s=s)
+    np.savez_compressed(os.path.join(OUT, "phi.npz"), **out)
+
+
+SPLIT_CASES = [  # (m, n, k, masked, lambda_l, lambda_s, seed)
+    (10, 8, 3, False, 1.0, 0.7, 31),
+    (10, 8, 3, True, 1.0, 0.7, 32),
+    (37, 29, 5, False, 0.9, 0.4, 33),
+    (64, 50, 7, True, 1.7, 0.3, 34),
+    (130, 97, 12, False, 2.0, 0.25, 35),
+    (200, 333, 33, True, 3.0, 0.5, 36),
+    (150, 80, 70, False, 1.5, 0.5, 37),
+]
+
+
+def gen_split(spcp):
+    out = {}
+    for idx, (m, n, k, masked, ll, ls, seed) in enumerate(SPLIT_CASES):
+        rng = np.random.default_rng(seed)
+        x = rng.standard_normal((m, n)) * 2.0
+        mask = rng.random((m, n)) < 0.8 if masked else None
+        u = rng.standard_normal((m, k)) * 0.5
+        v = rng.standard_normal((n, k)) * 0.5
+        spec = spcp.ProblemSpec(x=x, lambda_l=ll, lambda_s=ls, mask=mask)
+        f, gu, gv = spcp.split_objective(spcp.FactorPair(u, v), spec)
+        out.update({f"c{idx}_x": x, f"c{idx}_u": u, f"c{idx}_v": v, f"c{idx}_f": f,
+                    f"c{idx}_gu": gu, f"c{idx}_gv": gv,
+                    f"c{idx}_meta": np.array([m, n, k, int(masked), ll, ls], np.float64)})
+        if mask is not None:
+            out[f"c{idx}_mask"] = mask
+    spec = spcp.ProblemSpec(x=[[0.0]], lambda_l=1.0, lambda_s=10.0)
+    f, gu, gv = spcp.split_objective(spcp.FactorPair(np.array([[2.0]]), np.array([[3.0]])), spec)
+    out.update(kat_f=f, kat_gu=gu, kat_gv=gv, n_cases=len(SPLIT_CASES))
+    np.savez_compressed(os.path.join(OUT, "split.npz"), **out)
+
+
+def gen_lbfgs(spcp):
+    out = {}
+
+    def rosen(z):
+        a, b = z
+        f = (1 - a) ** 2 + 100.0 * (b - a * a) ** 2
+        g = np.array([-2 * (1 - a) - 400.0 * a * (b - a * a), 200.0 * (b - a * a)])
+        return f, g
+
+    res = spcp.minimize_lbfgs(rosen, np.array([-1.2, 1.0]), grad_tol=1e-12, max_iter=200)
+    it, ob, gn = _records(res.records)
+    out.update(rosen_x=res.x, rosen_f=res.objective, rosen_term=res.termination,
+               rosen_evals=res.n_evals, rosen_it=it, rosen_obj=ob, rosen_gn=gn)
+    c = np.random.default_rng(20).standard_normal(12)
+
+    def quad(z):
+        d = z - c
+        return 0.5 * float(d @ d), d
+
+    res = spcp.minimize_lbfgs(quad, np.zeros(12), grad_tol=1e-12, max_iter=12)
+    it, ob, gn = _records(res.records)
+    out.update(quad_c=c, quad_x=res.x, quad_term=res.termination, quad_evals=res.n_evals,
+               quad_obj=ob, quad_gn=gn)
+    np.savez_compressed(os.path.join(OUT, "lbfgs.npz"), **out)
+
+
+SOLVE_CASES = [  # (m, n, rank, frac, noise, gen_seed, lam_l, lam_s, k, masked, growth)
+    (20, 16, 3, 0.1, 1e-4, 99, 1.5, 0.4, 1, False, True),
+    (20, 15, 2, 0.15, 1e-3, 5, 1.2, 0.5, 6, False, False),
+    (40, 32, 8, 0.3, 1e-4, 11, 2.0, 0.5, 4, False, False),
+    (60, 45, 4, 0.1, 1e-3, 21, 1.0, 0.3, 6, True, False),
+    (120, 90, 5, 0.05, 1e-3, 22, 3.0, 0.2, 8, False, False),
+]
+
+
+def gen_solve(spcp):
+    out = {}
+    for idx, (m, n, rk, fr, nz, gs, ll, ls, k, masked, growth) in enumerate(SOLVE_CASES):
+        x, _, _ = spcp.gen_low_rank_plus_sparse(m, n, rk, fr, nz, seed=gs)
+        mask = spcp.gen_mask(m, n, 0.7, seed=gs + 1) if masked else None
+        spec = spcp.ProblemSpec(x=x, lambda_l=ll, lambda_s=ls, mask=mask)
+        cfg = spcp.SolverConfig(grad_tol=1e-9, max_iter=2000, rank_growth=growth,
+                                max_k=5 if growth else None)
+        rep = spcp.solve_split_spcp(spec, k, cfg)
+        it, ob, gn = _records(rep.iterations)
+        cert = spcp.certificate(rep.factors, spec, f_bound_hint=rep.best_objective)
+        out.update({f"s{idx}_x": x, f"s{idx}_u": rep.factors.u, f"s{idx}_v": rep.factors.v,
+                    f"s{idx}_l": rep.l, f"s{idx}_s": rep.s, f"s{idx}_obj": rep.objective,
+                    f"s{idx}_term": rep.termination, f"s{idx}_it": it, f"s{idx}_recobj": ob,
+                    f"s{idx}_recgn": gn, f"s{idx}_evals": rep.extra["n_evals"],
+                    f"s{idx}_kfinal": rep.extra["k_final"],
+                    f"s{idx}_grown": rep.extra["columns_grown"],
+                    f"s{idx}_cert": np.array([cert.e_norm, *cert.terms, cert.f_bound,
+                                              cert.gap_bound, cert.r, cert.l_norm]),
+                    f"s{idx}_meta": np.array([m, n, k, int(masked), ll, ls, int(growth)],
+                                             np.float64)})
+        if mask is not None:
+            out[f"s{idx}_mask"] = mask
+    out["n_cases"] = len(SOLVE_CASES)
+    np.savez_compressed(os.path.join(OUT, "solve.npz"), **out)
+
+
+def gen_cert(spcp):
+    out = {}
+    rng = np.random.default_rng(62)
+    for idx in range(6):
+        m, n, k = [(8, 6, 3), (7, 5, 2), (4, 3, 2), (30, 22, 4), (25, 40, 5), (12, 9, 4)][idx]
+        x = rng.standard_normal((m, n))
+        u = rng.standard_normal((m, k))
+        v = rng.standard_normal((n, k))
+        if idx == 5:
+            v[:, 3] = v[:, 2]  # rank-deficient product (test_certificate.py:35-44 analogue)
+        spec = spcp.ProblemSpec(x=x, lambda_l=1.1, lambda_s=0.4)
+        rep = spcp.certificate(spcp.FactorPair(u, v), spec)
+        out.update({f"q{idx}_x": x, f"q{idx}_u": u, f"q{idx}_v": v,
+                    f"q{idx}_cert": np.array([rep.e_norm, *rep.terms, rep.f_bound,
+                                              rep.gap_bound, rep.r, rep.l_norm])})
+    x = rng.standard_normal((6, 5))
+    spec = spcp.ProblemSpec(x=x, lambda_l=2.0, lambda_s=0.3)
+    rep = spcp.certificate(spcp.FactorPair(np.zeros((6, 1)), np.zeros((5, 1))), spec)
+    out.update(zero_x=x, zero_cert=np.array([rep.e_norm, *rep.terms, rep.f_bound,
+                                             rep.gap_bound, rep.r, rep.l_norm]))
+    out["n_cases"] = 6
+    np.savez_compressed(os.path.join(OUT, "cert.npz"), **out)
+
+
+def gen_c1(spcp):
+    """Config C1 (BASELINE.json configs[0]) solved by the reference at k=5,10,12."""
+    x, _, _ = spcp.gen_low_rank_plus_sparse(1000, 1000, 10, 0.05, 1e-3, seed=0)
+    x = x.astype(np.float32).astype(np.float64)  # the GPU and oracle see the same X32
+    spec = spcp.ProblemSpec(x=x, lambda_l=10.0, lambda_s=0.1)
+    out = {"x_sum": float(x.sum()), "x_sq": float((x * x).sum())}
+    fp0 = spcp.init_factors(spec, 10, strategy="rsvd", seed=0)
+    f0, gu0, gv0 = spcp.split_objective(fp0, spec)
+    out.update(init_u=fp0.u, init_v=fp0.v, init_f=f0, init_gu=gu0, init_gv=gv0)
+    for k in (5, 10, 12):
+        rep = spcp.solve_split_spcp(spec, k, spcp.SolverConfig())
+        it, ob, gn = _records(rep.iterations)
+        cert = spcp.certificate(rep.factors, spec, f_bound_hint=rep.best_objective)
+        out.update({f"k{k}_u": rep.factors.u, f"k{k}_v": rep.factors.v,
+                    f"k{k}_obj": rep.objective, f"k{k}_term": rep.termination,
+                    f"k{k}_recobj": ob, f"k{k}_recgn": gn, f"k{k}_evals": rep.extra["n_evals"],
+                    f"k{k}_s_nnz": int(np.count_nonzero(rep.s)),
+                    f"k{k}_s_fro": float(np.linalg.norm(rep.s)),
+                    f"k{k}_cert": np.array([cert.e_norm, *cert.terms, cert.f_bound,
+                                            cert.gap_bound, cert.r, cert.l_norm])})
+    np.savez_compressed(os.path.join(OUT, "c1.npz"), **out)
+
+
+def gen_synth(spcp):
+    x, l_ref, s_ref = spcp.gen_low_rank_plus_sparse(30, 20, 3, 0.1, 1e-3, seed=5)
+    mask = spcp.gen_mask(30, 20, 0.3, seed=6)
+    u, s, v = spcp.rand_svd(x, 3, oversample=5, power_iters=1, seed=3).__dict__.values()
+    np.savez_compressed(os.path.join(OUT, "synth.npz"), x=x, l_ref=l_ref, s_ref=s_ref,
+                        mask=mask, rsvd_u=u, rsvd_s=s, rsvd_v=v)
+
+
+if __name__ == "__main__":
+    ref = _ref()
+    for fn in (gen_phi, gen_split, gen_lbfgs, gen_solve, gen_cert, gen_synth, gen_c1):
+        fn(ref)
+        print("wrote", fn.__name__)

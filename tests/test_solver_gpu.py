@@ -1,0 +1,186 @@
+"""GPU solve / init / certificate parity against the reference (golden
+fixtures) and the oracle.  Final L and S within 1e-4 relative Frobenius,
+same certificate verdict (BASELINE.json north star)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.ravel(a) - np.ravel(b)) / max(np.linalg.norm(np.ravel(b)),
+                                                                 1e-300))
+
+
+@pytest.fixture(scope="module")
+def api():
+    import paper_1702_02241_b200 as pkg
+
+    return pkg
+
+
+def warns(cert, obj):
+    return cert.gap_bound > 1e-2 * max(1.0, abs(obj))
+
+
+def test_rsvd_init_matches_reference(api, golden):
+    d = golden("c1")
+    from oracle import spcp_oracle as orc
+
+    x, _, _ = orc.gen_low_rank_plus_sparse(1000, 1000, 10, 0.05, 1e-3, seed=0)
+    x = x.astype(np.float32).astype(np.float64)
+    spec = api.ProblemSpec(x=x, lambda_l=10.0, lambda_s=0.1)
+    fp = api.init_factors(spec, 10, strategy="rsvd", seed=0)
+    np.testing.assert_allclose(fp.u, d["init_u"], rtol=0, atol=1e-9)
+    np.testing.assert_allclose(fp.v, d["init_v"], rtol=0, atol=1e-9)
+    f, gu, gv = api.split_objective(fp, spec, precision="fp64")
+    assert f == pytest.approx(float(d["init_f"]), rel=1e-11)
+
+
+@pytest.mark.parametrize("case", range(5))
+def test_solve_golden_cases(api, golden, case):
+    d = golden("solve")
+    m, n, k, masked, ll, ls, growth = d[f"s{case}_meta"]
+    mask = d[f"s{case}_mask"] if masked else None
+    spec = api.ProblemSpec(x=d[f"s{case}_x"], lambda_l=ll, lambda_s=ls, mask=mask)
+    cfg = api.SolverConfig(grad_tol=1e-9, max_iter=2000, rank_growth=bool(growth),
+                           max_k=5 if growth else None)
+    rep = api.solve_split_spcp(spec, int(k), cfg)
+    ref_obj = float(d[f"s{case}_obj"])
+    assert rep.objective == pytest.approx(ref_obj, rel=1e-8)
+    assert rep.extra["k_final"] == int(d[f"s{case}_kfinal"])
+    assert rep.termination in ("converged", "line_search_failed")
+    assert rel(rep.l, d[f"s{case}_l"]) <= 1e-4
+    assert rel(rep.s, d[f"s{case}_s"]) <= 1e-4
+    objs = [r.objective for r in rep.iterations]
+    assert all(b <= a + 1e-12 * max(1.0, abs(a)) for a, b in zip(objs, objs[1:]))
+    cert = api.certificate(rep.factors, spec, f_bound_hint=rep.best_objective)
+    ref = d[f"s{case}_cert"]
+    assert cert.r == int(ref[7])
+    assert warns(cert, rep.objective) == (ref[6] > 1e-2 * max(1.0, abs(ref_obj)))
+
+
+@pytest.mark.parametrize("k", [5, 10, 12])
+def test_c1_solve_and_certificate(api, golden, k):
+    """Config C1 (BASELINE configs[0]) end to end: objective, L, S, verdict."""
+    from oracle import spcp_oracle as orc
+
+    d = golden("c1")
+    x, _, _ = orc.gen_low_rank_plus_sparse(1000, 1000, 10, 0.05, 1e-3, seed=0)
+    x = x.astype(np.float32).astype(np.float64)
+    spec = api.ProblemSpec(x=x, lambda_l=10.0, lambda_s=0.1)
+    rep = api.solve_split_spcp(spec, k, api.SolverConfig())
+    ref_obj = float(d[f"k{k}_obj"])
+    assert rep.objective == pytest.approx(ref_obj, rel=1e-8)
+    if k == 10:
+        assert rep.termination == str(d["k10_term"]) == "converged"
+    lr = d[f"k{k}_u"] @ d[f"k{k}_v"].T
+    assert rel(rep.l, lr) <= 1e-4
+    assert np.linalg.norm(rep.s) == pytest.approx(float(d[f"k{k}_s_fro"]), rel=1e-4)
+    cert = api.certificate(rep.factors, spec, f_bound_hint=rep.best_objective)
+    ref = d[f"k{k}_cert"]
+    assert cert.r == int(ref[7])
+    assert warns(cert, rep.objective) == (ref[6] > 1e-2 * max(1.0, abs(ref_obj)))
+    if k == 5:  # under-ranked: t4 dominates and must match the dense reference
+        assert cert.terms[3] == pytest.approx(ref[4], rel=1e-6)
+        assert cert.e_norm == pytest.approx(ref[0], rel=1e-6)
+
+
+def test_certificate_golden(api, golden):
+    d = golden("cert")
+    for i in range(int(d["n_cases"])):
+        spec = api.ProblemSpec(x=d[f"q{i}_x"], lambda_l=1.1, lambda_s=0.4)
+        fp = api.FactorPair(d[f"q{i}_u"], d[f"q{i}_v"])
+        cert = api.certificate(fp, spec)
+        ref = d[f"q{i}_cert"]
+        assert cert.r == int(ref[7]), i
+        np.testing.assert_allclose([cert.e_norm, *cert.terms, cert.f_bound, cert.gap_bound,
+                                    cert.l_norm], np.r_[ref[:7], ref[8]], rtol=1e-8, atol=1e-10)
+    spec = api.ProblemSpec(x=d["zero_x"], lambda_l=2.0, lambda_s=0.3)
+    cert = api.certificate(api.FactorPair(np.zeros((6, 1)), np.zeros((5, 1))), spec)
+    assert cert.r == 0 and cert.terms[:3] == (0.0, 0.0, 0.0)
+    assert cert.e_norm == pytest.approx(float(d["zero_cert"][0]), rel=1e-12)
+
+
+def test_certificate_subspace_matches_dense(api):
+    """The streaming subspace-iteration t4 (large-problem route) equals the
+    dense-SVD t4 on an under-ranked C1 iterate (several sigma(P) > 1)."""
+    from oracle import spcp_oracle as orc
+
+    x, _, _ = orc.gen_low_rank_plus_sparse(1000, 1000, 10, 0.05, 1e-3, seed=0)
+    x = x.astype(np.float32).astype(np.float64)
+    spec = api.ProblemSpec(x=x, lambda_l=10.0, lambda_s=0.1)
+    rep = api.solve_split_spcp(spec, 5, api.SolverConfig(max_iter=60))
+    dense = api.certificate(rep.factors, spec)
+    sub = api.certificate(rep.factors, spec, dense_limit=0)
+    assert sub.info["t4_method"] == "subspace"
+    assert dense.info["n_sigma_over_1"] >= 1
+    assert sub.terms[3] == pytest.approx(dense.terms[3], rel=1e-6)
+    assert sub.e_norm == pytest.approx(dense.e_norm, rel=1e-6)
+    # converged full-rank iterate: t4 = 0 on both routes
+    rep = api.solve_split_spcp(spec, 10, api.SolverConfig())
+    sub = api.certificate(rep.factors, spec, dense_limit=0)
+    assert sub.terms[3] == 0.0 and sub.info["sigma_p_max"] < 1.0
+
+
+def test_mixed_precision_solve_matches_oracle(api):
+    """A problem above MIXED_MIN_ELEMS runs fp32 bulk + fp64 finish; final
+    objective, L and S match the fp64 oracle (1e-4 rel Frobenius)."""
+    from oracle import spcp_oracle as orc
+
+    m, n = 2600, 1700
+    x, _, _ = orc.gen_low_rank_plus_sparse(m, n, 8, 0.05, 1e-3, seed=4)
+    x = x.astype(np.float32).astype(np.float64)
+    lam = 0.3 * np.sqrt(n)
+    spec = api.ProblemSpec(x=x, lambda_l=lam, lambda_s=0.1)
+    rep = api.solve_split_spcp(spec, 8, api.SolverConfig())
+    assert rep.extra["precision"] == "mixed"
+    ref = orc.solve_split_spcp(x, lam, 0.1, 8)
+    assert rep.objective == pytest.approx(ref["objective"], rel=1e-7)
+    assert rel(rep.l, ref["l"]) <= 1e-4
+    assert rel(rep.s, ref["s"]) <= 1e-4
+
+
+def test_rank_growth(api):
+    from oracle import spcp_oracle as orc
+
+    x, _, _ = orc.gen_low_rank_plus_sparse(20, 16, 3, 0.1, 1e-4, seed=99)
+    spec = api.ProblemSpec(x=x, lambda_l=1.5, lambda_s=0.4)
+    rep = api.solve_split_spcp(spec, 1, api.SolverConfig(grad_tol=1e-9, max_iter=2000,
+                                                         rank_growth=True, max_k=5))
+    assert rep.extra["k_final"] >= 3
+    ref = api.solve_split_spcp(spec, 5, api.SolverConfig(grad_tol=1e-9, max_iter=2000))
+    assert rep.objective == pytest.approx(ref.objective, rel=1e-4)
+
+
+def test_estimator(api):
+    from sklearn.base import clone
+
+    from oracle import spcp_oracle as orc
+
+    x, l_ref, _ = orc.gen_low_rank_plus_sparse(20, 16, 2, 0.15, 1e-3, seed=123)
+    est = api.SplitSPCP(lambda_l=0.8, lambda_s=0.25, rank=6, max_iter=2000).fit(x)
+    assert rel(est.low_rank_, l_ref) < 0.15
+    proj = est.transform(x)
+    q = est.components_
+    np.testing.assert_allclose(q @ (q.T @ proj), proj, atol=1e-10)
+    assert clone(est).get_params() == est.get_params()
+    cert = est.certify()
+    assert cert.gap_bound >= 0
+
+
+def test_hooks_and_records(api):
+    from oracle import spcp_oracle as orc
+
+    x, _, _ = orc.gen_low_rank_plus_sparse(10, 8, 2, 0.2, 1e-3, seed=8)
+    spec = api.ProblemSpec(x=x, lambda_l=1.0, lambda_s=0.5)
+    seen = []
+
+    def hook(it, state):
+        seen.append((it, state.factors.k))
+        return {"marker": it}
+
+    rep = api.solve_split_spcp(spec, 3, api.SolverConfig(max_iter=50), iter_hook=hook)
+    assert [r.extra["marker"] for r in rep.iterations] == [s[0] for s in seen]
+    assert all(r.extra["rank"] == 3 for r in rep.iterations)
