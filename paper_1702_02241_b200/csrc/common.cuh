@@ -26,9 +26,12 @@ int cuda_fail(cudaError_t e, const char* where);
     if (_e != cudaSuccess) return ::spcp::cuda_fail(_e, #call); \
   } while (0)
 
+bool debug_sync();  // SPCP_DEBUG_SYNC=1: synchronise after every launch
+
 #define SPCP_CHECK_LAUNCH(where)                                \
   do {                                                          \
     cudaError_t _e = cudaGetLastError();                        \
+    if (_e == cudaSuccess && ::spcp::debug_sync()) _e = cudaDeviceSynchronize(); \
     if (_e != cudaSuccess) return ::spcp::cuda_fail(_e, where); \
   } while (0)
 

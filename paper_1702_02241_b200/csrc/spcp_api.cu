@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -29,6 +30,15 @@ int fail(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
 }
+bool debug_sync() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SPCP_DEBUG_SYNC");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 int cuda_fail(cudaError_t e, const char* where) {
   g_last_error = std::string("CUDA error in ") + where + ": " + cudaGetErrorString(e);
   return SPCP_ERR_CUDA;
@@ -211,10 +221,10 @@ static inline int grid_for(int64_t total, int threads = 256, int64_t cap = 148 *
 
 static int ensure_common(spcp_problem* p) {
   int rc;
-  if ((rc = p->out_dev.ensure(64 * sizeof(double)))) return rc;
+  if ((rc = p->out_dev.ensure(256 * sizeof(double)))) return rc;
   if ((rc = p->counter.ensure(64))) return rc;
   if (!p->host_out) {
-    SPCP_CUDA(cudaMallocHost(&p->host_out, 64 * sizeof(double)));
+    SPCP_CUDA(cudaMallocHost(&p->host_out, 256 * sizeof(double)));
     SPCP_CUDA(cudaMemsetAsync(p->counter.ptr, 0, 64, p->stream));
   }
   return SPCP_OK;
@@ -333,11 +343,12 @@ static int dense_fallback_eval(spcp_problem* p, int64_t k, const double* z, cons
   // trial point in float64
   int rc;
   const int64_t len = (p->m + p->n) * k;
-  if ((rc = p->scratch.ensure(size_t(len) * sizeof(double) +
+  const int64_t len_al = round_up(len, 32);  // keep gmat 256B-aligned for cp.async16
+  if ((rc = p->scratch.ensure(size_t(len_al) * sizeof(double) +
                               size_t(p->m_pad) * p->ldx * sizeof(double))))
     return rc;
   double* w = p->scratch.as<double>();
-  double* gmat = w + len;
+  double* gmat = w + len_al;
   {
     VecPtrs vp{};
     vp.a[0] = z;
@@ -361,6 +372,12 @@ static int dense_fallback_eval(spcp_problem* p, int64_t k, const double* z, cons
                   : launch_dense<float>(p, 1, k, w, 0, p->m, gmat, nullptr, p->ldx,
                                         ph.as<double>());
   if (rc) return rc;
+  // fold phi now: the RAW launches below reuse the pphi buffer
+  if ((rc = p->scal.ensure(8 * sizeof(double)))) return rc;
+  sum_partials_kernel<<<1, 256, 0, p->stream>>>(ph.as<double>(), int(nbx * nby),
+                                                p->scal.as<double>());
+  SPCP_CHECK_LAUNCH("sum_partials(phi)");
+  p->launches++;
   // products G V and G^T U through the RAW streaming kernel over gmat, in
   // column blocks of 32 of the rank dimension
   const int64_t nrb = p->m_pad / 128;
@@ -426,10 +443,13 @@ static int dense_fallback_eval(spcp_problem* p, int64_t k, const double* z, cons
                             cudaMemcpyDeviceToDevice, p->stream));
   SPCP_CUDA(cudaMemcpyAsync(p->pright.ptr, pr, size_t(p->n_pad) * kp * sizeof(double),
                             cudaMemcpyDeviceToDevice, p->stream));
-  // pphi currently holds nbx*nby dense partials
+  // one phi partial: the folded dense value
+  if ((rc2 = p->pphi.ensure(sizeof(double)))) return rc2;
+  SPCP_CUDA(cudaMemcpyAsync(p->pphi.ptr, p->scal.ptr, sizeof(double), cudaMemcpyDeviceToDevice,
+                            p->stream));
   sh.nchunks = 1;
   sh.nrb = 1;
-  sh.chunk_cols = int64_t(nbx * nby);  // smuggle the phi partial count
+  sh.chunk_cols = 1;  // phi partial count seen by run_reduce (dense path)
   return SPCP_OK;
 }
 
@@ -606,7 +626,8 @@ int spcp_problem_create(spcp_problem** out, int device, int64_t m, int64_t n, co
           static_cast<const float*>(src), lds, rows, n, r0, p->x32.as<float>(),
           p->x64.as<double>(), p->ldx, mrows, psq, psq + nblk);
     cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return bail(cuda_fail(e, "convert_x"));
+    if (e == cudaSuccess && debug_sync()) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return bail(cuda_fail(e, "convert_x / pack_mask"));
     // stage buffers are reused next chunk: serialise
     e = cudaStreamSynchronize(p->stream);
     if (e != cudaSuccess) return bail(cuda_fail(e, "upload sync"));
@@ -632,6 +653,7 @@ int spcp_problem_create(spcp_problem** out, int device, int64_t m, int64_t n, co
 }
 
 int spcp_problem_destroy(spcp_problem* p) {
+  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
   if (!p) return SPCP_OK;
   cudaSetDevice(p->device);
   if (p->stream) cudaStreamSynchronize(p->stream);
@@ -647,11 +669,13 @@ int spcp_problem_destroy(spcp_problem* p) {
 }
 
 int spcp_problem_set_stream(spcp_problem* p, void* stream) {
+  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
   p->stream = reinterpret_cast<cudaStream_t>(stream);
   return SPCP_OK;
 }
 
 int spcp_problem_info(spcp_problem* p, double* info) {
+  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
   info[0] = p->f_zero;
   info[1] = p->n_obs;
   info[2] = double(p->stored);
@@ -677,6 +701,7 @@ static int eval_impl(spcp_problem* p, int64_t k, int dtype, const double* z, con
 
 int spcp_eval(spcp_problem* p, int64_t k, int dtype, const double* z, const double* dz,
               double alpha, double* g_out, double* out) {
+  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
   int rc = eval_impl(p, k, dtype, z, dz, alpha, g_out, U_FULL, nullptr, nullptr);
   if (rc) return rc;
   return fetch_out(p, out);
@@ -684,12 +709,14 @@ int spcp_eval(spcp_problem* p, int64_t k, int dtype, const double* z, const doub
 
 int spcp_eval_partial(spcp_problem* p, int64_t k, int dtype, const double* z, const double* dz,
                       double alpha, void* gu_part, double* scal, double* g_out) {
+  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
   return eval_impl(p, k, dtype, z, dz, alpha, g_out, U_PARTIAL, gu_part, scal);
 }
 
 int spcp_eval_finish(spcp_problem* p, int64_t k, int dtype, const double* z, const double* dz,
                      double alpha, const void* gu_sum, const double* scal_sum, double* g_out,
                      double* out) {
+  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
   int rc;
   if ((rc = check_k(p, k))) return rc;
   SPCP_CUDA(cudaSetDevice(p->device));
@@ -703,6 +730,7 @@ int spcp_eval_finish(spcp_problem* p, int64_t k, int dtype, const double* z, con
 
 int spcp_split_objective_host(spcp_problem* p, int64_t k, int dtype, const double* u,
                               const double* v, double* value, double* grad_u, double* grad_v) {
+  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
   int rc;
   if ((rc = check_k(p, k))) return rc;
   SPCP_CUDA(cudaSetDevice(p->device));
@@ -737,6 +765,7 @@ int spcp_split_objective_host(spcp_problem* p, int64_t k, int dtype, const doubl
 
 int spcp_phi_dense_host(spcp_problem* p, const double* l, double* value, double* grad,
                         double* s_star) {
+  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
   int rc;
   SPCP_CUDA(cudaSetDevice(p->device));
   const int64_t mn = p->m * p->n;
@@ -777,6 +806,7 @@ int spcp_phi_dense_host(spcp_problem* p, const double* l, double* value, double*
 
 int spcp_apply(spcp_problem* p, int64_t k, const double* z, int64_t b, const double* w_right,
                double* left_out, const double* w_left, double* right_out) {
+  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
   int rc;
   if (k < 0 || b < 1) return fail(SPCP_ERR_DIMENSION, "bad apply shape");
   SPCP_CUDA(cudaSetDevice(p->device));
@@ -868,6 +898,7 @@ int spcp_apply(spcp_problem* p, int64_t k, const double* z, int64_t b, const dou
 
 int spcp_materialize(spcp_problem* p, int64_t k, const double* z, int64_t row0, int64_t rows,
                      double* l_out, double* s_out, int out_on_host) {
+  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
   int rc;
   if (row0 < 0 || rows < 0 || row0 + rows > p->m) return fail(SPCP_ERR_DIMENSION, "bad row range");
   SPCP_CUDA(cudaSetDevice(p->device));
@@ -902,6 +933,7 @@ int spcp_materialize(spcp_problem* p, int64_t k, const double* z, int64_t row0, 
 
 int spcp_materialize_grad(spcp_problem* p, int64_t k, const double* z, double* g_out,
                           int64_t ldo) {
+  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
   int rc;
   if (k < 1) return fail(SPCP_ERR_DIMENSION, "k must be >= 1");
   if (ldo < p->n) return fail(SPCP_ERR_DIMENSION, "ldo < n");
@@ -919,6 +951,7 @@ int spcp_materialize_grad(spcp_problem* p, int64_t k, const double* z, double* g
 
 int spcp_vec_multidot(spcp_problem* p, int64_t len, int count, const double* const* a,
                       const double* const* b, double* out_host) {
+  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
   int rc;
   SPCP_CUDA(cudaSetDevice(p->device));
   if ((rc = ensure_common(p))) return rc;
@@ -948,6 +981,7 @@ int spcp_vec_multidot(spcp_problem* p, int64_t len, int count, const double* con
 
 int spcp_vec_lincomb(spcp_problem* p, int64_t len, int count, const double* coef,
                      const double* const* v, double* out) {
+  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
   SPCP_CUDA(cudaSetDevice(p->device));
   if (count < 1) return fail(SPCP_ERR_VALUE, "lincomb needs >= 1 vector");
   if (count > kMaxVec) return fail(SPCP_ERR_VALUE, "lincomb: too many vectors");
@@ -964,6 +998,7 @@ int spcp_vec_lincomb(spcp_problem* p, int64_t len, int count, const double* coef
 
 int spcp_vec_gram(spcp_problem* p, int64_t len, int na, const double* const* a, int nb,
                   const double* const* b, double* out_host) {
+  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
   int rc;
   SPCP_CUDA(cudaSetDevice(p->device));
   if (nb < 1 || nb > 4 || na < 1) return fail(SPCP_ERR_VALUE, "vec_gram: need 1<=nb<=4, na>=1");
@@ -996,6 +1031,7 @@ int spcp_vec_gram(spcp_problem* p, int64_t len, int na, const double* const* a, 
 
 int spcp_gram(spcp_problem* p, int64_t rows, int64_t pa, const double* a, int64_t qb,
               const double* b, double* out_host) {
+  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
   int rc;
   SPCP_CUDA(cudaSetDevice(p->device));
   const int64_t rpb = std::max<int64_t>(256, round_up(ceil_div(rows, 296), 32));
@@ -1018,6 +1054,7 @@ int spcp_gram(spcp_problem* p, int64_t rows, int64_t pa, const double* a, int64_
 
 int spcp_matmul_small(spcp_problem* p, int64_t rows, int64_t pa, const double* a, int64_t qb,
                       const double* m_host, double* c) {
+  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
   int rc;
   SPCP_CUDA(cudaSetDevice(p->device));
   if ((rc = p->small.ensure(std::max(p->small.bytes, size_t(pa * qb) * sizeof(double))))) return rc;
@@ -1035,6 +1072,7 @@ int spcp_matmul_small(spcp_problem* p, int64_t rows, int64_t pa, const double* a
 }
 
 int spcp_prof_enable(spcp_problem* p, int on) {
+  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
   p->prof = on != 0;
   p->prof_ms = 0.0;
   p->prof_count = 0;
@@ -1043,6 +1081,7 @@ int spcp_prof_enable(spcp_problem* p, int on) {
 }
 
 int spcp_prof_read(spcp_problem* p, double* ms_total, int64_t* launches, int64_t* kernels) {
+  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
   *ms_total = p->prof_ms;
   *launches = p->prof_count;
   *kernels = p->launches;

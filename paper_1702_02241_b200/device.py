@@ -104,12 +104,20 @@ class DeviceProblem:
         self._keep = None
         self._keep_mask = None
         info = (ctypes.c_double * 4)()
-        check(lib.spcp_problem_info(self.handle, info))
+        check(lib.spcp_problem_info(self.h, info))
         self.f_zero = float(info[0])
         self.n_obs = float(info[1])
         self._out = (ctypes.c_double * 8)()
 
     # ------------------------------------------------------------ lifecycle
+    @property
+    def h(self):
+        if not self.handle:
+            from .errors import DeviceError
+
+            raise DeviceError("device problem already released")
+        return self.handle
+
     def close(self):
         if getattr(self, "handle", None):
             lib.spcp_problem_destroy(self.handle)
@@ -138,16 +146,16 @@ class DeviceProblem:
     def eval(self, k, dtype, z, dz, alpha, g_out):
         """F and grad F at z + alpha*dz -> np.array([f, phi, reg, g.dz, |g|^2, |gU|^2,
         gU.dzU, 0]); g_out (device float64) receives the gradient."""
-        check(lib.spcp_eval(self.handle, int(k), int(dtype), dptr(z), dptr(dz), float(alpha),
+        check(lib.spcp_eval(self.h, int(k), int(dtype), dptr(z), dptr(dz), float(alpha),
                             dptr(g_out), self._out))
         return np.frombuffer(self._out, dtype=np.float64).copy()
 
     def eval_partial(self, k, dtype, z, dz, alpha, gu_part, scal, g_out):
-        check(lib.spcp_eval_partial(self.handle, int(k), int(dtype), dptr(z), dptr(dz),
+        check(lib.spcp_eval_partial(self.h, int(k), int(dtype), dptr(z), dptr(dz),
                                     float(alpha), dptr(gu_part), dptr(scal), dptr(g_out)))
 
     def eval_finish(self, k, dtype, z, dz, alpha, gu_sum, scal_sum, g_out):
-        check(lib.spcp_eval_finish(self.handle, int(k), int(dtype), dptr(z), dptr(dz),
+        check(lib.spcp_eval_finish(self.h, int(k), int(dtype), dptr(z), dptr(dz),
                                    float(alpha), dptr(gu_sum), dptr(scal_sum), dptr(g_out),
                                    self._out))
         return np.frombuffer(self._out, dtype=np.float64).copy()
@@ -159,7 +167,7 @@ class DeviceProblem:
         gu = np.empty_like(u)
         gv = np.empty_like(v)
         val = ctypes.c_double()
-        check(lib.spcp_split_objective_host(self.handle, k, int(dtype),
+        check(lib.spcp_split_objective_host(self.h, k, int(dtype),
                                             ctypes.c_void_p(u.ctypes.data),
                                             ctypes.c_void_p(v.ctypes.data), ctypes.byref(val),
                                             ctypes.c_void_p(gu.ctypes.data),
@@ -171,7 +179,7 @@ class DeviceProblem:
         g = np.empty_like(l) if want_grad else None
         s = np.empty_like(l) if want_s else None
         val = ctypes.c_double()
-        check(lib.spcp_phi_dense_host(self.handle, ctypes.c_void_p(l.ctypes.data),
+        check(lib.spcp_phi_dense_host(self.h, ctypes.c_void_p(l.ctypes.data),
                                       ctypes.byref(val),
                                       None if g is None else ctypes.c_void_p(g.ctypes.data),
                                       None if s is None else ctypes.c_void_p(s.ctypes.data)))
@@ -190,7 +198,7 @@ class DeviceProblem:
         if w_left is not None:
             w_left = w_left.contiguous()
             right = torch.empty((self.n, b), dtype=torch.float64, device=self.device)
-        check(lib.spcp_apply(self.handle, int(k), dptr(z), b, dptr(w_right), dptr(left),
+        check(lib.spcp_apply(self.h, int(k), dptr(z), b, dptr(w_right), dptr(left),
                              dptr(w_left), dptr(right)))
         return left, right
 
@@ -198,7 +206,7 @@ class DeviceProblem:
         rows = self.m - row0 if rows is None else rows
         l = np.empty((rows, self.n)) if want_l else None
         s = np.empty((rows, self.n)) if want_s else None
-        check(lib.spcp_materialize(self.handle, int(k), dptr(z), int(row0), int(rows),
+        check(lib.spcp_materialize(self.h, int(k), dptr(z), int(row0), int(rows),
                                    None if l is None else ctypes.c_void_p(l.ctypes.data),
                                    None if s is None else ctypes.c_void_p(s.ctypes.data), 1))
         return l, s
@@ -207,7 +215,7 @@ class DeviceProblem:
         """Dense grad phi(U V^T) as an (m x n) float64 device matrix."""
         torch = torch_mod()
         g = torch.empty((self.m, self.n), dtype=torch.float64, device=self.device)
-        check(lib.spcp_materialize_grad(self.handle, int(k), dptr(z), dptr(g), self.n))
+        check(lib.spcp_materialize_grad(self.h, int(k), dptr(z), dptr(g), self.n))
         return g
 
     # ------------------------------------------------------------ vector algebra
@@ -215,7 +223,7 @@ class DeviceProblem:
         cnt = len(a_list)
         out = (ctypes.c_double * cnt)()
         length = a_list[0].numel()
-        check(lib.spcp_vec_multidot(self.handle, length, cnt, _ptr_array(a_list),
+        check(lib.spcp_vec_multidot(self.h, length, cnt, _ptr_array(a_list),
                                     _ptr_array(b_list), out))
         return np.frombuffer(out, dtype=np.float64).copy()
 
@@ -223,14 +231,14 @@ class DeviceProblem:
         """Host (len(a) x len(b)) matrix of dots, each device vector read once."""
         na, nb = len(a_list), len(b_list)
         out = (ctypes.c_double * (na * nb))()
-        check(lib.spcp_vec_gram(self.handle, a_list[0].numel(), na, _ptr_array(a_list), nb,
+        check(lib.spcp_vec_gram(self.h, a_list[0].numel(), na, _ptr_array(a_list), nb,
                                 _ptr_array(b_list), out))
         return np.frombuffer(out, dtype=np.float64).reshape(na, nb).copy()
 
     def lincomb(self, coefs, vecs, out):
         cnt = len(vecs)
         c = (ctypes.c_double * cnt)(*[float(x) for x in coefs])
-        check(lib.spcp_vec_lincomb(self.handle, out.numel(), cnt, c, _ptr_array(vecs),
+        check(lib.spcp_vec_lincomb(self.h, out.numel(), cnt, c, _ptr_array(vecs),
                                    dptr(out)))
         return out
 
@@ -241,7 +249,7 @@ class DeviceProblem:
         rows, pa = a.shape
         qb = b.shape[1]
         out = np.empty((pa, qb))
-        check(lib.spcp_gram(self.handle, rows, pa, dptr(a), qb, dptr(b),
+        check(lib.spcp_gram(self.h, rows, pa, dptr(a), qb, dptr(b),
                             out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
         return out
 
@@ -253,18 +261,18 @@ class DeviceProblem:
         mat = np.ascontiguousarray(mat, dtype=np.float64)
         qb = mat.shape[1]
         c = torch.empty((rows, qb), dtype=torch.float64, device=self.device)
-        check(lib.spcp_matmul_small(self.handle, rows, pa, dptr(a), qb,
+        check(lib.spcp_matmul_small(self.h, rows, pa, dptr(a), qb,
                                     mat.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), dptr(c)))
         return c
 
     # ------------------------------------------------------------ profiling
     def prof_enable(self, on=True):
-        check(lib.spcp_prof_enable(self.handle, int(bool(on))))
+        check(lib.spcp_prof_enable(self.h, int(bool(on))))
 
     def prof_read(self):
         ms = ctypes.c_double()
         cnt = ctypes.c_int64()
         kl = ctypes.c_int64()
-        check(lib.spcp_prof_read(self.handle, ctypes.byref(ms), ctypes.byref(cnt),
+        check(lib.spcp_prof_read(self.h, ctypes.byref(ms), ctypes.byref(cnt),
                                  ctypes.byref(kl)))
         return float(ms.value), int(cnt.value), int(kl.value)

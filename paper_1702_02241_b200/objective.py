@@ -120,8 +120,8 @@ class ProblemSpec:
         if dev is not None and need <= dev.store:
             return dev
         store = set(need) | (set(dev.store) if dev is not None else set())
-        if dev is not None:
-            dev.close()
+        # the replaced problem is not closed here: callers may still hold it;
+        # it frees its HBM when the last reference goes away
         dev = DeviceProblem(self.x, self.lambda_l, self.lambda_s, self.mask,
                             store=tuple(sorted(store)))
         object.__setattr__(self, "_dev", dev)

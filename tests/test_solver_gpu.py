@@ -53,8 +53,11 @@ def test_solve_golden_cases(api, golden, case):
     assert rep.termination in ("converged", "line_search_failed")
     assert rel(rep.l, d[f"s{case}_l"]) <= 1e-4
     assert rel(rep.s, d[f"s{case}_s"]) <= 1e-4
-    objs = [r.objective for r in rep.iterations]
-    assert all(b <= a + 1e-12 * max(1.0, abs(a)) for a, b in zip(objs, objs[1:]))
+    # monotone within each rank phase (growth restarts the sequence)
+    recs = rep.iterations
+    for a, b in zip(recs, recs[1:]):
+        if a.extra["rank"] == b.extra["rank"]:
+            assert b.objective <= a.objective + 1e-12 * max(1.0, abs(a.objective))
     cert = api.certificate(rep.factors, spec, f_bound_hint=rep.best_objective)
     ref = d[f"s{case}_cert"]
     assert cert.r == int(ref[7])
