@@ -136,6 +136,13 @@ struct ReduceParams {
   const double* scal_sum;  // U_FROM_SUM: [phi, regV, gVdV, gV2] summed over ranks
   double* scal_out;        // U_PARTIAL: shard scalars out
   double* out;             // [8] totals (U_FULL / U_FROM_SUM)
+  // tensor-core partial layout (csr_u_off != nullptr): pleft[slot][128][kst],
+  // pright[slot][64][kst], sources per 128-row sub-band / 64-column tile
+  const int32_t* csr_u_off;
+  const int32_t* csr_u_idx;
+  const int32_t* csr_v_off;
+  const int32_t* csr_v_idx;
+  int kst;
 };
 
 template <typename T>
@@ -155,8 +162,15 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p) {
         acc = double(reinterpret_cast<const T*>(p.gu_sum)[q]);
       } else {
         acc = 0.0;
-        for (int ch = 0; ch < p.nchunks; ++ch)
-          acc += double(pl[(int64_t(ch) * p.m_pad + i) * p.kp + c]);
+        if (p.csr_u_off) {
+          const int sb = int(i >> 7);
+          const float* plf = reinterpret_cast<const float*>(p.pleft);
+          for (int e = p.csr_u_off[sb]; e < p.csr_u_off[sb + 1]; ++e)
+            acc += double(plf[(int64_t(p.csr_u_idx[e]) * 128 + (i & 127)) * p.kst + c]);
+        } else {
+          for (int ch = 0; ch < p.nchunks; ++ch)
+            acc += double(pl[(int64_t(ch) * p.m_pad + i) * p.kp + c]);
+        }
       }
       if (p.u_mode == U_PARTIAL) {
         reinterpret_cast<T*>(p.gu_part)[q] = T(acc);
@@ -177,7 +191,14 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p) {
     for (int64_t q = t0; q < nv; q += stride) {
       const int64_t j = q / p.k, c = q % p.k;
       double acc = 0.0;
-      for (int b = 0; b < p.nrb; ++b) acc += double(pr[(int64_t(b) * p.n_pad + j) * p.kp + c]);
+      if (p.csr_v_off) {
+        const int tcol = int(j >> 6);
+        const float* prf = reinterpret_cast<const float*>(p.pright);
+        for (int e = p.csr_v_off[tcol]; e < p.csr_v_off[tcol + 1]; ++e)
+          acc += double(prf[(int64_t(p.csr_v_idx[e]) * 64 + (j & 63)) * p.kst + c]);
+      } else {
+        for (int b = 0; b < p.nrb; ++b) acc += double(pr[(int64_t(b) * p.n_pad + j) * p.kp + c]);
+      }
       const int64_t o = nu + q;
       double w = p.z[o];
       const double d = p.dz ? p.dz[o] : 0.0;

@@ -20,6 +20,7 @@
 #include "aux_kernels.cuh"
 #include "common.cuh"
 #include "stream_simt.cuh"
+#include "stream_tc.cuh"
 
 namespace spcp {
 
@@ -92,6 +93,13 @@ struct spcp_problem {
   double prof_ms = 0.0;
   int64_t prof_count = 0;
   int64_t launches = 0;
+  // tensor-core streaming path (fp32, k <= 64)
+  bool tc_ready = false;
+  int tc_grid = 0, tc_runs = 0, tc_slots = 0;
+  int64_t tc_nsb = 0, tc_ntc = 0;
+  CUtensorMap tc_xmap, tc_mmap;
+  spcp::DevBuf tc_units, tc_begin, tc_csr, tc_uimg, tc_vimg, tc_scales;
+  int64_t tc_csr_u_off = 0, tc_csr_u_idx = 0, tc_csr_v_off = 0, tc_csr_v_idx = 0;
 };
 
 namespace spcp {
@@ -111,6 +119,8 @@ struct DT<double> {
 struct LaunchShape {
   int nchunks = 1, nrb = 1;
   int64_t chunk_cols = 0;
+  int tc = 0;  // partials in the tensor-core (CSR slot) layout
+  int kst = 0;
 };
 
 template <typename T, typename TX, int KR, int PW, int MODE, bool MASK>
@@ -285,6 +295,210 @@ static StreamParams base_params(spcp_problem* p, bool want_f64) {
 static int dense_fallback_eval(spcp_problem* p, int64_t k, const double* z, const double* dz,
                                double alpha, LaunchShape& sh);
 
+// ======================================================== tensor-core path
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static bool tc_env_enabled() {
+  const char* e = getenv("SPCP_FP32_KERNEL");
+  return !(e && std::string(e) == "simt");
+}
+
+// Static schedule: tiles (sb, tc) in 2-D super-block order, exactly balanced
+// contiguous ranges per CTA, run/slot bookkeeping and the CSR source lists
+// the reduce kernel folds in a fixed order.
+static int tc_build(spcp_problem* p) {
+  if (p->tc_ready) return SPCP_OK;
+  static EncodeTiledFn enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    SPCP_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess)
+      return fail(SPCP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    enc = reinterpret_cast<EncodeTiledFn>(fn);
+  }
+  {
+    cuuint64_t dims[2] = {cuuint64_t(p->ldx), cuuint64_t(p->m_pad)};
+    cuuint64_t strides[1] = {cuuint64_t(p->ldx) * 4};
+    cuuint32_t box[2] = {32, 128};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(&p->tc_xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, p->x32.ptr, dims, strides,
+                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(SPCP_ERR_CUDA, "tensor map (X) encode failed");
+  }
+  if (p->masked) {
+    cuuint64_t dims[2] = {cuuint64_t(p->ldm), cuuint64_t(p->m_pad)};
+    cuuint64_t strides[1] = {cuuint64_t(p->ldm) * 4};
+    cuuint32_t box[2] = {4, 128};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(&p->tc_mmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, p->mbits.ptr, dims,
+                     strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(SPCP_ERR_CUDA, "tensor map (mask) encode failed");
+  } else {
+    p->tc_mmap = p->tc_xmap;  // unused
+  }
+  const int64_t nsb = p->m_pad / 128, ntc = p->n_pad / 64;
+  if (nsb > 65535 || ntc > 65535) return fail(SPCP_ERR_UNSUPPORTED, "matrix too large for TC tiles");
+  const int64_t U = nsb * ntc;
+  const int G = int(std::min<int64_t>(kSMs, U));
+  const double per = double(U) / G;
+  int side = std::max(1, int(std::lround(std::sqrt(per))));
+  const int sbr = int(std::min<int64_t>(side, nsb));
+  const int sbc = int(std::min<int64_t>(std::max<int64_t>(1, std::lround(per / sbr)), ntc));
+  std::vector<TcUnit> units;
+  units.reserve(U);
+  for (int64_t r0 = 0; r0 < nsb; r0 += sbr)
+    for (int64_t c0 = 0; c0 < ntc; c0 += sbc)
+      for (int64_t sb = r0; sb < std::min<int64_t>(r0 + sbr, nsb); ++sb)
+        for (int64_t tc = c0; tc < std::min<int64_t>(c0 + sbc, ntc); ++tc) {
+          TcUnit u{};
+          u.sb = uint16_t(sb);
+          u.tc = uint16_t(tc);
+          units.push_back(u);
+        }
+  std::vector<int32_t> begin(G + 1);
+  for (int c = 0; c <= G; ++c) begin[c] = int32_t((int64_t(c) * U) / G);
+  int runs = 0, slots = 0;
+  std::vector<std::vector<int32_t>> u_src(nsb), v_src(ntc);
+  for (int c = 0; c < G; ++c) {
+    std::map<int, int> slot_of;  // tc -> global slot, this CTA
+    for (int i = begin[c]; i < begin[c + 1]; ++i) {
+      TcUnit& u = units[i];
+      const bool first = (i == begin[c]) || units[i - 1].sb != u.sb;
+      const bool last = (i + 1 == begin[c + 1]) || units[i + 1].sb != u.sb;
+      if (first) {
+        u_src[u.sb].push_back(runs);
+        ++runs;
+      }
+      u.gv_slot = runs - 1;
+      u.flags = (first ? TCU_FIRST_OF_RUN : 0u) | (last ? TCU_LAST_OF_RUN : 0u);
+      auto it = slot_of.find(u.tc);
+      if (it == slot_of.end()) {
+        slot_of[u.tc] = slots;
+        v_src[u.tc].push_back(slots);
+        u.gt_slot = slots++;
+        u.flags |= TCU_FIRST_TOUCH;
+      } else {
+        u.gt_slot = it->second;
+      }
+    }
+  }
+  std::vector<int32_t> csr;
+  p->tc_csr_u_off = 0;
+  csr.push_back(0);
+  for (int64_t s = 0; s < nsb; ++s) csr.push_back(csr.back() + int32_t(u_src[s].size()));
+  p->tc_csr_u_idx = int64_t(csr.size());
+  for (auto& v : u_src) csr.insert(csr.end(), v.begin(), v.end());
+  p->tc_csr_v_off = int64_t(csr.size());
+  csr.push_back(0);
+  for (int64_t t = 0; t < ntc; ++t)
+    csr.push_back(csr[p->tc_csr_v_off + t] + int32_t(v_src[t].size()));
+  p->tc_csr_v_idx = int64_t(csr.size());
+  for (auto& v : v_src) csr.insert(csr.end(), v.begin(), v.end());
+  int rc;
+  if ((rc = p->tc_units.ensure(units.size() * sizeof(TcUnit)))) return rc;
+  if ((rc = p->tc_begin.ensure(begin.size() * sizeof(int32_t)))) return rc;
+  if ((rc = p->tc_csr.ensure(csr.size() * sizeof(int32_t)))) return rc;
+  if ((rc = p->tc_scales.ensure(sizeof(TcScales)))) return rc;
+  SPCP_CUDA(cudaMemcpy(p->tc_units.ptr, units.data(), units.size() * sizeof(TcUnit),
+                       cudaMemcpyHostToDevice));
+  SPCP_CUDA(cudaMemcpy(p->tc_begin.ptr, begin.data(), begin.size() * sizeof(int32_t),
+                       cudaMemcpyHostToDevice));
+  SPCP_CUDA(cudaMemcpy(p->tc_csr.ptr, csr.data(), csr.size() * sizeof(int32_t),
+                       cudaMemcpyHostToDevice));
+  p->tc_grid = G;
+  p->tc_runs = runs;
+  p->tc_slots = slots;
+  p->tc_nsb = nsb;
+  p->tc_ntc = ntc;
+  p->tc_ready = true;
+  return SPCP_OK;
+}
+
+template <int KP16, bool MASK>
+static int tc_launch(spcp_problem* p, int64_t k) {
+  using C = TcCfg<KP16, MASK>;
+  auto kern = tc_eval_kernel<KP16, MASK>;
+  static bool attr = false;
+  if (!attr) {
+    SPCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr = true;
+  }
+  TcParams tp{};
+  tp.units = p->tc_units.as<TcUnit>();
+  tp.cta_begin = p->tc_begin.as<int32_t>();
+  tp.u_img = p->tc_uimg.as<unsigned char>();
+  tp.v_img = p->tc_vimg.as<unsigned char>();
+  tp.scales = p->tc_scales.as<TcScales>();
+  tp.pleft = p->pleft.as<float>();
+  tp.pright = p->pright.as<float>();
+  tp.pphi = p->pphi.as<double>();
+  tp.kstore = int(k);
+  if (p->prof) SPCP_CUDA(cudaEventRecord(p->ev0, p->stream));
+  kern<<<p->tc_grid, C::NTHREADS, C::SMEM, p->stream>>>(p->tc_xmap, p->tc_mmap, tp);
+  SPCP_CHECK_LAUNCH("tc_eval_kernel");
+  if (p->prof) SPCP_CUDA(cudaEventRecord(p->ev1, p->stream));
+  p->launches++;
+  return SPCP_OK;
+}
+
+template <int KP16>
+static int tc_images(spcp_problem* p, int64_t k, const double* z, const double* dz,
+                     double alpha) {
+  constexpr int RB = KP16 * 2;
+  int rc;
+  if ((rc = p->tc_uimg.ensure(size_t(p->tc_nsb) * 3 * 128 * RB))) return rc;
+  if ((rc = p->tc_vimg.ensure(size_t(p->tc_ntc) * 3 * 64 * RB))) return rc;
+  const int64_t total = (p->m_pad + p->n_pad) * KP16;
+  tc_images_kernel<KP16><<<grid_for(total), 256, 0, p->stream>>>(
+      z, dz, alpha, p->m, p->n, k, p->m_pad, p->n_pad, p->tc_scales.as<TcScales>(),
+      p->tc_uimg.as<unsigned char>(), p->tc_vimg.as<unsigned char>());
+  SPCP_CHECK_LAUNCH("tc_images");
+  p->launches++;
+  return SPCP_OK;
+}
+
+static int tc_eval(spcp_problem* p, int64_t k, const double* z, const double* dz, double alpha,
+                   LaunchShape& sh) {
+  int rc;
+  if ((rc = tc_build(p))) return rc;
+  const int kp16 = k <= 16 ? 16 : (k <= 32 ? 32 : 64);
+  // operand scales (max |U|, |V| of the trial point -> powers of two)
+  TcScales* sc = p->tc_scales.as<TcScales>();
+  SPCP_CUDA(cudaMemsetAsync(&sc->max_bits[0], 0, 2 * sizeof(unsigned long long), p->stream));
+  const int64_t nu = p->m * k, nv = p->n * k;
+  tc_max_kernel<<<grid_for(nu + nv, 256, 148 * 4), 256, 0, p->stream>>>(z, dz, alpha, nu, nv, sc);
+  SPCP_CHECK_LAUNCH("tc_max");
+  tc_scales_kernel<<<1, 1, 0, p->stream>>>(sc, p->lambda_s);
+  SPCP_CHECK_LAUNCH("tc_scales");
+  p->launches += 2;
+  rc = kp16 == 16 ? tc_images<16>(p, k, z, dz, alpha)
+                  : (kp16 == 32 ? tc_images<32>(p, k, z, dz, alpha)
+                                : tc_images<64>(p, k, z, dz, alpha));
+  if (rc) return rc;
+  if ((rc = p->pleft.ensure(size_t(p->tc_runs) * 128 * k * sizeof(float)))) return rc;
+  if ((rc = p->pright.ensure(size_t(p->tc_slots) * 64 * k * sizeof(float)))) return rc;
+  if ((rc = p->pphi.ensure(size_t(p->tc_grid) * sizeof(double)))) return rc;
+  if (p->masked)
+    rc = kp16 == 16 ? tc_launch<16, true>(p, k)
+                    : (kp16 == 32 ? tc_launch<32, true>(p, k) : tc_launch<64, true>(p, k));
+  else
+    rc = kp16 == 16 ? tc_launch<16, false>(p, k)
+                    : (kp16 == 32 ? tc_launch<32, false>(p, k) : tc_launch<64, false>(p, k));
+  if (rc) return rc;
+  sh.tc = 1;
+  sh.kst = int(k);
+  sh.nchunks = 1;
+  sh.nrb = 1;
+  sh.chunk_cols = p->tc_grid;  // phi partial count
+  return SPCP_OK;
+}
+
 static int run_stream_eval(spcp_problem* p, int64_t k, int dtype, const double* z,
                            const double* dz, double alpha, int& kp_used, LaunchShape& sh,
                            int& part_dtype) {
@@ -297,6 +511,10 @@ static int run_stream_eval(spcp_problem* p, int64_t k, int dtype, const double* 
     return dense_fallback_eval(p, k, z, dz, alpha, sh);
   }
   int rc;
+  if (dtype == SPCP_F32 && k <= 64 && tc_env_enabled()) {
+    part_dtype = SPCP_F32;
+    return tc_eval(p, k, z, dz, alpha, sh);
+  }
   if (dtype == SPCP_F32) {
     part_dtype = SPCP_F32;
     if ((rc = prep<float>(p, k, kp, z, dz, alpha))) return rc;
@@ -489,6 +707,15 @@ static int run_reduce(spcp_problem* p, int64_t k, int kp, int part_dtype, const 
   rp.scal_sum = scal_sum;
   rp.scal_out = scal_out;
   rp.out = p->out_dev.as<double>();
+  if (sh.tc) {
+    const int32_t* csr = p->tc_csr.as<int32_t>();
+    rp.nphi = (u_mode == U_FROM_SUM) ? 0 : int(sh.chunk_cols);
+    rp.csr_u_off = csr + p->tc_csr_u_off;
+    rp.csr_u_idx = csr + p->tc_csr_u_idx;
+    rp.csr_v_off = csr + p->tc_csr_v_off;
+    rp.csr_v_idx = csr + p->tc_csr_v_idx;
+    rp.kst = sh.kst;
+  }
   if (part_dtype == SPCP_F32)
     reduce_kernel<float><<<nblk, 256, 0, p->stream>>>(rp);
   else
@@ -552,7 +779,7 @@ int spcp_problem_create(spcp_problem** out, int device, int64_t m, int64_t n, co
   p->m_pad = round_up(m, 128);
   p->n_pad = round_up(n, 64);
   p->ldx = p->n_pad;
-  p->ldm = round_up(ceil_div(p->n_pad, 32), 2);
+  p->ldm = round_up(ceil_div(p->n_pad, 32), 4);  // 16 B rows for TMA
   p->masked = mask != nullptr;
   p->lambda_l = lambda_l;
   p->lambda_s = lambda_s;

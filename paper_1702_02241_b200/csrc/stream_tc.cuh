@@ -1,0 +1,590 @@
+// stream_tc.cuh — the fused objective/gradient pass on the 5th-gen tensor
+// cores (fp32 mode, k <= 64).  One launch streams X once (TMA, SWIZZLE_128B)
+// and computes, per 128 x 64 tile (sub-band sb, column tile tc):
+//
+//   S   = U_sb V_tc^T                  tcgen05.mma, fp16 operands, fp32 in TMEM
+//   r   = x - S  (mask), g = -clip(r, +-tau), phi += huber(r)   (epilogue warps)
+//   GV += G V_tc      (A = G from TMEM, B = V image MN-major)   -> grad_U block
+//   GT  = G^T U_sb    (A = G image in smem MN-major, M = 64)    -> grad_V block
+//
+// Precision: operands are power-of-two scaled and split into
+// fp16 pieces computed in fp64 on the device: U'' = uh + um + ul, V'' = vh +
+// vm + vl, so the residual uses the 6 products of total order <= 2 (relative
+// error ~2^-33 before fp32 accumulation); G'' = gh + gl and the reductions
+// use gh.vh + gh.vm + gl.vh (~2^-22).  Each product is exact in the fp32
+// accumulator; scales are exact powers of two and are undone at the drain.
+//
+// Roles: warp 0 = TMA/bulk producer, warp 1 = MMA issuer (+TMEM owner),
+// warps 2..9 = epilogue (warp w owns TMEM lane quarter w % 4 and column half
+// (w - 2) / 4 of each tile).  Work: a static, exactly balanced range of tiles
+// per CTA (one CTA per SM) in 2-D super-block order; GV accumulates in TMEM
+// over a run of tiles with the same sub-band and is drained once per run,
+// GT is drained per tile and summed into a CTA-private slot per column tile
+// (read-modify-write in L2).  Partials are reduced in a fixed order later:
+// deterministic, no float atomics.
+#pragma once
+
+#include "common.cuh"
+#include "tc_common.cuh"
+
+namespace spcp {
+
+struct TcUnit {
+  uint16_t sb, tc;
+  int32_t gt_slot;
+  int32_t gv_slot;
+  uint32_t flags;
+};
+enum : uint32_t { TCU_FIRST_OF_RUN = 1u, TCU_LAST_OF_RUN = 2u, TCU_FIRST_TOUCH = 4u };
+
+struct TcScales {
+  float sigma;       // s_u * s_v: S'' = sigma * L
+  float tau_s;       // sigma * tau
+  float kappa;       // G'' = kappa * (sigma g)
+  float gv_unscale;  // 1 / (kappa sigma s_v)
+  float gt_unscale;  // 1 / (kappa sigma s_u)
+  float pad0;
+  double phi_unscale;  // 1 / sigma^2
+  double su, sv;
+  unsigned long long max_bits[2];  // |U|max, |V|max as double bit patterns
+};
+
+struct TcParams {
+  const TcUnit* units;
+  const int32_t* cta_begin;  // [grid + 1]
+  const unsigned char* u_img;
+  const unsigned char* v_img;
+  const TcScales* scales;
+  float* pleft;   // [gv_slots][128][kstore]
+  float* pright;  // [gt_slots][64][kstore]
+  double* pphi;   // [grid]
+  int kstore;
+};
+
+template <int KP16, bool MASK>
+struct TcCfg {
+  static constexpr int RB = KP16 * 2;           // operand image row bytes (32/64/128)
+  static constexpr uint32_t SWK = RB == 128 ? tc::SW_128 : (RB == 64 ? tc::SW_64 : tc::SW_32);
+  static constexpr int NST = KP16 == 64 ? 2 : (KP16 == 32 ? 3 : 4);
+  static constexpr int UB = KP16 == 64 ? 1 : 2;  // U image buffers
+  static constexpr int X_BYTES = 128 * 64 * 4;
+  static constexpr int V_SPLIT = 64 * RB;
+  static constexpr int V_BYTES = 3 * V_SPLIT;
+  static constexpr int U_SPLIT = 128 * RB;
+  static constexpr int U_BYTES = 3 * U_SPLIT;
+  static constexpr int M_BYTES = MASK ? 128 * 4 * 4 : 0;  // box {4 words, 128 rows}
+  static constexpr int G_BYTES = 128 * 64 * 2;  // one fp16 G image (MN-major SW128)
+  // smem carve (all offsets multiples of 1 KB)
+  static constexpr int OFF_X = 0;
+  static constexpr int OFF_V = OFF_X + NST * X_BYTES;
+  static constexpr int OFF_U = OFF_V + NST * V_BYTES;
+  static constexpr int OFF_GH = OFF_U + UB * U_BYTES;
+  static constexpr int OFF_GL = OFF_GH + G_BYTES;
+  static constexpr int OFF_M = OFF_GL + G_BYTES;
+  static constexpr int OFF_BAR = OFF_M + NST * 2048;
+  static constexpr int SMEM = OFF_BAR + 1024 + 1024;  // barriers + 1 KB alignment slack
+  // TMEM columns
+  static constexpr uint32_t T_S = 0, T_GA = 128, T_GV = 256, T_GT = 256 + 2 * KP16;
+  static constexpr uint32_t TMEM_COLS = 512;
+  static constexpr int NEPI = 8;  // epilogue warps
+  static constexpr int NTHREADS = 32 * (2 + NEPI);
+};
+
+struct TcBarriers {
+  uint64_t stage_full[4], stage_empty[4];
+  uint64_t u_full[2], u_empty[2];
+  uint64_t s_full[2], s_empty[2];
+  uint64_t ga_full[2], ga_empty[2];
+  uint64_t gs_empty;
+  uint64_t gt_full[2], gt_empty[2];
+  uint64_t gv_full[2], gv_empty[2];
+  uint32_t tmem_base;
+  double phi[8];
+};
+
+__device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
+  __half2 h = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+template <int KP16, bool MASK>
+__global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
+    tc_eval_kernel(const __grid_constant__ CUtensorMap xmap,
+                   const __grid_constant__ CUtensorMap mmap, const TcParams p) {
+  using C = TcCfg<KP16, MASK>;
+  using namespace tc;
+  extern __shared__ unsigned char smem_dyn[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+  TcBarriers* bar = reinterpret_cast<TcBarriers*>(sm + C::OFF_BAR);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ub = p.cta_begin[blockIdx.x], ue = p.cta_begin[blockIdx.x + 1];
+  const int T = ue - ub;
+  const TcUnit* units = p.units + ub;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::NST; ++i) {
+      mbar_init(&bar->stage_full[i], 1);
+      mbar_init(&bar->stage_empty[i], C::NEPI + 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bar->u_full[i], 1);
+      mbar_init(&bar->u_empty[i], 1);
+      mbar_init(&bar->s_full[i], 1);
+      mbar_init(&bar->s_empty[i], C::NEPI);
+      mbar_init(&bar->ga_full[i], C::NEPI);
+      mbar_init(&bar->ga_empty[i], 1);
+      mbar_init(&bar->gt_full[i], 1);
+      mbar_init(&bar->gt_empty[i], C::NEPI);
+      mbar_init(&bar->gv_full[i], 1);
+      mbar_init(&bar->gv_empty[i], C::NEPI);
+    }
+    mbar_init(&bar->gs_empty, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(&bar->tmem_base, C::TMEM_COLS);
+  if (warp == 0 && lane == 0) {
+    prefetch_tensormap(&xmap);
+    if (MASK) prefetch_tensormap(&mmap);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = bar->tmem_base;
+
+  if (warp == 0) {
+    // ======================= producer ===================================
+    if (lane == 0) {
+      int prev_sb = -1, fills = 0;
+      for (int t = 0; t < T; ++t) {
+        const TcUnit un = units[t];
+        if ((un.flags & TCU_FIRST_OF_RUN) || un.sb != prev_sb) {
+          const int b = fills % C::UB;
+          mbar_wait(&bar->u_empty[b], ((fills / C::UB) & 1) ^ 1);
+          mbar_arrive_expect_tx(&bar->u_full[b], C::U_BYTES);
+          bulk_load(sm + C::OFF_U + b * C::U_BYTES, p.u_img + size_t(un.sb) * C::U_BYTES,
+                    C::U_BYTES, &bar->u_full[b]);
+          ++fills;
+          prev_sb = un.sb;
+        }
+        const int st = t % C::NST;
+        mbar_wait(&bar->stage_empty[st], ((t / C::NST) & 1) ^ 1);
+        mbar_arrive_expect_tx(&bar->stage_full[st], C::X_BYTES + C::V_BYTES + C::M_BYTES);
+        unsigned char* xs = sm + C::OFF_X + st * C::X_BYTES;
+        tma_load_2d(xs, &xmap, int(un.tc) * 64, int(un.sb) * 128, &bar->stage_full[st]);
+        tma_load_2d(xs + 16384, &xmap, int(un.tc) * 64 + 32, int(un.sb) * 128,
+                    &bar->stage_full[st]);
+        bulk_load(sm + C::OFF_V + st * C::V_BYTES, p.v_img + size_t(un.tc) * C::V_BYTES,
+                  C::V_BYTES, &bar->stage_full[st]);
+        if (MASK)
+          tma_load_2d(sm + C::OFF_M + st * 2048, &mmap, (int(un.tc) * 2) & ~3, int(un.sb) * 128,
+                      &bar->stage_full[st]);
+      }
+    }
+  } else if (warp == 1) {
+    // ======================= MMA issuer =================================
+    constexpr uint32_t ID_RES = idesc_f16(128, 64, false, false);
+    constexpr uint32_t ID_GV = idesc_f16(128, KP16, false, true);
+    constexpr uint32_t ID_GT = idesc_f16(64, KP16, true, true);
+    constexpr int KS = KP16 / 16;
+    const uint32_t u0 = smem_u32(sm + C::OFF_U), v0 = smem_u32(sm + C::OFF_V);
+    const uint32_t gh0 = smem_u32(sm + C::OFF_GH), gl0 = smem_u32(sm + C::OFF_GL);
+    int run = -1;       // run index of the tile being issued (residual)
+    int red_run = -1;   // run index of the tile being reduced
+    int prev_sb = -1;
+
+    auto residual = [&](int t, int ubuf) {
+      const int st = t % C::NST, b = t & 1;
+      mbar_wait(&bar->stage_full[st], (t / C::NST) & 1);
+      mbar_wait(&bar->s_empty[b], ((t >> 1) & 1) ^ 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t ua = u0 + ubuf * C::U_BYTES;
+        const uint32_t vb = v0 + st * C::V_BYTES;
+        // products of total split order <= 2: (h,h) (h,m) (m,h) (h,l) (m,m) (l,h)
+        const int pa[6] = {0, 0, 1, 0, 1, 2};
+        const int pb[6] = {0, 1, 0, 2, 1, 0};
+#pragma unroll
+        for (int q = 0; q < 6; ++q)
+#pragma unroll
+          for (int ks = 0; ks < KS; ++ks)
+            mma_ss(tm + C::T_S + b * 64,
+                   umma_desc(ua + pa[q] * C::U_SPLIT + ks * 32, 16, 8 * C::RB, C::SWK),
+                   umma_desc(vb + pb[q] * C::V_SPLIT + ks * 32, 16, 8 * C::RB, C::SWK), ID_RES,
+                   (q | ks) != 0);
+        mma_commit(&bar->s_full[b]);
+      }
+      __syncwarp();
+    };
+
+    auto reductions = [&](int t, int ubuf, int rrun, uint32_t flags) {
+      const int st = t % C::NST, b = t & 1, gvb = rrun & 1;
+      mbar_wait(&bar->ga_full[b], (t >> 1) & 1);
+      if (flags & TCU_FIRST_OF_RUN) mbar_wait(&bar->gv_empty[gvb], ((rrun >> 1) & 1) ^ 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t vb = v0 + st * C::V_BYTES;
+        const uint32_t gv = tm + C::T_GV + gvb * KP16;
+        const uint32_t ga = tm + C::T_GA + b * 64;
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const uint32_t vo = ks * 16 * C::RB;
+          mma_ts(gv, ga + 8 * ks, umma_desc(vb + vo, 8192, 8 * C::RB, C::SWK), ID_GV,
+                 !((flags & TCU_FIRST_OF_RUN) && ks == 0));
+          mma_ts(gv, ga + 8 * ks, umma_desc(vb + C::V_SPLIT + vo, 8192, 8 * C::RB, C::SWK),
+                 ID_GV, 1);
+          mma_ts(gv, ga + 32 + 8 * ks, umma_desc(vb + vo, 8192, 8 * C::RB, C::SWK), ID_GV, 1);
+        }
+        mma_commit(&bar->ga_empty[b]);
+        mma_commit(&bar->stage_empty[st]);
+      }
+      __syncwarp();
+      mbar_wait(&bar->gt_empty[b], ((t >> 1) & 1) ^ 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t ua = u0 + ubuf * C::U_BYTES;
+        const uint32_t gt = tm + C::T_GT + b * KP16;
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          const uint32_t uo = ks * 16 * C::RB;
+          mma_ss(gt, umma_desc(gh0 + 2048 * ks, 16384, 1024, SW_128),
+                 umma_desc(ua + uo, 8192, 8 * C::RB, C::SWK), ID_GT, ks > 0);
+          mma_ss(gt, umma_desc(gh0 + 2048 * ks, 16384, 1024, SW_128),
+                 umma_desc(ua + C::U_SPLIT + uo, 8192, 8 * C::RB, C::SWK), ID_GT, 1);
+          mma_ss(gt, umma_desc(gl0 + 2048 * ks, 16384, 1024, SW_128),
+                 umma_desc(ua + uo, 8192, 8 * C::RB, C::SWK), ID_GT, 1);
+        }
+        mma_commit(&bar->gt_full[b]);
+        mma_commit(&bar->gs_empty);
+        if (flags & TCU_LAST_OF_RUN) {
+          mma_commit(&bar->gv_full[gvb]);
+          mma_commit(&bar->u_empty[ubuf]);
+        }
+      }
+      __syncwarp();
+    };
+
+    int ubuf_of_t[2] = {0, 0};  // U buffer used by tiles t (ring of 2)
+    int run_of_t[2] = {0, 0};
+    uint32_t flags_of_t[2] = {0, 0};
+    for (int t = 0; t <= T; ++t) {
+      if (t < T) {
+        const TcUnit un = units[t];
+        const bool new_run = (un.flags & TCU_FIRST_OF_RUN) || un.sb != prev_sb;
+        if (new_run) {
+          ++run;
+          prev_sb = un.sb;
+        }
+        const int ubuf = run % C::UB;
+        ubuf_of_t[t & 1] = ubuf;
+        run_of_t[t & 1] = run;
+        flags_of_t[t & 1] = un.flags;
+        const bool reduce_first = new_run && C::UB == 1 && t >= 1;
+        if (reduce_first) {
+          reductions(t - 1, ubuf_of_t[(t - 1) & 1], run_of_t[(t - 1) & 1],
+                     flags_of_t[(t - 1) & 1]);
+        }
+        if (new_run) mbar_wait(&bar->u_full[ubuf], (run / C::UB) & 1);
+        residual(t, ubuf);
+        if (!reduce_first && t >= 1)
+          reductions(t - 1, ubuf_of_t[(t - 1) & 1], run_of_t[(t - 1) & 1],
+                     flags_of_t[(t - 1) & 1]);
+      } else if (T >= 1) {
+        reductions(T - 1, ubuf_of_t[(T - 1) & 1], run_of_t[(T - 1) & 1],
+                   flags_of_t[(T - 1) & 1]);
+      }
+    }
+    (void)red_run;
+  } else {
+    // ======================= epilogue warps =============================
+    const int q = warp & 3;
+    const int h = (warp - 2) >> 2;
+    const int row = 32 * q + lane;
+    const uint32_t lane_addr = uint32_t(32 * q) << 16;
+    const TcScales sc = *p.scales;
+    const float sigma = sc.sigma, tau_s = sc.tau_s, kappa = sc.kappa;
+    double phi_acc = 0.0;
+    int run = -1, prev_sb = -1;
+    int prev_gv_slot = -1;
+    const int kst = p.kstore;
+    constexpr int GTC = KP16 / 2;  // GT columns drained per warp half
+
+    auto drain_gt = [&](int t2, const TcUnit& u2) {
+      const int b = t2 & 1;
+      // prefetch-free RMW: only lanes < 16 hold rows of the M = 64 accumulator
+      mbar_wait(&bar->gt_full[b], (t2 >> 1) & 1);
+      tc_fence_after();
+      uint32_t v[GTC > 16 ? GTC : 16];
+#pragma unroll
+      for (int c0 = 0; c0 < GTC; c0 += 16) {
+        uint32_t r16[16];
+        tmem_ld16(tm + lane_addr + C::T_GT + b * KP16 + h * GTC + c0, r16);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[c0 + i] = r16[i];
+      }
+      if (GTC < 16) {
+        uint32_t r16[16];
+        tmem_ld16(tm + lane_addr + C::T_GT + b * KP16 + h * GTC, r16);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = r16[i];
+      }
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar->gt_empty[b]);
+      if (lane < 16) {
+        const int j = 16 * q + lane;  // row of G^T U = column within the tile
+        float* dst = p.pright + (size_t(u2.gt_slot) * 64 + j) * kst;
+        const bool first = (u2.flags & TCU_FIRST_TOUCH) != 0;
+#pragma unroll
+        for (int c = 0; c < GTC; ++c) {
+          const int col = h * GTC + c;
+          if (col < kst) {
+            const float val = __uint_as_float(v[c]) * sc.gt_unscale;
+            dst[col] = first ? val : dst[col] + val;
+          }
+        }
+      }
+    };
+
+    auto drain_gv = [&](int rrun, int slot) {
+      const int gvb = rrun & 1;
+      mbar_wait(&bar->gv_full[gvb], (rrun >> 1) & 1);
+      tc_fence_after();
+      uint32_t v[GTC > 16 ? GTC : 16];
+#pragma unroll
+      for (int c0 = 0; c0 < GTC; c0 += 16) {
+        uint32_t r16[16];
+        tmem_ld16(tm + lane_addr + C::T_GV + gvb * KP16 + h * GTC + c0, r16);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[c0 + i] = r16[i];
+      }
+      if (GTC < 16) {
+        uint32_t r16[16];
+        tmem_ld16(tm + lane_addr + C::T_GV + gvb * KP16 + h * GTC, r16);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = r16[i];
+      }
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar->gv_empty[gvb]);
+      float* dst = p.pleft + (size_t(slot) * 128 + row) * kst;
+#pragma unroll
+      for (int c = 0; c < GTC; ++c) {
+        const int col = h * GTC + c;
+        if (col < kst) dst[col] = __uint_as_float(v[c]) * sc.gv_unscale;
+      }
+    };
+
+    TcUnit prev_unit{};
+    for (int t = 0; t < T; ++t) {
+      const TcUnit un = units[t];
+      const bool new_run = (un.flags & TCU_FIRST_OF_RUN) || un.sb != prev_sb;
+      if (new_run) {
+        ++run;
+        prev_sb = un.sb;
+      }
+      const int st = t % C::NST, b = t & 1;
+      // ---- S tile and X tile
+      mbar_wait(&bar->s_full[b], (t >> 1) & 1);
+      tc_fence_after();
+      uint32_t s0[16], s1[16];
+      tmem_ld16(tm + lane_addr + C::T_S + b * 64 + 32 * h, s0);
+      tmem_ld16(tm + lane_addr + C::T_S + b * 64 + 32 * h + 16, s1);
+      mbar_wait(&bar->stage_full[st], (t / C::NST) & 1);
+      const unsigned char* xs = sm + C::OFF_X + st * C::X_BYTES + h * 16384;
+      float xv[32];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float4 f = *reinterpret_cast<const float4*>(xs + Swz<128>::offset(row, c * 16));
+        xv[4 * c] = f.x;
+        xv[4 * c + 1] = f.y;
+        xv[4 * c + 2] = f.z;
+        xv[4 * c + 3] = f.w;
+      }
+      uint32_t mw = 0xffffffffu;
+      if (MASK)
+        mw = reinterpret_cast<const uint32_t*>(sm + C::OFF_M + st * 2048)[row * 4 +
+                                                                          (un.tc & 1) * 2 + h];
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&bar->s_empty[b]);
+        mbar_arrive(&bar->stage_empty[st]);
+      }
+      // ---- epilogue math: r = x - L (scaled), clip, huber, split
+      uint32_t hi[16], lo[16];
+      float hsum = 0.f;
+#pragma unroll
+      for (int e = 0; e < 32; e += 2) {
+        float g2[2];
+#pragma unroll
+        for (int f = 0; f < 2; ++f) {
+          const int c = e + f;
+          const float sv = __uint_as_float(c < 16 ? s0[c] : s1[c - 16]);
+          float r = fmaf(xv[c], sigma, -sv);
+          if (MASK) r = ((mw >> c) & 1u) ? r : 0.f;
+          const float a = fabsf(r);
+          const float cl = fminf(a, tau_s);
+          hsum = fmaf(cl, fmaf(-0.5f, cl, a), hsum);
+          g2[f] = -copysignf(cl, r) * kappa;
+        }
+        const __half2 hh = __floats2half2_rn(g2[0], g2[1]);
+        const float2 hf = __half22float2(hh);
+        hi[e >> 1] = *reinterpret_cast<const uint32_t*>(&hh);
+        lo[e >> 1] = pack_half2(g2[0] - hf.x, g2[1] - hf.y);
+      }
+      phi_acc += double(hsum);
+      // ---- G to TMEM (A of G.V) and to smem (A of G^T.U)
+      mbar_wait(&bar->ga_empty[b], ((t >> 1) & 1) ^ 1);
+      tmem_st16(tm + lane_addr + C::T_GA + b * 64 + 16 * h, hi);
+      tmem_st16(tm + lane_addr + C::T_GA + b * 64 + 32 + 16 * h, lo);
+      mbar_wait(&bar->gs_empty, (t & 1) ^ 1);
+      unsigned char* gh = sm + C::OFF_GH;
+      unsigned char* gl = sm + C::OFF_GL;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint32_t o = Swz<128>::offset(row, 64 * h + 16 * c);
+        *reinterpret_cast<uint4*>(gh + o) = make_uint4(hi[4 * c], hi[4 * c + 1], hi[4 * c + 2],
+                                                       hi[4 * c + 3]);
+        *reinterpret_cast<uint4*>(gl + o) = make_uint4(lo[4 * c], lo[4 * c + 1], lo[4 * c + 2],
+                                                       lo[4 * c + 3]);
+      }
+      tmem_wait_st();
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar->ga_full[b]);
+      // ---- deferred drains
+      if (t >= 1) drain_gt(t - 1, prev_unit);
+      if (new_run && t >= 1) drain_gv(run - 1, prev_gv_slot);
+      prev_unit = un;
+      prev_gv_slot = un.gv_slot;
+    }
+    if (T >= 1) {
+      drain_gt(T - 1, prev_unit);
+      drain_gv(run, prev_gv_slot);
+    }
+    // phi: per-thread fp64, fold over the epilogue warps in a fixed order
+    double w = warp_sum(phi_acc);
+    if (lane == 0) bar->phi[warp - 2] = w;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < C::NEPI; ++i) s += bar->phi[i];
+    p.pphi[blockIdx.x] = s * p.scales->phi_unscale;
+  }
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tm, C::TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------ prep
+// pass 1: max |w| over the U and V parts of the trial point (bit patterns of
+// non-negative doubles order like unsigned integers).
+__global__ void tc_max_kernel(const double* __restrict__ z, const double* __restrict__ dz,
+                              double alpha, int64_t nu, int64_t nv, TcScales* sc) {
+  unsigned long long mu = 0, mv = 0;
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < nu + nv;
+       q += int64_t(gridDim.x) * blockDim.x) {
+    double w = z[q];
+    if (dz) w += alpha * dz[q];
+    const unsigned long long bits = __double_as_longlong(fabs(w));
+    if (q < nu)
+      mu = bits > mu ? bits : mu;
+    else
+      mv = bits > mv ? bits : mv;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long a = __shfl_xor_sync(0xffffffffu, mu, o);
+    const unsigned long long b = __shfl_xor_sync(0xffffffffu, mv, o);
+    mu = a > mu ? a : mu;
+    mv = b > mv ? b : mv;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&sc->max_bits[0], mu);
+    atomicMax(&sc->max_bits[1], mv);
+  }
+}
+
+// pass 2: power-of-two scales (one thread)
+__global__ void tc_scales_kernel(TcScales* sc, double tau) {
+  const double mu = __longlong_as_double(sc->max_bits[0]);
+  const double mv = __longlong_as_double(sc->max_bits[1]);
+  auto pow2_for = [](double mx) {  // largest 2^e with mx * 2^e <= 2^14
+    if (!(mx > 0.0)) return 1.0;
+    int e;
+    frexp(mx, &e);  // mx = f * 2^e, f in [0.5, 1)
+    return ldexp(1.0, 14 - e);
+  };
+  const double su = pow2_for(mu), sv = pow2_for(mv);
+  const double sigma = su * sv;
+  const double taus = sigma * tau;
+  int e;
+  frexp(taus, &e);
+  const double kappa = ldexp(1.0, 14 - e);
+  sc->su = su;
+  sc->sv = sv;
+  sc->sigma = float(sigma);
+  sc->tau_s = float(taus);
+  sc->kappa = float(kappa);
+  sc->gv_unscale = float(1.0 / (kappa * sigma * sv));
+  sc->gt_unscale = float(1.0 / (kappa * sigma * su));
+  sc->phi_unscale = 1.0 / (sigma * sigma);
+}
+
+template <int RB>
+__device__ __forceinline__ void split3_store(unsigned char* base, int split_bytes, int row, int c,
+                                             double x) {
+  const __half h = __double2half(x);
+  const double r1 = x - double(__half2float(h));
+  const __half m = __double2half(r1);
+  const double r2 = r1 - double(__half2float(m));
+  const __half l = __double2half(r2);
+  const uint32_t o = tc::Swz<RB>::offset(row, c * 2);
+  *reinterpret_cast<__half*>(base + o) = h;
+  *reinterpret_cast<__half*>(base + split_bytes + o) = m;
+  *reinterpret_cast<__half*>(base + 2 * split_bytes + o) = l;
+}
+
+// pass 3: fp16 split images of U (per 128-row sub-band) and V (per 64-row tile)
+template <int KP16>
+__global__ void tc_images_kernel(const double* __restrict__ z, const double* __restrict__ dz,
+                                 double alpha, int64_t m, int64_t n, int64_t k, int64_t m_pad,
+                                 int64_t n_pad, const TcScales* sc, unsigned char* u_img,
+                                 unsigned char* v_img) {
+  constexpr int RB = KP16 * 2;
+  const double su = sc->su, sv = sc->sv;
+  const int64_t total = (m_pad + n_pad) * KP16;
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < total;
+       q += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t row = q / KP16;
+    const int c = int(q % KP16);
+    if (row < m_pad) {
+      double w = 0.0;
+      if (row < m && c < k) {
+        const int64_t o = row * k + c;
+        w = z[o] + (dz ? alpha * dz[o] : 0.0);
+      }
+      const int64_t sb = row >> 7;
+      split3_store<RB>(u_img + sb * (3 * 128 * RB), 128 * RB, int(row & 127), c, w * su);
+    } else {
+      const int64_t j = row - m_pad;
+      double w = 0.0;
+      if (j < n && c < k) {
+        const int64_t o = m * k + j * k + c;
+        w = z[o] + (dz ? alpha * dz[o] : 0.0);
+      }
+      const int64_t tcol = j >> 6;
+      split3_store<RB>(v_img + tcol * (3 * 64 * RB), 64 * RB, int(j & 63), c, w * sv);
+    }
+  }
+}
+
+}  // namespace spcp
