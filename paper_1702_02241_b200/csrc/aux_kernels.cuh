@@ -142,7 +142,8 @@ struct ReduceParams {
   const int32_t* csr_u_idx;
   const int32_t* csr_v_off;
   const int32_t* csr_v_idx;
-  int kst;
+  int kst;                  // partial row stride (the kernel's padded rank)
+  const float* tc_unscale;  // [0]: G.V partials, [1]: G^T.U partials
 };
 
 template <typename T>
@@ -167,6 +168,7 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p) {
           const float* plf = reinterpret_cast<const float*>(p.pleft);
           for (int e = p.csr_u_off[sb]; e < p.csr_u_off[sb + 1]; ++e)
             acc += double(plf[(int64_t(p.csr_u_idx[e]) * 128 + (i & 127)) * p.kst + c]);
+          acc *= double(p.tc_unscale[0]);
         } else {
           for (int ch = 0; ch < p.nchunks; ++ch)
             acc += double(pl[(int64_t(ch) * p.m_pad + i) * p.kp + c]);
@@ -196,6 +198,7 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p) {
         const float* prf = reinterpret_cast<const float*>(p.pright);
         for (int e = p.csr_v_off[tcol]; e < p.csr_v_off[tcol + 1]; ++e)
           acc += double(prf[(int64_t(p.csr_v_idx[e]) * 64 + (j & 63)) * p.kst + c]);
+        acc *= double(p.tc_unscale[1]);
       } else {
         for (int b = 0; b < p.nrb; ++b) acc += double(pr[(int64_t(b) * p.n_pad + j) * p.kp + c]);
       }

@@ -481,8 +481,8 @@ static int tc_eval(spcp_problem* p, int64_t k, const double* z, const double* dz
                   : (kp16 == 32 ? tc_images<32>(p, k, z, dz, alpha)
                                 : tc_images<64>(p, k, z, dz, alpha));
   if (rc) return rc;
-  if ((rc = p->pleft.ensure(size_t(p->tc_runs) * 128 * k * sizeof(float)))) return rc;
-  if ((rc = p->pright.ensure(size_t(p->tc_slots) * 64 * k * sizeof(float)))) return rc;
+  if ((rc = p->pleft.ensure(size_t(p->tc_runs) * 128 * kp16 * sizeof(float)))) return rc;
+  if ((rc = p->pright.ensure(size_t(p->tc_slots) * 64 * kp16 * sizeof(float)))) return rc;
   if ((rc = p->pphi.ensure(size_t(p->tc_grid) * sizeof(double)))) return rc;
   if (p->masked)
     rc = kp16 == 16 ? tc_launch<16, true>(p, k)
@@ -492,7 +492,7 @@ static int tc_eval(spcp_problem* p, int64_t k, const double* z, const double* dz
                     : (kp16 == 32 ? tc_launch<32, false>(p, k) : tc_launch<64, false>(p, k));
   if (rc) return rc;
   sh.tc = 1;
-  sh.kst = int(k);
+  sh.kst = kp16;
   sh.nchunks = 1;
   sh.nrb = 1;
   sh.chunk_cols = p->tc_grid;  // phi partial count
@@ -715,6 +715,7 @@ static int run_reduce(spcp_problem* p, int64_t k, int kp, int part_dtype, const 
     rp.csr_v_off = csr + p->tc_csr_v_off;
     rp.csr_v_idx = csr + p->tc_csr_v_idx;
     rp.kst = sh.kst;
+    rp.tc_unscale = &p->tc_scales.as<TcScales>()->gv_unscale;
   }
   if (part_dtype == SPCP_F32)
     reduce_kernel<float><<<nblk, 256, 0, p->stream>>>(rp);

@@ -81,8 +81,10 @@ struct TcCfg {
   static constexpr int OFF_GH = OFF_U + UB * U_BYTES;
   static constexpr int OFF_GL = OFF_GH + G_BYTES;
   static constexpr int OFF_M = OFF_GL + G_BYTES;
-  static constexpr int OFF_BAR = OFF_M + NST * 2048;
-  static constexpr int SMEM = OFF_BAR + 1024 + 1024;  // barriers + 1 KB alignment slack
+  static constexpr int OFF_STG = OFF_M + (MASK ? NST * 2048 : 0);
+  static constexpr int STG_BYTES = 64 * KP16 * 4;  // G^T U tile staged for the bulk reduce
+  static constexpr int OFF_BAR = OFF_STG + STG_BYTES;
+  static constexpr int SMEM = OFF_BAR + 512;  // dynamic smem base is 1 KB aligned
   // TMEM columns
   static constexpr uint32_t T_S = 0, T_GA = 128, T_GV = 256, T_GT = 256 + 2 * KP16;
   static constexpr uint32_t TMEM_COLS = 512;
@@ -113,9 +115,9 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
                    const __grid_constant__ CUtensorMap mmap, const TcParams p) {
   using C = TcCfg<KP16, MASK>;
   using namespace tc;
-  extern __shared__ unsigned char smem_dyn[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) unsigned char smem_dyn[];
+  unsigned char* sm = smem_dyn;
+  if ((smem_u32(sm) & 1023u) != 0u) __trap();  // swizzled TMA/UMMA images need 1 KB alignment
   TcBarriers* bar = reinterpret_cast<TcBarriers*>(sm + C::OFF_BAR);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ub = p.cta_begin[blockIdx.x], ue = p.cta_begin[blockIdx.x + 1];
@@ -190,7 +192,6 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
     const uint32_t u0 = smem_u32(sm + C::OFF_U), v0 = smem_u32(sm + C::OFF_V);
     const uint32_t gh0 = smem_u32(sm + C::OFF_GH), gl0 = smem_u32(sm + C::OFF_GL);
     int run = -1;       // run index of the tile being issued (residual)
-    int red_run = -1;   // run index of the tile being reduced
     int prev_sb = -1;
 
     auto residual = [&](int t, int ubuf) {
@@ -220,28 +221,12 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
     auto reductions = [&](int t, int ubuf, int rrun, uint32_t flags) {
       const int st = t % C::NST, b = t & 1, gvb = rrun & 1;
       mbar_wait(&bar->ga_full[b], (t >> 1) & 1);
+      mbar_wait(&bar->gt_empty[b], ((t >> 1) & 1) ^ 1);
       if (flags & TCU_FIRST_OF_RUN) mbar_wait(&bar->gv_empty[gvb], ((rrun >> 1) & 1) ^ 1);
       tc_fence_after();
       if (elect_one()) {
-        const uint32_t vb = v0 + st * C::V_BYTES;
-        const uint32_t gv = tm + C::T_GV + gvb * KP16;
-        const uint32_t ga = tm + C::T_GA + b * 64;
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-          const uint32_t vo = ks * 16 * C::RB;
-          mma_ts(gv, ga + 8 * ks, umma_desc(vb + vo, 8192, 8 * C::RB, C::SWK), ID_GV,
-                 !((flags & TCU_FIRST_OF_RUN) && ks == 0));
-          mma_ts(gv, ga + 8 * ks, umma_desc(vb + C::V_SPLIT + vo, 8192, 8 * C::RB, C::SWK),
-                 ID_GV, 1);
-          mma_ts(gv, ga + 32 + 8 * ks, umma_desc(vb + vo, 8192, 8 * C::RB, C::SWK), ID_GV, 1);
-        }
-        mma_commit(&bar->ga_empty[b]);
-        mma_commit(&bar->stage_empty[st]);
-      }
-      __syncwarp();
-      mbar_wait(&bar->gt_empty[b], ((t >> 1) & 1) ^ 1);
-      tc_fence_after();
-      if (elect_one()) {
+        // G^T U first: it releases the single G staging image the epilogue
+        // needs for the next tile
         const uint32_t ua = u0 + ubuf * C::U_BYTES;
         const uint32_t gt = tm + C::T_GT + b * KP16;
 #pragma unroll
@@ -256,6 +241,20 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
         }
         mma_commit(&bar->gt_full[b]);
         mma_commit(&bar->gs_empty);
+        const uint32_t vb = v0 + st * C::V_BYTES;
+        const uint32_t gv = tm + C::T_GV + gvb * KP16;
+        const uint32_t ga = tm + C::T_GA + b * 64;
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const uint32_t vo = ks * 16 * C::RB;
+          mma_ts(gv, ga + 8 * ks, umma_desc(vb + vo, 8192, 8 * C::RB, C::SWK), ID_GV,
+                 !((flags & TCU_FIRST_OF_RUN) && ks == 0));
+          mma_ts(gv, ga + 8 * ks, umma_desc(vb + C::V_SPLIT + vo, 8192, 8 * C::RB, C::SWK),
+                 ID_GV, 1);
+          mma_ts(gv, ga + 32 + 8 * ks, umma_desc(vb + vo, 8192, 8 * C::RB, C::SWK), ID_GV, 1);
+        }
+        mma_commit(&bar->ga_empty[b]);
+        mma_commit(&bar->stage_empty[st]);
         if (flags & TCU_LAST_OF_RUN) {
           mma_commit(&bar->gv_full[gvb]);
           mma_commit(&bar->u_empty[ubuf]);
@@ -264,37 +263,27 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
       __syncwarp();
     };
 
-    int ubuf_of_t[2] = {0, 0};  // U buffer used by tiles t (ring of 2)
-    int run_of_t[2] = {0, 0};
-    uint32_t flags_of_t[2] = {0, 0};
-    for (int t = 0; t <= T; ++t) {
-      if (t < T) {
-        const TcUnit un = units[t];
-        const bool new_run = (un.flags & TCU_FIRST_OF_RUN) || un.sb != prev_sb;
-        if (new_run) {
-          ++run;
-          prev_sb = un.sb;
-        }
-        const int ubuf = run % C::UB;
-        ubuf_of_t[t & 1] = ubuf;
-        run_of_t[t & 1] = run;
-        flags_of_t[t & 1] = un.flags;
-        const bool reduce_first = new_run && C::UB == 1 && t >= 1;
-        if (reduce_first) {
-          reductions(t - 1, ubuf_of_t[(t - 1) & 1], run_of_t[(t - 1) & 1],
-                     flags_of_t[(t - 1) & 1]);
-        }
-        if (new_run) mbar_wait(&bar->u_full[ubuf], (run / C::UB) & 1);
-        residual(t, ubuf);
-        if (!reduce_first && t >= 1)
-          reductions(t - 1, ubuf_of_t[(t - 1) & 1], run_of_t[(t - 1) & 1],
-                     flags_of_t[(t - 1) & 1]);
-      } else if (T >= 1) {
-        reductions(T - 1, ubuf_of_t[(T - 1) & 1], run_of_t[(T - 1) & 1],
-                   flags_of_t[(T - 1) & 1]);
+    // bookkeeping of the previous tile (its reductions trail its residual)
+    int p_ubuf = 0, p_run = 0;
+    uint32_t p_flags = 0;
+    for (int t = 0; t < T; ++t) {
+      const TcUnit un = units[t];
+      const bool new_run = (un.flags & TCU_FIRST_OF_RUN) || un.sb != prev_sb;
+      if (new_run) {
+        ++run;
+        prev_sb = un.sb;
       }
+      const int ubuf = run % C::UB;
+      const bool reduce_first = new_run && C::UB == 1 && t >= 1;
+      if (reduce_first) reductions(t - 1, p_ubuf, p_run, p_flags);
+      if (new_run) mbar_wait(&bar->u_full[ubuf], (run / C::UB) & 1);
+      residual(t, ubuf);
+      if (!reduce_first && t >= 1) reductions(t - 1, p_ubuf, p_run, p_flags);
+      p_ubuf = ubuf;
+      p_run = run;
+      p_flags = un.flags;
     }
-    (void)red_run;
+    if (T >= 1) reductions(T - 1, p_ubuf, p_run, p_flags);
   } else {
     // ======================= epilogue warps =============================
     const int q = warp & 3;
@@ -306,44 +295,47 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
     double phi_acc = 0.0;
     int run = -1, prev_sb = -1;
     int prev_gv_slot = -1;
-    const int kst = p.kstore;
     constexpr int GTC = KP16 / 2;  // GT columns drained per warp half
 
+    // G^T U of tile t2 -> staging tile -> one TMA bulk store (first touch of
+    // the slot) or fp32 bulk reduce-add into this CTA's private slot.  The
+    // leader waits for all earlier bulk ops first: the staging tile is free
+    // and adds into one slot land in program order (deterministic).
+    float* stg = reinterpret_cast<float*>(sm + C::OFF_STG);
+    const bool leader = threadIdx.x == 64;
     auto drain_gt = [&](int t2, const TcUnit& u2) {
       const int b = t2 & 1;
-      // prefetch-free RMW: only lanes < 16 hold rows of the M = 64 accumulator
       mbar_wait(&bar->gt_full[b], (t2 >> 1) & 1);
       tc_fence_after();
-      uint32_t v[GTC > 16 ? GTC : 16];
+      uint32_t v[GTC >= 16 ? GTC : 16];
 #pragma unroll
-      for (int c0 = 0; c0 < GTC; c0 += 16) {
+      for (int c0 = 0; c0 < (GTC >= 16 ? GTC : 16); c0 += 16) {
         uint32_t r16[16];
         tmem_ld16(tm + lane_addr + C::T_GT + b * KP16 + h * GTC + c0, r16);
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[c0 + i] = r16[i];
       }
-      if (GTC < 16) {
-        uint32_t r16[16];
-        tmem_ld16(tm + lane_addr + C::T_GT + b * KP16 + h * GTC, r16);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = r16[i];
-      }
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar->gt_empty[b]);
-      if (lane < 16) {
-        const int j = 16 * q + lane;  // row of G^T U = column within the tile
-        float* dst = p.pright + (size_t(u2.gt_slot) * 64 + j) * kst;
-        const bool first = (u2.flags & TCU_FIRST_TOUCH) != 0;
+      if (leader) bulk_wait_all();
+      named_bar_sync(1, 32 * C::NEPI);
+      if (lane < 16) {  // M = 64 accumulator: row j = 16 q + lane lives in lanes 0..15
+        float* srow = stg + (16 * q + lane) * KP16 + h * GTC;
 #pragma unroll
-        for (int c = 0; c < GTC; ++c) {
-          const int col = h * GTC + c;
-          if (col < kst) {
-            const float val = __uint_as_float(v[c]) * sc.gt_unscale;
-            dst[col] = first ? val : dst[col] + val;
-          }
-        }
+        for (int c = 0; c < GTC; c += 4)
+          *reinterpret_cast<uint4*>(srow + c) = make_uint4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(1, 32 * C::NEPI);
+      if (leader) {
+        float* dst = p.pright + size_t(u2.gt_slot) * 64 * KP16;
+        if (u2.flags & TCU_FIRST_TOUCH)
+          bulk_store(dst, stg, C::STG_BYTES);
+        else
+          bulk_reduce_add_f32(dst, stg, C::STG_BYTES);
+        bulk_commit();
       }
     };
 
@@ -351,30 +343,22 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
       const int gvb = rrun & 1;
       mbar_wait(&bar->gv_full[gvb], (rrun >> 1) & 1);
       tc_fence_after();
-      uint32_t v[GTC > 16 ? GTC : 16];
+      uint32_t v[GTC >= 16 ? GTC : 16];
 #pragma unroll
-      for (int c0 = 0; c0 < GTC; c0 += 16) {
+      for (int c0 = 0; c0 < (GTC >= 16 ? GTC : 16); c0 += 16) {
         uint32_t r16[16];
         tmem_ld16(tm + lane_addr + C::T_GV + gvb * KP16 + h * GTC + c0, r16);
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[c0 + i] = r16[i];
       }
-      if (GTC < 16) {
-        uint32_t r16[16];
-        tmem_ld16(tm + lane_addr + C::T_GV + gvb * KP16 + h * GTC, r16);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = r16[i];
-      }
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar->gv_empty[gvb]);
-      float* dst = p.pleft + (size_t(slot) * 128 + row) * kst;
+      float* dst = p.pleft + (size_t(slot) * 128 + row) * KP16 + h * GTC;
 #pragma unroll
-      for (int c = 0; c < GTC; ++c) {
-        const int col = h * GTC + c;
-        if (col < kst) dst[col] = __uint_as_float(v[c]) * sc.gv_unscale;
-      }
+      for (int c = 0; c < GTC; c += 4)
+        *reinterpret_cast<uint4*>(dst + c) = make_uint4(v[c], v[c + 1], v[c + 2], v[c + 3]);
     };
 
     TcUnit prev_unit{};
@@ -467,6 +451,7 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
       drain_gt(T - 1, prev_unit);
       drain_gv(run, prev_gv_slot);
     }
+    if (leader) bulk_wait_all();
     // phi: per-thread fp64, fold over the epilogue warps in a fixed order
     double w = warp_sum(phi_acc);
     if (lane == 0) bar->phi[warp - 2] = w;
