@@ -439,10 +439,33 @@ static int tc_launch(spcp_problem* p, int64_t k) {
   tp.pright = p->pright.as<float>();
   tp.pphi = p->pphi.as<double>();
   tp.kstore = int(k);
+  {
+    const char* e = getenv("SPCP_TC_DEBUG");
+    tp.debug = e ? atoi(e) : 0;
+  }
+  static long long* dbg = nullptr;
+  if (tp.debug & 4) {
+    if (!dbg) SPCP_CUDA(cudaMalloc(&dbg, 64 * 16 * sizeof(long long)));
+    SPCP_CUDA(cudaMemsetAsync(dbg, 0, 64 * 16 * sizeof(long long), p->stream));
+    tp.dbg_ts = dbg;
+  }
   if (p->prof) SPCP_CUDA(cudaEventRecord(p->ev0, p->stream));
   kern<<<p->tc_grid, C::NTHREADS, C::SMEM, p->stream>>>(p->tc_xmap, p->tc_mmap, tp);
   SPCP_CHECK_LAUNCH("tc_eval_kernel");
   if (p->prof) SPCP_CUDA(cudaEventRecord(p->ev1, p->stream));
+  if (tp.debug & 4) {
+    long long h[64 * 16];
+    SPCP_CUDA(cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, p->stream));
+    SPCP_CUDA(cudaStreamSynchronize(p->stream));
+    FILE* f = fopen("gpurun_out/tc_ts.txt", "w");
+    if (f) {
+      for (int t = 0; t < 64; ++t) {
+        for (int c = 0; c < 11; ++c) fprintf(f, "%lld ", h[t * 16 + c] ? h[t * 16 + c] - h[0] : -1);
+        fprintf(f, "\n");
+      }
+      fclose(f);
+    }
+  }
   p->launches++;
   return SPCP_OK;
 }

@@ -14,7 +14,8 @@
 // use gh.vh + gh.vm + gl.vh (~2^-22).  Each product is exact in the fp32
 // accumulator; scales are exact powers of two and are undone at the drain.
 //
-// Roles: warp 0 = TMA/bulk producer, warp 1 = MMA issuer (+TMEM owner),
+// Roles: warp 0 = X/mask TMA producer, warp 1 = MMA issuer (+TMEM owner),
+// warp 2 = U/V operand-image bulk producer,
 // warps 2..9 = epilogue (warp w owns TMEM lane quarter w % 4 and column half
 // (w - 2) / 4 of each tile).  Work: a static, exactly balanced range of tiles
 // per CTA (one CTA per SM) in 2-D super-block order; GV accumulates in TMEM
@@ -26,6 +27,10 @@
 
 #include "common.cuh"
 #include "tc_common.cuh"
+
+#ifndef SPCP_TC_NRES
+#define SPCP_TC_NRES 6
+#endif
 
 namespace spcp {
 
@@ -59,13 +64,19 @@ struct TcParams {
   float* pright;  // [gt_slots][64][kstore]
   double* pphi;   // [grid]
   int kstore;
+  int debug;  // bisection switches (SPCP_TC_DEBUG): 1 skip GT stores, 2 skip GV stores,
+              // 4 record per-tile timestamps of CTA 0 into dbg_ts
+  long long* dbg_ts;  // [64][16]
 };
 
 template <int KP16, bool MASK>
 struct TcCfg {
   static constexpr int RB = KP16 * 2;           // operand image row bytes (32/64/128)
   static constexpr uint32_t SWK = RB == 128 ? tc::SW_128 : (RB == 64 ? tc::SW_64 : tc::SW_32);
-  static constexpr int NST = KP16 == 64 ? 2 : (KP16 == 32 ? 3 : 4);
+  // X ring (released by the epilogue as soon as it has read the tile) and a
+  // separate V-image ring (released when the tile's G.V MMA has finished)
+  static constexpr int NST = KP16 == 16 ? 4 : ((KP16 == 64 && MASK) ? 2 : 3);
+  static constexpr int NSV = KP16 == 64 ? 2 : 3;
   static constexpr int UB = KP16 == 64 ? 1 : 2;  // U image buffers
   static constexpr int X_BYTES = 128 * 64 * 4;
   static constexpr int V_SPLIT = 64 * RB;
@@ -77,23 +88,27 @@ struct TcCfg {
   // smem carve (all offsets multiples of 1 KB)
   static constexpr int OFF_X = 0;
   static constexpr int OFF_V = OFF_X + NST * X_BYTES;
-  static constexpr int OFF_U = OFF_V + NST * V_BYTES;
+  static constexpr int OFF_U = OFF_V + NSV * V_BYTES;
   static constexpr int OFF_GH = OFF_U + UB * U_BYTES;
   static constexpr int OFF_GL = OFF_GH + G_BYTES;
   static constexpr int OFF_M = OFF_GL + G_BYTES;
-  static constexpr int OFF_STG = OFF_M + (MASK ? NST * 2048 : 0);
-  static constexpr int STG_BYTES = 64 * KP16 * 4;  // G^T U tile staged for the bulk reduce
-  static constexpr int OFF_BAR = OFF_STG + STG_BYTES;
+  static constexpr int OFF_BAR = OFF_M + (MASK ? NST * 2048 : 0);
   static constexpr int SMEM = OFF_BAR + 512;  // dynamic smem base is 1 KB aligned
   // TMEM columns
+  // GT holds [G^T uh | G^T um] (N = GCAT * KP16, halves summed at the drain)
+  // when TMEM allows; KP16 = 64 keeps the three-product form
+  static constexpr int GCAT = KP16 <= 32 ? 2 : 1;
+  static constexpr int NRES = SPCP_TC_NRES;  // residual split products (6: order <= 2, 3: order <= 1)
   static constexpr uint32_t T_S = 0, T_GA = 128, T_GV = 256, T_GT = 256 + 2 * KP16;
+  static_assert(T_GT + 2 * GCAT * KP16 <= 512, "TMEM budget");
   static constexpr uint32_t TMEM_COLS = 512;
-  static constexpr int NEPI = 8;  // epilogue warps
-  static constexpr int NTHREADS = 32 * (2 + NEPI);
+  static constexpr int NEPI = 16;  // epilogue warps (4 per SM sub-partition)
+  static constexpr int NTHREADS = 32 * (3 + NEPI);  // X producer, MMA, U/V producer, epilogue
 };
 
 struct TcBarriers {
   uint64_t stage_full[4], stage_empty[4];
+  uint64_t v_full[3], v_empty[3];
   uint64_t u_full[2], u_empty[2];
   uint64_t s_full[2], s_empty[2];
   uint64_t ga_full[2], ga_empty[2];
@@ -101,13 +116,18 @@ struct TcBarriers {
   uint64_t gt_full[2], gt_empty[2];
   uint64_t gv_full[2], gv_empty[2];
   uint32_t tmem_base;
-  double phi[8];
+  double phi[16];
 };
 
 __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
   __half2 h = __floats2half2_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&h);
 }
+
+#define TC_TS(t, slot)                                                              \
+  do {                                                                             \
+    if ((p.debug & 4) && blockIdx.x == 0 && (t) < 64) p.dbg_ts[(t) * 16 + (slot)] = clock64(); \
+  } while (0)
 
 template <int KP16, bool MASK>
 __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
@@ -127,7 +147,11 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::NST; ++i) {
       mbar_init(&bar->stage_full[i], 1);
-      mbar_init(&bar->stage_empty[i], C::NEPI + 1);
+      mbar_init(&bar->stage_empty[i], C::NEPI);
+    }
+    for (int i = 0; i < C::NSV; ++i) {
+      mbar_init(&bar->v_full[i], 1);
+      mbar_init(&bar->v_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bar->u_full[i], 1);
@@ -155,7 +179,27 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
   const uint32_t tm = bar->tmem_base;
 
   if (warp == 0) {
-    // ======================= producer ===================================
+    // ======================= X / mask producer (TMA) ====================
+    if (lane == 0) {
+      const uint64_t pol_x = policy_evict_first();
+      for (int t = 0; t < T; ++t) {
+        const TcUnit un = units[t];
+        const int st = t % C::NST;
+        mbar_wait(&bar->stage_empty[st], ((t / C::NST) & 1) ^ 1);
+        TC_TS(t, 0);
+        mbar_arrive_expect_tx(&bar->stage_full[st], C::X_BYTES + C::M_BYTES);
+        unsigned char* xs = sm + C::OFF_X + st * C::X_BYTES;
+        tma_load_2d_hint(xs, &xmap, int(un.tc) * 64, int(un.sb) * 128, &bar->stage_full[st],
+                         pol_x);
+        tma_load_2d_hint(xs + 16384, &xmap, int(un.tc) * 64 + 32, int(un.sb) * 128,
+                         &bar->stage_full[st], pol_x);
+        if (MASK)
+          tma_load_2d_hint(sm + C::OFF_M + st * 2048, &mmap, (int(un.tc) * 2) & ~3,
+                           int(un.sb) * 128, &bar->stage_full[st], pol_x);
+      }
+    }
+  } else if (warp == 2) {
+    // ======================= U / V operand-image producer (bulk) ========
     if (lane == 0) {
       int prev_sb = -1, fills = 0;
       for (int t = 0; t < T; ++t) {
@@ -169,25 +213,18 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
           ++fills;
           prev_sb = un.sb;
         }
-        const int st = t % C::NST;
-        mbar_wait(&bar->stage_empty[st], ((t / C::NST) & 1) ^ 1);
-        mbar_arrive_expect_tx(&bar->stage_full[st], C::X_BYTES + C::V_BYTES + C::M_BYTES);
-        unsigned char* xs = sm + C::OFF_X + st * C::X_BYTES;
-        tma_load_2d(xs, &xmap, int(un.tc) * 64, int(un.sb) * 128, &bar->stage_full[st]);
-        tma_load_2d(xs + 16384, &xmap, int(un.tc) * 64 + 32, int(un.sb) * 128,
-                    &bar->stage_full[st]);
-        bulk_load(sm + C::OFF_V + st * C::V_BYTES, p.v_img + size_t(un.tc) * C::V_BYTES,
-                  C::V_BYTES, &bar->stage_full[st]);
-        if (MASK)
-          tma_load_2d(sm + C::OFF_M + st * 2048, &mmap, (int(un.tc) * 2) & ~3, int(un.sb) * 128,
-                      &bar->stage_full[st]);
+        const int sv = t % C::NSV;
+        mbar_wait(&bar->v_empty[sv], ((t / C::NSV) & 1) ^ 1);
+        mbar_arrive_expect_tx(&bar->v_full[sv], C::V_BYTES);
+        bulk_load(sm + C::OFF_V + sv * C::V_BYTES, p.v_img + size_t(un.tc) * C::V_BYTES,
+                  C::V_BYTES, &bar->v_full[sv]);
       }
     }
   } else if (warp == 1) {
     // ======================= MMA issuer =================================
     constexpr uint32_t ID_RES = idesc_f16(128, 64, false, false);
     constexpr uint32_t ID_GV = idesc_f16(128, KP16, false, true);
-    constexpr uint32_t ID_GT = idesc_f16(64, KP16, true, true);
+    constexpr uint32_t ID_GT = idesc_f16(64, C::GCAT * KP16, true, true);
     constexpr int KS = KP16 / 16;
     const uint32_t u0 = smem_u32(sm + C::OFF_U), v0 = smem_u32(sm + C::OFF_V);
     const uint32_t gh0 = smem_u32(sm + C::OFF_GH), gl0 = smem_u32(sm + C::OFF_GL);
@@ -195,72 +232,82 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
     int prev_sb = -1;
 
     auto residual = [&](int t, int ubuf) {
-      const int st = t % C::NST, b = t & 1;
-      mbar_wait(&bar->stage_full[st], (t / C::NST) & 1);
+      const int st = t % C::NSV, b = t & 1;
+      mbar_wait(&bar->v_full[st], (t / C::NSV) & 1);
+      if (lane == 0) TC_TS(t, 1);
       mbar_wait(&bar->s_empty[b], ((t >> 1) & 1) ^ 1);
+      if (lane == 0) TC_TS(t, 2);
       tc_fence_after();
-      if (elect_one()) {
+      {
         const uint32_t ua = u0 + ubuf * C::U_BYTES;
         const uint32_t vb = v0 + st * C::V_BYTES;
         // products of total split order <= 2: (h,h) (h,m) (m,h) (h,l) (m,m) (l,h)
         const int pa[6] = {0, 0, 1, 0, 1, 2};
         const int pb[6] = {0, 1, 0, 2, 1, 0};
 #pragma unroll
-        for (int q = 0; q < 6; ++q)
+        for (int q = 0; q < C::NRES; ++q)
 #pragma unroll
           for (int ks = 0; ks < KS; ++ks)
-            mma_ss(tm + C::T_S + b * 64,
+            mma_ss_w(tm + C::T_S + b * 64,
                    umma_desc(ua + pa[q] * C::U_SPLIT + ks * 32, 16, 8 * C::RB, C::SWK),
                    umma_desc(vb + pb[q] * C::V_SPLIT + ks * 32, 16, 8 * C::RB, C::SWK), ID_RES,
                    (q | ks) != 0);
-        mma_commit(&bar->s_full[b]);
+        mma_commit_w(&bar->s_full[b]);
       }
-      __syncwarp();
     };
 
     auto reductions = [&](int t, int ubuf, int rrun, uint32_t flags) {
-      const int st = t % C::NST, b = t & 1, gvb = rrun & 1;
+      const int st = t % C::NSV, b = t & 1, gvb = rrun & 1;
       mbar_wait(&bar->ga_full[b], (t >> 1) & 1);
+      if (lane == 0) TC_TS(t, 3);
       mbar_wait(&bar->gt_empty[b], ((t >> 1) & 1) ^ 1);
       if (flags & TCU_FIRST_OF_RUN) mbar_wait(&bar->gv_empty[gvb], ((rrun >> 1) & 1) ^ 1);
       tc_fence_after();
-      if (elect_one()) {
+      {
         // G^T U first: it releases the single G staging image the epilogue
         // needs for the next tile
         const uint32_t ua = u0 + ubuf * C::U_BYTES;
-        const uint32_t gt = tm + C::T_GT + b * KP16;
+        const uint32_t gt = tm + C::T_GT + b * C::GCAT * KP16;
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
           const uint32_t uo = ks * 16 * C::RB;
-          mma_ss(gt, umma_desc(gh0 + 2048 * ks, 16384, 1024, SW_128),
-                 umma_desc(ua + uo, 8192, 8 * C::RB, C::SWK), ID_GT, ks > 0);
-          mma_ss(gt, umma_desc(gh0 + 2048 * ks, 16384, 1024, SW_128),
-                 umma_desc(ua + C::U_SPLIT + uo, 8192, 8 * C::RB, C::SWK), ID_GT, 1);
-          mma_ss(gt, umma_desc(gl0 + 2048 * ks, 16384, 1024, SW_128),
-                 umma_desc(ua + uo, 8192, 8 * C::RB, C::SWK), ID_GT, 1);
+          if constexpr (C::GCAT == 2) {
+            // B = [uh | um]: two N-atoms of the U image (LBO = split stride);
+            // every G byte is read once
+            mma_ss_w(gt, umma_desc(gh0 + 2048 * ks, 16384, 1024, SW_128),
+                     umma_desc(ua + uo, C::U_SPLIT, 8 * C::RB, C::SWK), ID_GT, ks > 0);
+            mma_ss_w(gt, umma_desc(gl0 + 2048 * ks, 16384, 1024, SW_128),
+                     umma_desc(ua + uo, C::U_SPLIT, 8 * C::RB, C::SWK), ID_GT, 1);
+          } else {
+            mma_ss_w(gt, umma_desc(gh0 + 2048 * ks, 16384, 1024, SW_128),
+                     umma_desc(ua + uo, 8192, 8 * C::RB, C::SWK), ID_GT, ks > 0);
+            mma_ss_w(gt, umma_desc(gh0 + 2048 * ks, 16384, 1024, SW_128),
+                     umma_desc(ua + C::U_SPLIT + uo, 8192, 8 * C::RB, C::SWK), ID_GT, 1);
+            mma_ss_w(gt, umma_desc(gl0 + 2048 * ks, 16384, 1024, SW_128),
+                     umma_desc(ua + uo, 8192, 8 * C::RB, C::SWK), ID_GT, 1);
+          }
         }
-        mma_commit(&bar->gt_full[b]);
-        mma_commit(&bar->gs_empty);
+        mma_commit_w(&bar->gt_full[b]);
+        mma_commit_w(&bar->gs_empty);
         const uint32_t vb = v0 + st * C::V_BYTES;
         const uint32_t gv = tm + C::T_GV + gvb * KP16;
         const uint32_t ga = tm + C::T_GA + b * 64;
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
           const uint32_t vo = ks * 16 * C::RB;
-          mma_ts(gv, ga + 8 * ks, umma_desc(vb + vo, 8192, 8 * C::RB, C::SWK), ID_GV,
+          mma_ts_w(gv, ga + 8 * ks, umma_desc(vb + vo, 8192, 8 * C::RB, C::SWK), ID_GV,
                  !((flags & TCU_FIRST_OF_RUN) && ks == 0));
-          mma_ts(gv, ga + 8 * ks, umma_desc(vb + C::V_SPLIT + vo, 8192, 8 * C::RB, C::SWK),
+          mma_ts_w(gv, ga + 8 * ks, umma_desc(vb + C::V_SPLIT + vo, 8192, 8 * C::RB, C::SWK),
                  ID_GV, 1);
-          mma_ts(gv, ga + 32 + 8 * ks, umma_desc(vb + vo, 8192, 8 * C::RB, C::SWK), ID_GV, 1);
+          mma_ts_w(gv, ga + 32 + 8 * ks, umma_desc(vb + vo, 8192, 8 * C::RB, C::SWK), ID_GV, 1);
         }
-        mma_commit(&bar->ga_empty[b]);
-        mma_commit(&bar->stage_empty[st]);
+        mma_commit_w(&bar->ga_empty[b]);
+        mma_commit_w(&bar->v_empty[st]);
         if (flags & TCU_LAST_OF_RUN) {
-          mma_commit(&bar->gv_full[gvb]);
-          mma_commit(&bar->u_empty[ubuf]);
+          mma_commit_w(&bar->gv_full[gvb]);
+          mma_commit_w(&bar->u_empty[ubuf]);
         }
       }
-      __syncwarp();
     };
 
     // bookkeeping of the previous tile (its reductions trail its residual)
@@ -286,8 +333,12 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
     if (T >= 1) reductions(T - 1, p_ubuf, p_run, p_flags);
   } else {
     // ======================= epilogue warps =============================
+    // warp e = warp - 3 owns TMEM lane quarter q = warp % 4 (rows 32q..32q+31)
+    // and columns [part * CPW, part * CPW + CPW) of every 64-column tile.
+    constexpr int CPW = 256 / C::NEPI;      // columns per epilogue warp (16 or 32)
+    constexpr int NPAIR = CPW / 2;          // packed half2 registers per split
     const int q = warp & 3;
-    const int h = (warp - 2) >> 2;
+    const int part = (warp - 3) >> 2;
     const int row = 32 * q + lane;
     const uint32_t lane_addr = uint32_t(32 * q) << 16;
     const TcScales sc = *p.scales;
@@ -295,75 +346,85 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
     double phi_acc = 0.0;
     int run = -1, prev_sb = -1;
     int prev_gv_slot = -1;
-    constexpr int GTC = KP16 / 2;  // GT columns drained per warp half
+    constexpr int GTC = KP16 / 2;  // accumulator columns drained per draining warp
+    const bool drainer = part < 2;  // two warps per lane quarter drain G.V / G^T.U
+    const int dpart = part & 1;
+    // swizzled byte offsets of this thread's X row chunks (box = 32 columns)
+    const int xbox = (part * CPW) >> 5;
+    const int xc0 = ((part * CPW) & 31) >> 2;  // first 16 B chunk within the box row
 
-    // G^T U of tile t2 -> staging tile -> one TMA bulk store (first touch of
-    // the slot) or fp32 bulk reduce-add into this CTA's private slot.  The
-    // leader waits for all earlier bulk ops first: the staging tile is free
-    // and adds into one slot land in program order (deterministic).
-    float* stg = reinterpret_cast<float*>(sm + C::OFF_STG);
-    const bool leader = threadIdx.x == 64;
+    // G^T U of tile t2 -> this CTA's private slot for the column tile: plain
+    // stores on first touch, then fp32x4 reductions in L2.  Each (row, col)
+    // of a slot is owned by one thread, whose same-address operations apply
+    // in program order: deterministic without staging or fences.
     auto drain_gt = [&](int t2, const TcUnit& u2) {
       const int b = t2 & 1;
       mbar_wait(&bar->gt_full[b], (t2 >> 1) & 1);
       tc_fence_after();
-      uint32_t v[GTC >= 16 ? GTC : 16];
+      if (drainer && !(p.debug & 1)) {
+        float* dst =
+            p.pright + (size_t(u2.gt_slot) * 64 + 16 * q + lane) * KP16 + dpart * GTC;
+        const bool first = (u2.flags & TCU_FIRST_TOUCH) != 0;
+        constexpr int CH = GTC < 16 ? GTC : 16;
 #pragma unroll
-      for (int c0 = 0; c0 < (GTC >= 16 ? GTC : 16); c0 += 16) {
-        uint32_t r16[16];
-        tmem_ld16(tm + lane_addr + C::T_GT + b * KP16 + h * GTC + c0, r16);
+        for (int c0 = 0; c0 < GTC; c0 += CH) {
+          uint32_t v[CH], w[CH];
+          const uint32_t col =
+              tm + lane_addr + C::T_GT + b * C::GCAT * KP16 + dpart * GTC + c0;
+          tmem_ldn<CH>(col, v);
+          if constexpr (C::GCAT == 2) {
+            tmem_ldn<CH>(col + KP16, w);
+            tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[c0 + i] = r16[i];
+            for (int c = 0; c < CH; ++c)
+              v[c] = __float_as_uint(__uint_as_float(v[c]) + __uint_as_float(w[c]));
+          } else {
+            tmem_wait_ld();
+          }
+          if (lane < 16) {  // M = 64 accumulator: row j = 16 q + lane in lanes 0..15
+#pragma unroll
+            for (int c = 0; c < CH; c += 4) {
+              if (first)
+                *reinterpret_cast<uint4*>(dst + c0 + c) =
+                    make_uint4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+              else
+                red_add_v4(dst + c0 + c, v[c], v[c + 1], v[c + 2], v[c + 3]);
+            }
+          }
+        }
       }
-      tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar->gt_empty[b]);
-      if (leader) bulk_wait_all();
-      named_bar_sync(1, 32 * C::NEPI);
-      if (lane < 16) {  // M = 64 accumulator: row j = 16 q + lane lives in lanes 0..15
-        float* srow = stg + (16 * q + lane) * KP16 + h * GTC;
-#pragma unroll
-        for (int c = 0; c < GTC; c += 4)
-          *reinterpret_cast<uint4*>(srow + c) = make_uint4(v[c], v[c + 1], v[c + 2], v[c + 3]);
-      }
-      fence_proxy_async_smem();
-      named_bar_sync(1, 32 * C::NEPI);
-      if (leader) {
-        float* dst = p.pright + size_t(u2.gt_slot) * 64 * KP16;
-        if (u2.flags & TCU_FIRST_TOUCH)
-          bulk_store(dst, stg, C::STG_BYTES);
-        else
-          bulk_reduce_add_f32(dst, stg, C::STG_BYTES);
-        bulk_commit();
-      }
     };
 
     auto drain_gv = [&](int rrun, int slot) {
       const int gvb = rrun & 1;
       mbar_wait(&bar->gv_full[gvb], (rrun >> 1) & 1);
       tc_fence_after();
-      uint32_t v[GTC >= 16 ? GTC : 16];
+      if (drainer && !(p.debug & 2)) {
+        float* dst = p.pleft + (size_t(slot) * 128 + row) * KP16 + dpart * GTC;
+        constexpr int CH = GTC < 16 ? GTC : 16;
 #pragma unroll
-      for (int c0 = 0; c0 < (GTC >= 16 ? GTC : 16); c0 += 16) {
-        uint32_t r16[16];
-        tmem_ld16(tm + lane_addr + C::T_GV + gvb * KP16 + h * GTC + c0, r16);
+        for (int c0 = 0; c0 < GTC; c0 += CH) {
+          uint32_t v[CH];
+          tmem_ldn<CH>(tm + lane_addr + C::T_GV + gvb * KP16 + dpart * GTC + c0, v);
+          tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[c0 + i] = r16[i];
+          for (int c = 0; c < CH; c += 4)
+            *reinterpret_cast<uint4*>(dst + c0 + c) = make_uint4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+        }
       }
-      tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar->gv_empty[gvb]);
-      float* dst = p.pleft + (size_t(slot) * 128 + row) * KP16 + h * GTC;
-#pragma unroll
-      for (int c = 0; c < GTC; c += 4)
-        *reinterpret_cast<uint4*>(dst + c) = make_uint4(v[c], v[c + 1], v[c + 2], v[c + 3]);
     };
 
     TcUnit prev_unit{};
+    TcUnit un_next = T > 0 ? units[0] : TcUnit{};
     for (int t = 0; t < T; ++t) {
-      const TcUnit un = units[t];
+      const TcUnit un = un_next;
+      if (t + 1 < T) un_next = units[t + 1];  // consumed next iteration: latency hidden
       const bool new_run = (un.flags & TCU_FIRST_OF_RUN) || un.sb != prev_sb;
       if (new_run) {
         ++run;
@@ -371,26 +432,33 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
       }
       const int st = t % C::NST, b = t & 1;
       // ---- S tile and X tile
+      const bool ts_w = (warp == 3 && lane == 0);
+      if (ts_w) TC_TS(t, 4);
       mbar_wait(&bar->s_full[b], (t >> 1) & 1);
+      if (ts_w) TC_TS(t, 5);
       tc_fence_after();
-      uint32_t s0[16], s1[16];
-      tmem_ld16(tm + lane_addr + C::T_S + b * 64 + 32 * h, s0);
-      tmem_ld16(tm + lane_addr + C::T_S + b * 64 + 32 * h + 16, s1);
+      uint32_t sv[CPW];
+      tmem_ldn<CPW>(tm + lane_addr + C::T_S + b * 64 + part * CPW, sv);
       mbar_wait(&bar->stage_full[st], (t / C::NST) & 1);
-      const unsigned char* xs = sm + C::OFF_X + st * C::X_BYTES + h * 16384;
-      float xv[32];
+      if (ts_w) TC_TS(t, 6);
+      const unsigned char* xs = sm + C::OFF_X + st * C::X_BYTES + xbox * 16384;
+      float xv[CPW];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const float4 f = *reinterpret_cast<const float4*>(xs + Swz<128>::offset(row, c * 16));
+      for (int c = 0; c < CPW / 4; ++c) {
+        const float4 f =
+            *reinterpret_cast<const float4*>(xs + Swz<128>::offset(row, (xc0 + c) * 16));
         xv[4 * c] = f.x;
         xv[4 * c + 1] = f.y;
         xv[4 * c + 2] = f.z;
         xv[4 * c + 3] = f.w;
       }
       uint32_t mw = 0xffffffffu;
-      if (MASK)
+      if (MASK) {
         mw = reinterpret_cast<const uint32_t*>(sm + C::OFF_M + st * 2048)[row * 4 +
-                                                                          (un.tc & 1) * 2 + h];
+                                                                          (un.tc & 1) * 2 +
+                                                                          ((part * CPW) >> 5)];
+        mw >>= (part * CPW) & 31;
+      }
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
@@ -399,20 +467,19 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
         mbar_arrive(&bar->stage_empty[st]);
       }
       // ---- epilogue math: r = x - L (scaled), clip, huber, split
-      uint32_t hi[16], lo[16];
-      float hsum = 0.f;
+      uint32_t hi[NPAIR], lo[NPAIR];
+      float hs[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int e = 0; e < 32; e += 2) {
+      for (int e = 0; e < CPW; e += 2) {
         float g2[2];
 #pragma unroll
         for (int f = 0; f < 2; ++f) {
           const int c = e + f;
-          const float sv = __uint_as_float(c < 16 ? s0[c] : s1[c - 16]);
-          float r = fmaf(xv[c], sigma, -sv);
+          float r = fmaf(xv[c], sigma, -__uint_as_float(sv[c]));
           if (MASK) r = ((mw >> c) & 1u) ? r : 0.f;
           const float a = fabsf(r);
           const float cl = fminf(a, tau_s);
-          hsum = fmaf(cl, fmaf(-0.5f, cl, a), hsum);
+          hs[c & 3] = fmaf(cl, fmaf(-0.5f, cl, a), hs[c & 3]);
           g2[f] = -copysignf(cl, r) * kappa;
         }
         const __half2 hh = __floats2half2_rn(g2[0], g2[1]);
@@ -420,17 +487,24 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
         hi[e >> 1] = *reinterpret_cast<const uint32_t*>(&hh);
         lo[e >> 1] = pack_half2(g2[0] - hf.x, g2[1] - hf.y);
       }
-      phi_acc += double(hsum);
+      phi_acc += double((hs[0] + hs[1]) + (hs[2] + hs[3]));
       // ---- G to TMEM (A of G.V) and to smem (A of G^T.U)
       mbar_wait(&bar->ga_empty[b], ((t >> 1) & 1) ^ 1);
-      tmem_st16(tm + lane_addr + C::T_GA + b * 64 + 16 * h, hi);
-      tmem_st16(tm + lane_addr + C::T_GA + b * 64 + 32 + 16 * h, lo);
+      if constexpr (NPAIR == 16) {
+        tmem_st16(tm + lane_addr + C::T_GA + b * 64 + part * NPAIR, hi);
+        tmem_st16(tm + lane_addr + C::T_GA + b * 64 + 32 + part * NPAIR, lo);
+      } else {
+        tmem_st8(tm + lane_addr + C::T_GA + b * 64 + part * NPAIR, hi);
+        tmem_st8(tm + lane_addr + C::T_GA + b * 64 + 32 + part * NPAIR, lo);
+      }
+      if (ts_w) TC_TS(t, 7);
       mbar_wait(&bar->gs_empty, (t & 1) ^ 1);
+      if (ts_w) TC_TS(t, 8);
       unsigned char* gh = sm + C::OFF_GH;
       unsigned char* gl = sm + C::OFF_GL;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const uint32_t o = Swz<128>::offset(row, 64 * h + 16 * c);
+      for (int c = 0; c < NPAIR / 4; ++c) {
+        const uint32_t o = Swz<128>::offset(row, part * CPW * 2 + 16 * c);
         *reinterpret_cast<uint4*>(gh + o) = make_uint4(hi[4 * c], hi[4 * c + 1], hi[4 * c + 2],
                                                        hi[4 * c + 3]);
         *reinterpret_cast<uint4*>(gl + o) = make_uint4(lo[4 * c], lo[4 * c + 1], lo[4 * c + 2],
@@ -441,9 +515,11 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar->ga_full[b]);
+      if (ts_w) TC_TS(t, 9);
       // ---- deferred drains
       if (t >= 1) drain_gt(t - 1, prev_unit);
       if (new_run && t >= 1) drain_gv(run - 1, prev_gv_slot);
+      if (ts_w) TC_TS(t, 10);
       prev_unit = un;
       prev_gv_slot = un.gv_slot;
     }
@@ -451,10 +527,9 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
       drain_gt(T - 1, prev_unit);
       drain_gv(run, prev_gv_slot);
     }
-    if (leader) bulk_wait_all();
     // phi: per-thread fp64, fold over the epilogue warps in a fixed order
     double w = warp_sum(phi_acc);
-    if (lane == 0) bar->phi[warp - 2] = w;
+    if (lane == 0) bar->phi[warp - 3] = w;
   }
   tc_fence_before();
   __syncthreads();
