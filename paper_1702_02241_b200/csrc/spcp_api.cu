@@ -445,8 +445,8 @@ static int tc_launch(spcp_problem* p, int64_t k) {
   }
   static long long* dbg = nullptr;
   if (tp.debug & 4) {
-    if (!dbg) SPCP_CUDA(cudaMalloc(&dbg, 64 * 16 * sizeof(long long)));
-    SPCP_CUDA(cudaMemsetAsync(dbg, 0, 64 * 16 * sizeof(long long), p->stream));
+    if (!dbg) SPCP_CUDA(cudaMalloc(&dbg, 64 * 32 * sizeof(long long)));
+    SPCP_CUDA(cudaMemsetAsync(dbg, 0, 64 * 32 * sizeof(long long), p->stream));
     tp.dbg_ts = dbg;
   }
   if (p->prof) SPCP_CUDA(cudaEventRecord(p->ev0, p->stream));
@@ -454,13 +454,13 @@ static int tc_launch(spcp_problem* p, int64_t k) {
   SPCP_CHECK_LAUNCH("tc_eval_kernel");
   if (p->prof) SPCP_CUDA(cudaEventRecord(p->ev1, p->stream));
   if (tp.debug & 4) {
-    long long h[64 * 16];
+    long long h[64 * 32];
     SPCP_CUDA(cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, p->stream));
     SPCP_CUDA(cudaStreamSynchronize(p->stream));
     FILE* f = fopen("gpurun_out/tc_ts.txt", "w");
     if (f) {
       for (int t = 0; t < 64; ++t) {
-        for (int c = 0; c < 11; ++c) fprintf(f, "%lld ", h[t * 16 + c] ? h[t * 16 + c] - h[0] : -1);
+        for (int c = 0; c < 26; ++c) fprintf(f, "%lld ", h[t * 32 + c] ? h[t * 32 + c] - h[0] : -1);
         fprintf(f, "\n");
       }
       fclose(f);
@@ -475,8 +475,8 @@ static int tc_images(spcp_problem* p, int64_t k, const double* z, const double* 
                      double alpha) {
   constexpr int RB = KP16 * 2;
   int rc;
-  if ((rc = p->tc_uimg.ensure(size_t(p->tc_nsb) * 3 * 128 * RB))) return rc;
-  if ((rc = p->tc_vimg.ensure(size_t(p->tc_ntc) * 3 * 64 * RB))) return rc;
+  if ((rc = p->tc_uimg.ensure(size_t(p->tc_nsb) * 2 * 128 * RB))) return rc;
+  if ((rc = p->tc_vimg.ensure(size_t(p->tc_ntc) * 2 * 64 * RB))) return rc;
   const int64_t total = (p->m_pad + p->n_pad) * KP16;
   tc_images_kernel<KP16><<<grid_for(total), 256, 0, p->stream>>>(
       z, dz, alpha, p->m, p->n, k, p->m_pad, p->n_pad, p->tc_scales.as<TcScales>(),

@@ -8,36 +8,45 @@
 //   GT  = G^T U_sb    (A = G image in smem MN-major, M = 64)    -> grad_V block
 //
 // Precision: operands are power-of-two scaled and split into
-// fp16 pieces computed in fp64 on the device: U'' = uh + um + ul, V'' = vh +
-// vm + vl, so the residual uses the 6 products of total order <= 2 (relative
-// error ~2^-33 before fp32 accumulation); G'' = gh + gl and the reductions
-// use gh.vh + gh.vm + gl.vh (~2^-22).  Each product is exact in the fp32
-// accumulator; scales are exact powers of two and are undone at the drain.
+// two fp16 pieces computed in fp64 on the device, U'' = uh + um, V'' = vh +
+// vm (relative representation error ~2^-22); the residual uses the three
+// products uh.vh + uh.vm + um.vh, G'' = gh + gl, and the reductions use
+// [gh|gl] x [vh|vm] (all four products where the N-concatenated form makes
+// the fourth free).  Every product is exact in the fp32 accumulator; scales
+// are exact powers of two, undone in the reduce kernel.
 //
-// Roles: warp 0 = X/mask TMA producer, warp 1 = MMA issuer (+TMEM owner),
-// warp 2 = U/V operand-image bulk producer,
-// warps 2..9 = epilogue (warp w owns TMEM lane quarter w % 4 and column half
-// (w - 2) / 4 of each tile).  Work: a static, exactly balanced range of tiles
-// per CTA (one CTA per SM) in 2-D super-block order; GV accumulates in TMEM
-// over a run of tiles with the same sub-band and is drained once per run,
-// GT is drained per tile and summed into a CTA-private slot per column tile
-// (read-modify-write in L2).  Partials are reduced in a fixed order later:
-// deterministic, no float atomics.
+// Roles (640 threads = 20 warps, 5 per SM sub-partition, one CTA per SM):
+//   warp 0      X / mask TMA producer (L2 evict-first),
+//   warp 1      residual MMA issuer (+ TMEM owner): runs ahead of the
+//               epilogue, bounded only by the S / V / U buffers,
+//   warp 2      U / V operand-image producer (L2-resident images, LSU copies),
+//   warp 3      reduction MMA issuer: G^T U then G.V of each tile once its G
+//               is staged (two issuers keep the tensor pipe fed),
+//   warps 4-19  epilogue, two groups of 8 warps that take alternate tiles
+//               (group g = tile parity), so one group's math overlaps the
+//               other group's wait on the reduction MMAs.  Group g owns buffer
+//               set g of S, GA (G in TMEM), the G smem image and GT.
+//               Warp (quarter q = warp % 4, half h) handles rows 32q..32q+31
+//               and columns 32h..32h+31 of its group's tiles.
+// Work: a static, exactly balanced range of tiles per CTA in 2-D super-block
+// order; GV accumulates in TMEM over a run of tiles with the same sub-band
+// and is drained once per run, GT is drained per tile into a CTA-private slot
+// per column tile (store on first touch, then fp32x4 reductions in L2 by the
+// thread that owns the address — program order, so deterministic).
+// Partials are folded in a fixed order by the reduce kernel.
 #pragma once
 
 #include "common.cuh"
 #include "tc_common.cuh"
 
-#ifndef SPCP_TC_NRES
-#define SPCP_TC_NRES 6
-#endif
+#include <utility>
 
 namespace spcp {
 
 struct TcUnit {
   uint16_t sb, tc;
   int32_t gt_slot;
-  int32_t gv_slot;
+  int32_t gv_slot;  // global run id (consecutive within a CTA)
   uint32_t flags;
 };
 enum : uint32_t { TCU_FIRST_OF_RUN = 1u, TCU_LAST_OF_RUN = 2u, TCU_FIRST_TOUCH = 4u };
@@ -46,8 +55,8 @@ struct TcScales {
   float sigma;       // s_u * s_v: S'' = sigma * L
   float tau_s;       // sigma * tau
   float kappa;       // G'' = kappa * (sigma g)
-  float gv_unscale;  // 1 / (kappa sigma s_v)
-  float gt_unscale;  // 1 / (kappa sigma s_u)
+  float gv_unscale;  // -1 / (kappa sigma s_v)   (partials are gp.V'', gp = -G'')
+  float gt_unscale;  // 1 / (kappa sigma s_u)    (gp^T (-U'') = G''^T U'')
   float pad0;
   double phi_unscale;  // 1 / sigma^2
   double su, sv;
@@ -65,54 +74,62 @@ struct TcParams {
   double* pphi;   // [grid]
   int kstore;
   int debug;  // bisection switches (SPCP_TC_DEBUG): 1 skip GT stores, 2 skip GV stores,
-              // 4 record per-tile timestamps of CTA 0 into dbg_ts
-  long long* dbg_ts;  // [64][16]
+              // 8 skip all MMAs (pipeline skeleton only), 16 / 32 / 64 skip the
+              // G^T U / G.V / residual MMAs
+  long long* dbg_ts;  // [64][16] per-tile timestamps of CTA 0 (SPCP_TC_TIMESTAMPS builds)
 };
 
 template <int KP16, bool MASK>
 struct TcCfg {
-  static constexpr int RB = KP16 * 2;           // operand image row bytes (32/64/128)
+  static constexpr int RB = KP16 * 2;  // operand image row bytes (32/64/128)
   static constexpr uint32_t SWK = RB == 128 ? tc::SW_128 : (RB == 64 ? tc::SW_64 : tc::SW_32);
-  // X ring (released by the epilogue as soon as it has read the tile) and a
-  // separate V-image ring (released when the tile's G.V MMA has finished)
-  static constexpr int NST = KP16 == 16 ? 4 : ((KP16 == 64 && MASK) ? 2 : 3);
-  static constexpr int NSV = KP16 == 64 ? 2 : 3;
-  static constexpr int UB = KP16 == 64 ? 1 : 2;  // U image buffers
+  static constexpr int NSPLIT = 2;
+  // X ring (released by the epilogue as soon as it has read the tile), V ring
+  // (released when the tile's G.V MMA has finished), U buffers (per run)
+  static constexpr int NST = KP16 == 16 ? (MASK ? 3 : 4) : (KP16 == 32 ? 3 : (MASK ? 2 : 3));
+  static constexpr int NSV = KP16 == 64 ? 2 : (MASK ? 3 : 4);
+  static constexpr int UB = KP16 == 64 ? 1 : 2;
+  static constexpr int LOOKAHEAD = NSV - 1 < 2 ? NSV - 1 : 2;  // residual issue lead (tiles)
   static constexpr int X_BYTES = 128 * 64 * 4;
   static constexpr int V_SPLIT = 64 * RB;
-  static constexpr int V_BYTES = 3 * V_SPLIT;
+  static constexpr int V_BYTES = NSPLIT * V_SPLIT;
   static constexpr int U_SPLIT = 128 * RB;
-  static constexpr int U_BYTES = 3 * U_SPLIT;
+  static constexpr int U_BYTES = NSPLIT * U_SPLIT;
   static constexpr int M_BYTES = MASK ? 128 * 4 * 4 : 0;  // box {4 words, 128 rows}
-  static constexpr int G_BYTES = 128 * 64 * 2;  // one fp16 G image (MN-major SW128)
+  static constexpr int G_SPLIT = 128 * 64 * 2;            // one fp16 G image (MN-major SW128)
+  static constexpr int G_BYTES = 2 * G_SPLIT;             // gh, gl
   // smem carve (all offsets multiples of 1 KB)
   static constexpr int OFF_X = 0;
   static constexpr int OFF_V = OFF_X + NST * X_BYTES;
   static constexpr int OFF_U = OFF_V + NSV * V_BYTES;
-  static constexpr int OFF_GH = OFF_U + UB * U_BYTES;
-  static constexpr int OFF_GL = OFF_GH + G_BYTES;
-  static constexpr int OFF_M = OFF_GL + G_BYTES;
+  static constexpr int OFF_G = OFF_U + UB * U_BYTES;
+  static constexpr int OFF_M = OFF_G + 2 * G_BYTES;
   static constexpr int OFF_BAR = OFF_M + (MASK ? NST * 2048 : 0);
   static constexpr int SMEM = OFF_BAR + 512;  // dynamic smem base is 1 KB aligned
-  // TMEM columns
-  // GT holds [G^T uh | G^T um] (N = GCAT * KP16, halves summed at the drain)
-  // when TMEM allows; KP16 = 64 keeps the three-product form
+  static_assert(SMEM <= 232448, "shared memory budget");
+  // TMEM columns: S [2 x 64] | GA [2 x 64: hi 32 + lo 32 packed fp16] |
+  // GV [2 x GVC*KP16] | GT [2 x GCAT*KP16]; the N-concatenated forms hold the
+  // [vh|vm] (resp. [uh|um]) halves side by side, summed at the drain
   static constexpr int GCAT = KP16 <= 32 ? 2 : 1;
-  static constexpr int NRES = SPCP_TC_NRES;  // residual split products (6: order <= 2, 3: order <= 1)
-  static constexpr uint32_t T_S = 0, T_GA = 128, T_GV = 256, T_GT = 256 + 2 * KP16;
+  static constexpr int GVC = KP16 <= 32 ? 2 : 1;
+  static constexpr uint32_t T_S = 0, T_GA = 128, T_GV = 256;
+  static constexpr uint32_t T_GT = T_GV + 2 * GVC * KP16;
   static_assert(T_GT + 2 * GCAT * KP16 <= 512, "TMEM budget");
   static constexpr uint32_t TMEM_COLS = 512;
-  static constexpr int NEPI = 16;  // epilogue warps (4 per SM sub-partition)
-  static constexpr int NTHREADS = 32 * (3 + NEPI);  // X producer, MMA, U/V producer, epilogue
+  static constexpr int NEPI = 16;  // epilogue warps: 2 groups x 4 quarters x 2 halves
+  static constexpr int NEG = NEPI / 2;
+  static constexpr int FIRST_EPI = 4;  // warps 0-3: X producer, residual MMA issuer,
+                                       // U/V producer, reduction MMA issuer
+  static constexpr int NTHREADS = 32 * (FIRST_EPI + NEPI);
 };
 
 struct TcBarriers {
   uint64_t stage_full[4], stage_empty[4];
-  uint64_t v_full[3], v_empty[3];
+  uint64_t v_full[4], v_empty[4];
   uint64_t u_full[2], u_empty[2];
   uint64_t s_full[2], s_empty[2];
   uint64_t ga_full[2], ga_empty[2];
-  uint64_t gs_empty;
+  uint64_t gs_empty[2];
   uint64_t gt_full[2], gt_empty[2];
   uint64_t gv_full[2], gv_empty[2];
   uint32_t tmem_base;
@@ -124,10 +141,59 @@ __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-#define TC_TS(t, slot)                                                              \
-  do {                                                                             \
-    if ((p.debug & 4) && blockIdx.x == 0 && (t) < 64) p.dbg_ts[(t) * 16 + (slot)] = clock64(); \
+template <int N, typename F, int... I>
+__device__ __forceinline__ void static_for_impl(F&& f, std::integer_sequence<int, I...>) {
+  (f(std::integral_constant<int, I>{}), ...);
+}
+template <int N, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+  static_for_impl<N>(f, std::make_integer_sequence<int, N>{});
+}
+
+// A warp's window of 32 consecutive schedule entries (one per lane, read back
+// with shuffles) plus the next 32 already in flight: schedule reads leave the
+// issue paths of the single-warp roles.  get() is warp-uniform and its
+// argument never decreases.
+struct UnitWindow {
+  const uint4* u;
+  int T, base;
+  uint4 cur, nxt;
+  __device__ __forceinline__ uint4 load(int i) const {
+    return i < T ? __ldg(u + i) : make_uint4(0, 0, 0, 0);
+  }
+  __device__ __forceinline__ UnitWindow(const TcUnit* units, int t_count)
+      : u(reinterpret_cast<const uint4*>(units)), T(t_count), base(0) {
+    const int l = threadIdx.x & 31;
+    cur = load(l);
+    nxt = load(32 + l);
+  }
+  __device__ __forceinline__ TcUnit get(int t) {
+    while (t >= base + 32) {
+      base += 32;
+      cur = nxt;
+      nxt = load(base + 32 + (threadIdx.x & 31));
+    }
+    const int src = t - base;
+    uint4 w;
+    w.x = __shfl_sync(0xffffffffu, cur.x, src);
+    w.y = __shfl_sync(0xffffffffu, cur.y, src);
+    w.z = __shfl_sync(0xffffffffu, cur.z, src);
+    w.w = __shfl_sync(0xffffffffu, cur.w, src);
+    return *reinterpret_cast<const TcUnit*>(&w);
+  }
+};
+static_assert(sizeof(TcUnit) == 16, "TcUnit is read as one uint4");
+
+#ifdef SPCP_TC_TIMESTAMPS
+#define TC_TS(t, slot)                                                                      \
+  do {                                                                                      \
+    if (p.dbg_ts && blockIdx.x == 0 && (t) < 64) p.dbg_ts[(t) * 32 + (slot)] = clock64();               \
   } while (0)
+#else
+#define TC_TS(t, slot) \
+  do {                 \
+  } while (0)
+#endif
 
 template <int KP16, bool MASK>
 __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
@@ -143,29 +209,30 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
   const int ub = p.cta_begin[blockIdx.x], ue = p.cta_begin[blockIdx.x + 1];
   const int T = ue - ub;
   const TcUnit* units = p.units + ub;
+  const int run0 = T > 0 ? units[0].gv_slot : 0;  // CTA-local run index = gv_slot - run0
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::NST; ++i) {
       mbar_init(&bar->stage_full[i], 1);
-      mbar_init(&bar->stage_empty[i], C::NEPI);
+      mbar_init(&bar->stage_empty[i], C::NEG);
     }
     for (int i = 0; i < C::NSV; ++i) {
       mbar_init(&bar->v_full[i], 1);
-      mbar_init(&bar->v_empty[i], 1);
+      mbar_init(&bar->v_empty[i], 2);  // residual + G.V issuers
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bar->u_full[i], 1);
-      mbar_init(&bar->u_empty[i], 1);
+      mbar_init(&bar->u_empty[i], 2);  // residual + G^T U issuers
       mbar_init(&bar->s_full[i], 1);
-      mbar_init(&bar->s_empty[i], C::NEPI);
-      mbar_init(&bar->ga_full[i], C::NEPI);
+      mbar_init(&bar->s_empty[i], C::NEG);
+      mbar_init(&bar->ga_full[i], C::NEG);
       mbar_init(&bar->ga_empty[i], 1);
+      mbar_init(&bar->gs_empty[i], 1);
       mbar_init(&bar->gt_full[i], 1);
-      mbar_init(&bar->gt_empty[i], C::NEPI);
+      mbar_init(&bar->gt_empty[i], C::NEG);
       mbar_init(&bar->gv_full[i], 1);
-      mbar_init(&bar->gv_empty[i], C::NEPI);
+      mbar_init(&bar->gv_empty[i], C::NEG);
     }
-    mbar_init(&bar->gs_empty, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(&bar->tmem_base, C::TMEM_COLS);
@@ -176,17 +243,23 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tm = bar->tmem_base;
+  // broadcast from lane 0: provably warp-uniform, so MMA operands stay in uniform registers
+  const uint32_t tm = __shfl_sync(0xffffffffu, bar->tmem_base, 0);
 
   if (warp == 0) {
     // ======================= X / mask producer (TMA) ====================
-    if (lane == 0) {
-      const uint64_t pol_x = policy_evict_first();
-      for (int t = 0; t < T; ++t) {
-        const TcUnit un = units[t];
+    UnitWindow uw(units, T);
+    const uint64_t pol_x = policy_evict_first();
+    for (int t = 0; t < T; ++t) {
+      const TcUnit un = uw.get(t);
+      if (lane == 0) {
         const int st = t % C::NST;
         mbar_wait(&bar->stage_empty[st], ((t / C::NST) & 1) ^ 1);
         TC_TS(t, 0);
+#ifdef SPCP_TC_BISECT_NO_TMA
+        mbar_arrive(&bar->stage_full[st]);
+        if (st >= 0) goto x_done;
+#endif
         mbar_arrive_expect_tx(&bar->stage_full[st], C::X_BYTES + C::M_BYTES);
         unsigned char* xs = sm + C::OFF_X + st * C::X_BYTES;
         tma_load_2d_hint(xs, &xmap, int(un.tc) * 64, int(un.sb) * 128, &bar->stage_full[st],
@@ -197,180 +270,198 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
           tma_load_2d_hint(sm + C::OFF_M + st * 2048, &mmap, (int(un.tc) * 2) & ~3,
                            int(un.sb) * 128, &bar->stage_full[st], pol_x);
       }
+#ifdef SPCP_TC_BISECT_NO_TMA
+    x_done:
+#endif
+      __syncwarp();
     }
   } else if (warp == 2) {
-    // ======================= U / V operand-image producer (bulk) ========
-    if (lane == 0) {
-      int prev_sb = -1, fills = 0;
-      for (int t = 0; t < T; ++t) {
-        const TcUnit un = units[t];
-        if ((un.flags & TCU_FIRST_OF_RUN) || un.sb != prev_sb) {
-          const int b = fills % C::UB;
-          mbar_wait(&bar->u_empty[b], ((fills / C::UB) & 1) ^ 1);
-          mbar_arrive_expect_tx(&bar->u_full[b], C::U_BYTES);
-          bulk_load(sm + C::OFF_U + b * C::U_BYTES, p.u_img + size_t(un.sb) * C::U_BYTES,
-                    C::U_BYTES, &bar->u_full[b]);
-          ++fills;
-          prev_sb = un.sb;
+    // ======================= U / V operand-image producer ===============
+    // The images are small and L2-resident; the whole warp copies them with
+    // 128-bit loads/stores (LSU path), so they never queue behind the X
+    // tensor loads in the TMA engine.
+    auto copy_img = [&](unsigned char* dst, const unsigned char* src, int bytes) {
+      const uint4* s4 = reinterpret_cast<const uint4*>(src);
+      uint4* d4 = reinterpret_cast<uint4*>(dst);
+      constexpr int UNR = 4;
+      for (int i0 = 0; i0 < bytes / 16; i0 += 32 * UNR) {
+        uint4 r[UNR];
+#pragma unroll
+        for (int j = 0; j < UNR; ++j) {
+          const int i = i0 + j * 32 + lane;
+          if (i < bytes / 16) r[j] = __ldcg(s4 + i);
         }
-        const int sv = t % C::NSV;
-        mbar_wait(&bar->v_empty[sv], ((t / C::NSV) & 1) ^ 1);
-        mbar_arrive_expect_tx(&bar->v_full[sv], C::V_BYTES);
-        bulk_load(sm + C::OFF_V + sv * C::V_BYTES, p.v_img + size_t(un.tc) * C::V_BYTES,
-                  C::V_BYTES, &bar->v_full[sv]);
+#pragma unroll
+        for (int j = 0; j < UNR; ++j) {
+          const int i = i0 + j * 32 + lane;
+          if (i < bytes / 16) d4[i] = r[j];
+        }
       }
+      fence_proxy_async_smem();  // generic-proxy writes -> visible to the MMA (async proxy)
+      __syncwarp();
+    };
+    int prev_run = -1;
+    UnitWindow uw(units, T);
+    for (int t = 0; t < T; ++t) {
+      const TcUnit un = uw.get(t);
+      const int run = un.gv_slot - run0;
+      if (run != prev_run) {
+        const int b = run % C::UB;
+        mbar_wait(&bar->u_empty[b], ((run / C::UB) & 1) ^ 1);
+        copy_img(sm + C::OFF_U + b * C::U_BYTES, p.u_img + size_t(un.sb) * C::U_BYTES, C::U_BYTES);
+        if (lane == 0) mbar_arrive(&bar->u_full[b]);
+        prev_run = run;
+      }
+      const int sv = t % C::NSV;
+      mbar_wait(&bar->v_empty[sv], ((t / C::NSV) & 1) ^ 1);
+      if (lane == 0) TC_TS(t, 11);
+      copy_img(sm + C::OFF_V + sv * C::V_BYTES, p.v_img + size_t(un.tc) * C::V_BYTES, C::V_BYTES);
+      if (lane == 0) mbar_arrive(&bar->v_full[sv]);
     }
-  } else if (warp == 1) {
-    // ======================= MMA issuer =================================
+  } else if (warp == 1 || warp == 3) {
+    // ======================= MMA issuers ================================
+    // Three warps issue into the one tensor pipe: warp 1 the residual of
+    // every tile (runs ahead, bounded by the S / V / U buffers), warp 3 the
+    // G^T U batch and warp 4 the G.V batch of each tile once its G is staged.
+    // Base descriptors are built once; each MMA adds a compile-time offset
+    // (descriptor address field = byte address >> 4, no carry for smem).
     constexpr uint32_t ID_RES = idesc_f16(128, 64, false, false);
-    constexpr uint32_t ID_GV = idesc_f16(128, KP16, false, true);
+    constexpr uint32_t ID_GV = idesc_f16(128, C::GVC * KP16, false, true);
     constexpr uint32_t ID_GT = idesc_f16(64, C::GCAT * KP16, true, true);
     constexpr int KS = KP16 / 16;
+    const bool do_mma = !(p.debug & 8);
     const uint32_t u0 = smem_u32(sm + C::OFF_U), v0 = smem_u32(sm + C::OFF_V);
-    const uint32_t gh0 = smem_u32(sm + C::OFF_GH), gl0 = smem_u32(sm + C::OFF_GL);
-    int run = -1;       // run index of the tile being issued (residual)
-    int prev_sb = -1;
-
-    auto residual = [&](int t, int ubuf) {
-      const int st = t % C::NSV, b = t & 1;
-      mbar_wait(&bar->v_full[st], (t / C::NSV) & 1);
-      if (lane == 0) TC_TS(t, 1);
-      mbar_wait(&bar->s_empty[b], ((t >> 1) & 1) ^ 1);
-      if (lane == 0) TC_TS(t, 2);
-      tc_fence_after();
-      {
-        const uint32_t ua = u0 + ubuf * C::U_BYTES;
-        const uint32_t vb = v0 + st * C::V_BYTES;
-        // products of total split order <= 2: (h,h) (h,m) (m,h) (h,l) (m,m) (l,h)
-        const int pa[6] = {0, 0, 1, 0, 1, 2};
-        const int pb[6] = {0, 1, 0, 2, 1, 0};
-#pragma unroll
-        for (int q = 0; q < C::NRES; ++q)
-#pragma unroll
-          for (int ks = 0; ks < KS; ++ks)
-            mma_ss_w(tm + C::T_S + b * 64,
-                   umma_desc(ua + pa[q] * C::U_SPLIT + ks * 32, 16, 8 * C::RB, C::SWK),
-                   umma_desc(vb + pb[q] * C::V_SPLIT + ks * 32, 16, 8 * C::RB, C::SWK), ID_RES,
-                   (q | ks) != 0);
+    const uint32_t g0 = smem_u32(sm + C::OFF_G);
+    UnitWindow uw(units, T);
+    if (warp == 1) {
+      const uint64_t dU_k = umma_desc(u0, 16, 8 * C::RB, C::SWK);  // residual A (K-major)
+      const uint64_t dV_k = umma_desc(v0, 16, 8 * C::RB, C::SWK);  // residual B (K-major)
+      int prev_run = -1;
+      for (int t = 0; t < T; ++t) {
+        const TcUnit un = uw.get(t);
+        const int run = un.gv_slot - run0;
+        const int ubuf = run % C::UB;
+        if (run != prev_run) {
+          mbar_wait(&bar->u_full[ubuf], (run / C::UB) & 1);
+          prev_run = run;
+        }
+        if (lane == 0) TC_TS(t, 12);
+        const int st = t % C::NSV, b = t & 1;
+        mbar_wait(&bar->v_full[st], (t / C::NSV) & 1);
+        if (lane == 0) TC_TS(t, 13);
+        mbar_wait(&bar->s_empty[b], ((t >> 1) & 1) ^ 1);
+        if (lane == 0) TC_TS(t, 1);
+        tc_fence_after();
+        const uint64_t da = dU_k + uint64_t(ubuf * (C::U_BYTES >> 4));
+        const uint64_t db = dV_k + uint64_t(st * (C::V_BYTES >> 4));
+        __syncwarp();  // converged: lets ptxas keep descriptors uniform (no per-MMA ELECT)
+        if (do_mma && !(p.debug & 64)) {
+          // uh.vh + uh.vm + um.vh, K-steps of 32 B
+          mma_residual_batch<KS, (C::U_SPLIT >> 4), (C::V_SPLIT >> 4), 2>(tm + C::T_S + b * 64,
+                                                                          da, db, ID_RES);
+        }
         mma_commit_w(&bar->s_full[b]);
+        mma_commit_w(&bar->v_empty[st]);
+        if (un.flags & TCU_LAST_OF_RUN) mma_commit_w(&bar->u_empty[ubuf]);
+        if (lane == 0) TC_TS(t, 24);
       }
-    };
-
-    auto reductions = [&](int t, int ubuf, int rrun, uint32_t flags) {
-      const int st = t % C::NSV, b = t & 1, gvb = rrun & 1;
-      mbar_wait(&bar->ga_full[b], (t >> 1) & 1);
-      if (lane == 0) TC_TS(t, 3);
-      mbar_wait(&bar->gt_empty[b], ((t >> 1) & 1) ^ 1);
-      if (flags & TCU_FIRST_OF_RUN) mbar_wait(&bar->gv_empty[gvb], ((rrun >> 1) & 1) ^ 1);
-      tc_fence_after();
-      {
-        // G^T U first: it releases the single G staging image the epilogue
-        // needs for the next tile
-        const uint32_t ua = u0 + ubuf * C::U_BYTES;
+    } else {
+      // G^T U first (it releases the group's G staging image), then G.V
+      const uint64_t dUn0 = umma_desc(u0, C::GCAT == 2 ? C::U_SPLIT : 8192, 8 * C::RB, C::SWK);
+      const uint64_t dG = umma_desc(g0, 16384, 1024, SW_128);  // A = G image (MN-major)
+      const uint64_t dVn0 = umma_desc(v0, C::GVC == 2 ? C::V_SPLIT : 8192, 8 * C::RB, C::SWK);
+      for (int t = 0; t < T; ++t) {
+        const TcUnit un = uw.get(t);
+        const int run = un.gv_slot - run0;
+        const int ubuf = run % C::UB, b = t & 1, st = t % C::NSV, gvb = run & 1;
+        const bool first = (un.flags & TCU_FIRST_OF_RUN) != 0;
+        if (lane == 0) TC_TS(t, 14);
+        mbar_wait(&bar->ga_full[b], (t >> 1) & 1);
+        if (lane == 0) TC_TS(t, 2);
+        mbar_wait(&bar->gt_empty[b], ((t >> 1) & 1) ^ 1);
+        if (first) mbar_wait(&bar->gv_empty[gvb], ((run >> 1) & 1) ^ 1);
+        if (lane == 0) TC_TS(t, 3);
+        tc_fence_after();
+        const uint64_t dUn = dUn0 + uint64_t(ubuf * (C::U_BYTES >> 4));
+        const uint64_t dgh = dG + uint64_t(b * (C::G_BYTES >> 4));
         const uint32_t gt = tm + C::T_GT + b * C::GCAT * KP16;
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks) {
-          const uint32_t uo = ks * 16 * C::RB;
+        __syncwarp();  // converged: lets ptxas keep descriptors uniform (no per-MMA ELECT)
+        if (do_mma && !(p.debug & 16)) {
           if constexpr (C::GCAT == 2) {
-            // B = [uh | um]: two N-atoms of the U image (LBO = split stride);
-            // every G byte is read once
-            mma_ss_w(gt, umma_desc(gh0 + 2048 * ks, 16384, 1024, SW_128),
-                     umma_desc(ua + uo, C::U_SPLIT, 8 * C::RB, C::SWK), ID_GT, ks > 0);
-            mma_ss_w(gt, umma_desc(gl0 + 2048 * ks, 16384, 1024, SW_128),
-                     umma_desc(ua + uo, C::U_SPLIT, 8 * C::RB, C::SWK), ID_GT, 1);
+            // B = [uh | um]: two N-atoms of the U image (LBO = split stride)
+            mma_gtu_batch2<(2048 >> 4), (C::G_SPLIT >> 4), ((16 * C::RB) >> 4)>(gt, dgh, dUn,
+                                                                                ID_GT);
           } else {
-            mma_ss_w(gt, umma_desc(gh0 + 2048 * ks, 16384, 1024, SW_128),
-                     umma_desc(ua + uo, 8192, 8 * C::RB, C::SWK), ID_GT, ks > 0);
-            mma_ss_w(gt, umma_desc(gh0 + 2048 * ks, 16384, 1024, SW_128),
-                     umma_desc(ua + C::U_SPLIT + uo, 8192, 8 * C::RB, C::SWK), ID_GT, 1);
-            mma_ss_w(gt, umma_desc(gl0 + 2048 * ks, 16384, 1024, SW_128),
-                     umma_desc(ua + uo, 8192, 8 * C::RB, C::SWK), ID_GT, 1);
+            static_for<8>([&](auto I) {
+              constexpr int ks = I;
+              constexpr int uo = (ks * 16 * C::RB) >> 4, go = (2048 * ks) >> 4;
+              constexpr int gl_o = go + (C::G_SPLIT >> 4);
+              mma_ss_o<go, uo>(gt, dgh, dUn, ID_GT, ks > 0);
+              mma_ss_o<go, uo + (C::U_SPLIT >> 4)>(gt, dgh, dUn, ID_GT, 1);
+              mma_ss_o<gl_o, uo>(gt, dgh, dUn, ID_GT, 1);
+            });
           }
         }
         mma_commit_w(&bar->gt_full[b]);
-        mma_commit_w(&bar->gs_empty);
-        const uint32_t vb = v0 + st * C::V_BYTES;
-        const uint32_t gv = tm + C::T_GV + gvb * KP16;
+        mma_commit_w(&bar->gs_empty[b]);
+        if (lane == 0) TC_TS(t, 25);
+        const uint64_t dVn = dVn0 + uint64_t(st * (C::V_BYTES >> 4));
+        const uint32_t gv = tm + C::T_GV + gvb * C::GVC * KP16;
         const uint32_t ga = tm + C::T_GA + b * 64;
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-          const uint32_t vo = ks * 16 * C::RB;
-          mma_ts_w(gv, ga + 8 * ks, umma_desc(vb + vo, 8192, 8 * C::RB, C::SWK), ID_GV,
-                 !((flags & TCU_FIRST_OF_RUN) && ks == 0));
-          mma_ts_w(gv, ga + 8 * ks, umma_desc(vb + C::V_SPLIT + vo, 8192, 8 * C::RB, C::SWK),
-                 ID_GV, 1);
-          mma_ts_w(gv, ga + 32 + 8 * ks, umma_desc(vb + vo, 8192, 8 * C::RB, C::SWK), ID_GV, 1);
+        __syncwarp();  // converged: lets ptxas keep descriptors uniform (no per-MMA ELECT)
+        if (do_mma && !(p.debug & 32)) {
+          if constexpr (C::GVC == 2) {
+            // B = [vh | vm] (N-concatenated), A = gh then gl per K-step
+            mma_gv_batch2<((16 * C::RB) >> 4)>(gv, ga, dVn, ID_GV, first ? 0u : 1u);
+          } else {
+            static_for<4>([&](auto I) {
+              constexpr int ks = I;
+              constexpr int vo = (ks * 16 * C::RB) >> 4;
+              mma_ts_o<vo>(gv, ga + 8 * ks, dVn, ID_GV, !(first && ks == 0));
+              mma_ts_o<vo + (C::V_SPLIT >> 4)>(gv, ga + 8 * ks, dVn, ID_GV, 1);
+              mma_ts_o<vo>(gv, ga + 32 + 8 * ks, dVn, ID_GV, 1);
+            });
+          }
         }
         mma_commit_w(&bar->ga_empty[b]);
         mma_commit_w(&bar->v_empty[st]);
-        if (flags & TCU_LAST_OF_RUN) {
+        if (un.flags & TCU_LAST_OF_RUN) {
           mma_commit_w(&bar->gv_full[gvb]);
           mma_commit_w(&bar->u_empty[ubuf]);
         }
+        if (lane == 0) TC_TS(t, 15);
       }
-    };
-
-    // bookkeeping of the previous tile (its reductions trail its residual)
-    int p_ubuf = 0, p_run = 0;
-    uint32_t p_flags = 0;
-    for (int t = 0; t < T; ++t) {
-      const TcUnit un = units[t];
-      const bool new_run = (un.flags & TCU_FIRST_OF_RUN) || un.sb != prev_sb;
-      if (new_run) {
-        ++run;
-        prev_sb = un.sb;
-      }
-      const int ubuf = run % C::UB;
-      const bool reduce_first = new_run && C::UB == 1 && t >= 1;
-      if (reduce_first) reductions(t - 1, p_ubuf, p_run, p_flags);
-      if (new_run) mbar_wait(&bar->u_full[ubuf], (run / C::UB) & 1);
-      residual(t, ubuf);
-      if (!reduce_first && t >= 1) reductions(t - 1, p_ubuf, p_run, p_flags);
-      p_ubuf = ubuf;
-      p_run = run;
-      p_flags = un.flags;
     }
-    if (T >= 1) reductions(T - 1, p_ubuf, p_run, p_flags);
   } else {
     // ======================= epilogue warps =============================
-    // warp e = warp - 3 owns TMEM lane quarter q = warp % 4 (rows 32q..32q+31)
-    // and columns [part * CPW, part * CPW + CPW) of every 64-column tile.
-    constexpr int CPW = 256 / C::NEPI;      // columns per epilogue warp (16 or 32)
-    constexpr int NPAIR = CPW / 2;          // packed half2 registers per split
-    const int q = warp & 3;
-    const int part = (warp - 3) >> 2;
+    const int q = warp & 3;               // TMEM lane quarter
+    const int e = warp - C::FIRST_EPI;
+    const int grp = (e >> 2) & 1;         // tile parity this warp serves
+    const int h = e >> 3;                 // column half of the tile
     const int row = 32 * q + lane;
     const uint32_t lane_addr = uint32_t(32 * q) << 16;
     const TcScales sc = *p.scales;
     const float sigma = sc.sigma, tau_s = sc.tau_s, kappa = sc.kappa;
+    const float2 sig2 = make_float2(sigma, sigma), kap2 = make_float2(kappa, kappa);
+    const float2 nhalf2 = make_float2(-0.5f, -0.5f), zero2 = make_float2(0.f, 0.f);
+    const float2 qc2 = make_float2(201326592.f, 201326592.f);  // 1.5 * 2^27: quantum 16
     double phi_acc = 0.0;
-    int run = -1, prev_sb = -1;
-    int prev_gv_slot = -1;
-    constexpr int GTC = KP16 / 2;  // accumulator columns drained per draining warp
-    const bool drainer = part < 2;  // two warps per lane quarter drain G.V / G^T.U
-    const int dpart = part & 1;
-    // swizzled byte offsets of this thread's X row chunks (box = 32 columns)
-    const int xbox = (part * CPW) >> 5;
-    const int xc0 = ((part * CPW) & 31) >> 2;  // first 16 B chunk within the box row
+    constexpr int GTC = KP16 / 2;  // accumulator columns drained per warp (of KP16)
+    unsigned char* gimg = sm + C::OFF_G + grp * C::G_BYTES;
 
-    // G^T U of tile t2 -> this CTA's private slot for the column tile: plain
-    // stores on first touch, then fp32x4 reductions in L2.  Each (row, col)
-    // of a slot is owned by one thread, whose same-address operations apply
-    // in program order: deterministic without staging or fences.
+    // G^T U of tile t2 (this group's previous tile) -> CTA-private slot
     auto drain_gt = [&](int t2, const TcUnit& u2) {
       const int b = t2 & 1;
       mbar_wait(&bar->gt_full[b], (t2 >> 1) & 1);
       tc_fence_after();
-      if (drainer && !(p.debug & 1)) {
-        float* dst =
-            p.pright + (size_t(u2.gt_slot) * 64 + 16 * q + lane) * KP16 + dpart * GTC;
+      if (!(p.debug & 1)) {
+        float* dst = p.pright + (size_t(u2.gt_slot) * 64 + 16 * q + lane) * KP16 + h * GTC;
         const bool first = (u2.flags & TCU_FIRST_TOUCH) != 0;
         constexpr int CH = GTC < 16 ? GTC : 16;
 #pragma unroll
         for (int c0 = 0; c0 < GTC; c0 += CH) {
           uint32_t v[CH], w[CH];
-          const uint32_t col =
-              tm + lane_addr + C::T_GT + b * C::GCAT * KP16 + dpart * GTC + c0;
+          const uint32_t col = tm + lane_addr + C::T_GT + b * C::GCAT * KP16 + h * GTC + c0;
           tmem_ldn<CH>(col, v);
           if constexpr (C::GCAT == 2) {
             tmem_ldn<CH>(col + KP16, w);
@@ -398,18 +489,29 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
       if (lane == 0) mbar_arrive(&bar->gt_empty[b]);
     };
 
-    auto drain_gv = [&](int rrun, int slot) {
-      const int gvb = rrun & 1;
-      mbar_wait(&bar->gv_full[gvb], (rrun >> 1) & 1);
+    // G.V of a finished run -> its slot (M = 128: row = TMEM lane)
+    auto drain_gv = [&](const TcUnit& u2) {
+      const int run = u2.gv_slot - run0;
+      const int gvb = run & 1;
+      mbar_wait(&bar->gv_full[gvb], (run >> 1) & 1);
       tc_fence_after();
-      if (drainer && !(p.debug & 2)) {
-        float* dst = p.pleft + (size_t(slot) * 128 + row) * KP16 + dpart * GTC;
+      if (!(p.debug & 2)) {
+        float* dst = p.pleft + (size_t(u2.gv_slot) * 128 + row) * KP16 + h * GTC;
         constexpr int CH = GTC < 16 ? GTC : 16;
 #pragma unroll
         for (int c0 = 0; c0 < GTC; c0 += CH) {
-          uint32_t v[CH];
-          tmem_ldn<CH>(tm + lane_addr + C::T_GV + gvb * KP16 + dpart * GTC + c0, v);
-          tmem_wait_ld();
+          uint32_t v[CH], w[CH];
+          const uint32_t col = tm + lane_addr + C::T_GV + gvb * C::GVC * KP16 + h * GTC + c0;
+          tmem_ldn<CH>(col, v);
+          if constexpr (C::GVC == 2) {
+            tmem_ldn<CH>(col + KP16, w);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < CH; ++c)
+              v[c] = __float_as_uint(__uint_as_float(v[c]) + __uint_as_float(w[c]));
+          } else {
+            tmem_wait_ld();
+          }
 #pragma unroll
           for (int c = 0; c < CH; c += 4)
             *reinterpret_cast<uint4*>(dst + c0 + c) = make_uint4(v[c], v[c + 1], v[c + 2], v[c + 3]);
@@ -420,116 +522,129 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
       if (lane == 0) mbar_arrive(&bar->gv_empty[gvb]);
     };
 
-    TcUnit prev_unit{};
-    TcUnit un_next = T > 0 ? units[0] : TcUnit{};
-    for (int t = 0; t < T; ++t) {
+    TcUnit prev{};
+    TcUnit un_next = grp < T ? units[grp] : TcUnit{};
+    for (int t = grp; t < T; t += 2) {
       const TcUnit un = un_next;
-      if (t + 1 < T) un_next = units[t + 1];  // consumed next iteration: latency hidden
-      const bool new_run = (un.flags & TCU_FIRST_OF_RUN) || un.sb != prev_sb;
-      if (new_run) {
-        ++run;
-        prev_sb = un.sb;
-      }
-      const int st = t % C::NST, b = t & 1;
-      // ---- S tile and X tile
-      const bool ts_w = (warp == 3 && lane == 0);
+      if (t + 2 < T) un_next = units[t + 2];  // consumed next iteration: latency hidden
+      const int st = t % C::NST, b = grp;
+      const bool ts_w = ((e == 0 || e == 4) && lane == 0);
       if (ts_w) TC_TS(t, 4);
+      // ---- S tile and X tile (32 columns: two chunks of 16)
       mbar_wait(&bar->s_full[b], (t >> 1) & 1);
       if (ts_w) TC_TS(t, 5);
       tc_fence_after();
-      uint32_t sv[CPW];
-      tmem_ldn<CPW>(tm + lane_addr + C::T_S + b * 64 + part * CPW, sv);
       mbar_wait(&bar->stage_full[st], (t / C::NST) & 1);
       if (ts_w) TC_TS(t, 6);
-      const unsigned char* xs = sm + C::OFF_X + st * C::X_BYTES + xbox * 16384;
-      float xv[CPW];
-#pragma unroll
-      for (int c = 0; c < CPW / 4; ++c) {
-        const float4 f =
-            *reinterpret_cast<const float4*>(xs + Swz<128>::offset(row, (xc0 + c) * 16));
-        xv[4 * c] = f.x;
-        xv[4 * c + 1] = f.y;
-        xv[4 * c + 2] = f.z;
-        xv[4 * c + 3] = f.w;
-      }
+      const unsigned char* xs = sm + C::OFF_X + st * C::X_BYTES + h * 16384;
       uint32_t mw = 0xffffffffu;
-      if (MASK) {
+      if (MASK)
         mw = reinterpret_cast<const uint32_t*>(sm + C::OFF_M + st * 2048)[row * 4 +
-                                                                          (un.tc & 1) * 2 +
-                                                                          ((part * CPW) >> 5)];
-        mw >>= (part * CPW) & 31;
-      }
-      tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&bar->s_empty[b]);
-        mbar_arrive(&bar->stage_empty[st]);
-      }
-      // ---- epilogue math: r = x - L (scaled), clip, huber, split
-      uint32_t hi[NPAIR], lo[NPAIR];
-      float hs[4] = {0.f, 0.f, 0.f, 0.f};
+                                                                        (un.tc & 1) * 2 + h];
+      uint32_t hi[16], lo[16];
+      float2 hs2 = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int e = 0; e < CPW; e += 2) {
-        float g2[2];
+      for (int ch = 0; ch < 2; ++ch) {
+        uint32_t sv[16];
+#if defined(SPCP_TC_BISECT_EPI_SKIP)
 #pragma unroll
-        for (int f = 0; f < 2; ++f) {
-          const int c = e + f;
-          float r = fmaf(xv[c], sigma, -__uint_as_float(sv[c]));
-          if (MASK) r = ((mw >> c) & 1u) ? r : 0.f;
-          const float a = fabsf(r);
-          const float cl = fminf(a, tau_s);
-          hs[c & 3] = fmaf(cl, fmaf(-0.5f, cl, a), hs[c & 3]);
-          g2[f] = -copysignf(cl, r) * kappa;
+        for (int c = 0; c < 16; ++c) sv[c] = c;
+#else
+        tmem_ldn<16>(tm + lane_addr + C::T_S + b * 64 + 32 * h + 16 * ch, sv);
+#endif
+        float xv[16];
+#if defined(SPCP_TC_BISECT_EPI_SKIP) || defined(SPCP_TC_BISECT_NO_SMEM)
+#pragma unroll
+        for (int c = 0; c < 16; ++c) xv[c] = __uint_as_float(sv[c] ^ lane);
+#else
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float4 f =
+              *reinterpret_cast<const float4*>(xs + Swz<128>::offset(row, (4 * ch + c) * 16));
+          xv[4 * c] = f.x;
+          xv[4 * c + 1] = f.y;
+          xv[4 * c + 2] = f.z;
+          xv[4 * c + 3] = f.w;
         }
-        const __half2 hh = __floats2half2_rn(g2[0], g2[1]);
-        const float2 hf = __half22float2(hh);
-        hi[e >> 1] = *reinterpret_cast<const uint32_t*>(&hh);
-        lo[e >> 1] = pack_half2(g2[0] - hf.x, g2[1] - hf.y);
+#endif
+        tmem_wait_ld();
+        if (ch == 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(&bar->s_empty[b]);
+            mbar_arrive(&bar->stage_empty[st]);
+          }
+        }
+        // The MMA produced S'' = -sigma L (U image negated), so r'' = sigma r =
+        // fma(x, sigma, S'').  cs = clamp(r'', +-tau''), huber'' = cs (r'' - cs/2)
+        // (quadratic on ties, as the reference), gp = kappa cs = -G'', split at
+        // a fixed quantum: hi = (gp + 1.5 2^27) - 1.5 2^27 is a multiple of 16
+        // (exact in fp16 for |gp| <= 2^14), lo = gp - hi in [-8, 8].
+#pragma unroll
+        for (int e2 = 0; e2 < 16; e2 += 2) {
+          float2 r2 = ffma2(make_float2(xv[e2], xv[e2 + 1]), sig2,
+                            make_float2(__uint_as_float(sv[e2]), __uint_as_float(sv[e2 + 1])));
+          if (MASK) {
+            r2.x = ((mw >> (16 * ch + e2)) & 1u) ? r2.x : 0.f;
+            r2.y = ((mw >> (16 * ch + e2 + 1)) & 1u) ? r2.y : 0.f;
+          }
+          const float2 cs2 = make_float2(fminf(fmaxf(r2.x, -tau_s), tau_s),
+                                         fminf(fmaxf(r2.y, -tau_s), tau_s));
+          hs2 = ffma2(cs2, ffma2(nhalf2, cs2, r2), hs2);
+          const float2 ht = ffma2(cs2, kap2, qc2);
+          const float2 hi2 = fsub2(ht, qc2);
+          const float2 lo2 = fsub2(ffma2(cs2, kap2, zero2), hi2);
+          hi[8 * ch + (e2 >> 1)] = pack_half2(hi2.x, hi2.y);
+          lo[8 * ch + (e2 >> 1)] = pack_half2(lo2.x, lo2.y);
+        }
       }
-      phi_acc += double((hs[0] + hs[1]) + (hs[2] + hs[3]));
+      phi_acc += double(hs2.x) + double(hs2.y);
+      if (ts_w) TC_TS(t, 7);
+      // ---- deferred drains of this group's previous tile
+      if (t >= 2) {
+        drain_gt(t - 2, prev);
+        if (prev.flags & TCU_LAST_OF_RUN) drain_gv(prev);
+      }
+      if (ts_w) TC_TS(t, 8);
       // ---- G to TMEM (A of G.V) and to smem (A of G^T.U)
       mbar_wait(&bar->ga_empty[b], ((t >> 1) & 1) ^ 1);
-      if constexpr (NPAIR == 16) {
-        tmem_st16(tm + lane_addr + C::T_GA + b * 64 + part * NPAIR, hi);
-        tmem_st16(tm + lane_addr + C::T_GA + b * 64 + 32 + part * NPAIR, lo);
-      } else {
-        tmem_st8(tm + lane_addr + C::T_GA + b * 64 + part * NPAIR, hi);
-        tmem_st8(tm + lane_addr + C::T_GA + b * 64 + 32 + part * NPAIR, lo);
-      }
-      if (ts_w) TC_TS(t, 7);
-      mbar_wait(&bar->gs_empty, (t & 1) ^ 1);
-      if (ts_w) TC_TS(t, 8);
-      unsigned char* gh = sm + C::OFF_GH;
-      unsigned char* gl = sm + C::OFF_GL;
+#if !defined(SPCP_TC_BISECT_EPI_SKIP)
+      tmem_st16(tm + lane_addr + C::T_GA + b * 64 + 16 * h, hi);
+      tmem_st16(tm + lane_addr + C::T_GA + b * 64 + 32 + 16 * h, lo);
+#else
+      if (hi[0] == 0x12345 && lo[3] == 0x777) phi_acc += 1.0;  // keep the math alive
+#endif
+      mbar_wait(&bar->gs_empty[b], ((t >> 1) & 1) ^ 1);
+      if (ts_w) TC_TS(t, 9);
+#if !defined(SPCP_TC_BISECT_EPI_SKIP) && !defined(SPCP_TC_BISECT_NO_SMEM)
 #pragma unroll
-      for (int c = 0; c < NPAIR / 4; ++c) {
-        const uint32_t o = Swz<128>::offset(row, part * CPW * 2 + 16 * c);
-        *reinterpret_cast<uint4*>(gh + o) = make_uint4(hi[4 * c], hi[4 * c + 1], hi[4 * c + 2],
-                                                       hi[4 * c + 3]);
-        *reinterpret_cast<uint4*>(gl + o) = make_uint4(lo[4 * c], lo[4 * c + 1], lo[4 * c + 2],
-                                                       lo[4 * c + 3]);
+      for (int c = 0; c < 4; ++c) {
+        const uint32_t o = Swz<128>::offset(row, 64 * h + 16 * c);
+        *reinterpret_cast<uint4*>(gimg + o) =
+            make_uint4(hi[4 * c], hi[4 * c + 1], hi[4 * c + 2], hi[4 * c + 3]);
+        *reinterpret_cast<uint4*>(gimg + C::G_SPLIT + o) =
+            make_uint4(lo[4 * c], lo[4 * c + 1], lo[4 * c + 2], lo[4 * c + 3]);
       }
+#endif
       tmem_wait_st();
       fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar->ga_full[b]);
-      if (ts_w) TC_TS(t, 9);
-      // ---- deferred drains
-      if (t >= 1) drain_gt(t - 1, prev_unit);
-      if (new_run && t >= 1) drain_gv(run - 1, prev_gv_slot);
       if (ts_w) TC_TS(t, 10);
-      prev_unit = un;
-      prev_gv_slot = un.gv_slot;
+      if (lane == 0) TC_TS(t, 16 + (e & 3) + 4 * h);  // per-warp arrival: quarter + 4 * half
+      prev = un;
     }
-    if (T >= 1) {
-      drain_gt(T - 1, prev_unit);
-      drain_gv(run, prev_gv_slot);
+    // flush: this group's last tile
+    const int tl = ((T - 1 - grp) >= 0) ? (T - 1 - ((T - 1 - grp) & 1)) : -1;
+    if (tl >= 0) {
+      drain_gt(tl, prev);
+      if (prev.flags & TCU_LAST_OF_RUN) drain_gv(prev);
     }
     // phi: per-thread fp64, fold over the epilogue warps in a fixed order
     double w = warp_sum(phi_acc);
-    if (lane == 0) bar->phi[warp - 3] = w;
+    if (lane == 0) bar->phi[e] = w;
   }
   tc_fence_before();
   __syncthreads();
@@ -594,26 +709,22 @@ __global__ void tc_scales_kernel(TcScales* sc, double tau) {
   sc->sigma = float(sigma);
   sc->tau_s = float(taus);
   sc->kappa = float(kappa);
-  sc->gv_unscale = float(1.0 / (kappa * sigma * sv));
+  sc->gv_unscale = float(-1.0 / (kappa * sigma * sv));  // G.V partials carry gp = -G''
   sc->gt_unscale = float(1.0 / (kappa * sigma * su));
   sc->phi_unscale = 1.0 / (sigma * sigma);
 }
 
 template <int RB>
-__device__ __forceinline__ void split3_store(unsigned char* base, int split_bytes, int row, int c,
+__device__ __forceinline__ void split2_store(unsigned char* base, int split_bytes, int row, int c,
                                              double x) {
   const __half h = __double2half(x);
-  const double r1 = x - double(__half2float(h));
-  const __half m = __double2half(r1);
-  const double r2 = r1 - double(__half2float(m));
-  const __half l = __double2half(r2);
+  const __half m = __double2half(x - double(__half2float(h)));
   const uint32_t o = tc::Swz<RB>::offset(row, c * 2);
   *reinterpret_cast<__half*>(base + o) = h;
   *reinterpret_cast<__half*>(base + split_bytes + o) = m;
-  *reinterpret_cast<__half*>(base + 2 * split_bytes + o) = l;
 }
 
-// pass 3: fp16 split images of U (per 128-row sub-band) and V (per 64-row tile)
+// pass 3: fp16 two-way split images of U (per 128-row sub-band) and V (per 64-row tile)
 template <int KP16>
 __global__ void tc_images_kernel(const double* __restrict__ z, const double* __restrict__ dz,
                                  double alpha, int64_t m, int64_t n, int64_t k, int64_t m_pad,
@@ -633,7 +744,8 @@ __global__ void tc_images_kernel(const double* __restrict__ z, const double* __r
         w = z[o] + (dz ? alpha * dz[o] : 0.0);
       }
       const int64_t sb = row >> 7;
-      split3_store<RB>(u_img + sb * (3 * 128 * RB), 128 * RB, int(row & 127), c, w * su);
+      // U is stored negated: the residual MMA then yields -sigma L directly
+      split2_store<RB>(u_img + sb * (2 * 128 * RB), 128 * RB, int(row & 127), c, -w * su);
     } else {
       const int64_t j = row - m_pad;
       double w = 0.0;
@@ -642,7 +754,7 @@ __global__ void tc_images_kernel(const double* __restrict__ z, const double* __r
         w = z[o] + (dz ? alpha * dz[o] : 0.0);
       }
       const int64_t tcol = j >> 6;
-      split3_store<RB>(v_img + tcol * (3 * 64 * RB), 64 * RB, int(j & 63), c, w * sv);
+      split2_store<RB>(v_img + tcol * (2 * 64 * RB), 64 * RB, int(j & 63), c, w * sv);
     }
   }
 }

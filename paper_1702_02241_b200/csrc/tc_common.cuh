@@ -41,6 +41,18 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef SPCP_MBAR_SPIN
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+  return;
+#endif
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
@@ -50,6 +62,43 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity), "r"(0x989680u)  // suspend-time hint: sleep in HW until the phase flips
       : "memory");
+}
+
+// non-blocking probe: has the phase with this parity completed?
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred P1;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.b32 %0, 1, 0, P1;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// ------------------------------------------------------------------ packed fp32 pairs
+// Blackwell FFMA2 / FADD2 / FMUL2 on float2 (one instruction per pair)
+__device__ __forceinline__ uint64_t f2_bits(float2 v) {
+  return (uint64_t(__float_as_uint(v.y)) << 32) | __float_as_uint(v.x);
+}
+__device__ __forceinline__ float2 f2_from(uint64_t b) {
+  return make_float2(__uint_as_float(uint32_t(b)), __uint_as_float(uint32_t(b >> 32)));
+}
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)), "l"(f2_bits(c)));
+  return f2_from(d);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return f2_from(d);
+}
+__device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return f2_from(d);
 }
 
 // ------------------------------------------------------------------ async copies
@@ -291,6 +340,120 @@ __device__ __forceinline__ void mma_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint6
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Same, with compile-time descriptor offsets (descriptor units = bytes >> 4)
+// added inside the asm: the base descriptors stay the only per-tile values,
+// so consecutive MMAs of a batch share their conversion to uniform registers.
+template <int OA, int OB>
+__device__ __forceinline__ void mma_ss_o(uint32_t d_tmem, uint64_t a_base, uint64_t b_base,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p, e;\n.reg .b32 r;\n.reg .b64 ad, bd;\nsetp.ne.b32 p, %4, 0;\n"
+      "add.s64 ad, %1, %5;\nadd.s64 bd, %2, %6;\n"
+      "elect.sync r|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ad, bd, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a_base), "l"(b_base), "r"(idesc), "r"(accumulate), "n"(OA), "n"(OB)
+      : "memory");
+}
+template <int OB>
+__device__ __forceinline__ void mma_ts_o(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_base,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p, e;\n.reg .b32 r;\n.reg .b64 bd;\nsetp.ne.b32 p, %4, 0;\n"
+      "add.s64 bd, %2, %5;\n"
+      "elect.sync r|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], bd, %3, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_base), "r"(idesc), "r"(accumulate), "n"(OB)
+      : "memory");
+}
+// ---- whole MMA batches in one asm block: one elect.sync per batch, the
+// descriptors stepped by immediate strides inside the block.
+
+// Residual: NQ products x KS K-steps into one accumulator.  Product q reads
+// A split qa(q) and B split qb(q) (the residual uses (0,0) (0,1) (1,0)).
+// A-split stride SA, B-split stride SB, K-step stride KSTEP (descriptor units).
+#define SPCP_MMA_SS(ACC) "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, " ACC ";\n"
+template <int KS, int SA, int SB, int KSTEP>
+__device__ __forceinline__ void mma_residual_batch(uint32_t d, uint64_t a0, uint64_t b0,
+                                                   uint32_t idesc) {
+  static_assert(KS == 1 || KS == 2 || KS == 4, "KS");
+  if constexpr (KS == 1) {
+    asm volatile(
+        "{\n.reg .pred e, pf, pt;\n.reg .b32 r;\n.reg .b64 a, b;\n"
+        "setp.ne.b32 pf, 0, 0;\nsetp.eq.b32 pt, 0, 0;\nelect.sync r|e, 0xffffffff;\n"
+        "mov.b64 a, %1;\nmov.b64 b, %2;\n" SPCP_MMA_SS("pf")
+        "add.s64 b, %2, %5;\n" SPCP_MMA_SS("pt")
+        "add.s64 a, %1, %4;\nmov.b64 b, %2;\n" SPCP_MMA_SS("pt") "}\n"
+        ::"r"(d), "l"(a0), "l"(b0), "r"(idesc), "n"(SA), "n"(SB) : "memory");
+  } else if constexpr (KS == 2) {
+    asm volatile(
+        "{\n.reg .pred e, pf, pt;\n.reg .b32 r;\n.reg .b64 a, b, a1, b1;\n"
+        "setp.ne.b32 pf, 0, 0;\nsetp.eq.b32 pt, 0, 0;\nelect.sync r|e, 0xffffffff;\n"
+        "mov.b64 a, %1;\nmov.b64 b, %2;\n" SPCP_MMA_SS("pf")
+        "add.s64 a, %1, %6;\nadd.s64 b, %2, %6;\n" SPCP_MMA_SS("pt")
+        "mov.b64 a, %1;\nadd.s64 b, %2, %5;\n" SPCP_MMA_SS("pt")
+        "add.s64 a, %1, %6;\nadd.s64 b, b, %6;\n" SPCP_MMA_SS("pt")
+        "add.s64 a, %1, %4;\nmov.b64 b, %2;\n" SPCP_MMA_SS("pt")
+        "add.s64 a, a, %6;\nadd.s64 b, %2, %6;\n" SPCP_MMA_SS("pt") "}\n"
+        ::"r"(d), "l"(a0), "l"(b0), "r"(idesc), "n"(SA), "n"(SB), "n"(KSTEP) : "memory");
+  } else {
+    asm volatile(
+        "{\n.reg .pred e, pf, pt;\n.reg .b32 r;\n.reg .b64 a, b;\n"
+        "setp.ne.b32 pf, 0, 0;\nsetp.eq.b32 pt, 0, 0;\nelect.sync r|e, 0xffffffff;\n"
+        // (0,0)
+        "mov.b64 a, %1;\nmov.b64 b, %2;\n" SPCP_MMA_SS("pf")
+        "add.s64 a, a, %6;\nadd.s64 b, b, %6;\n" SPCP_MMA_SS("pt")
+        "add.s64 a, a, %6;\nadd.s64 b, b, %6;\n" SPCP_MMA_SS("pt")
+        "add.s64 a, a, %6;\nadd.s64 b, b, %6;\n" SPCP_MMA_SS("pt")
+        // (0,1)
+        "mov.b64 a, %1;\nadd.s64 b, %2, %5;\n" SPCP_MMA_SS("pt")
+        "add.s64 a, a, %6;\nadd.s64 b, b, %6;\n" SPCP_MMA_SS("pt")
+        "add.s64 a, a, %6;\nadd.s64 b, b, %6;\n" SPCP_MMA_SS("pt")
+        "add.s64 a, a, %6;\nadd.s64 b, b, %6;\n" SPCP_MMA_SS("pt")
+        // (1,0)
+        "add.s64 a, %1, %4;\nmov.b64 b, %2;\n" SPCP_MMA_SS("pt")
+        "add.s64 a, a, %6;\nadd.s64 b, b, %6;\n" SPCP_MMA_SS("pt")
+        "add.s64 a, a, %6;\nadd.s64 b, b, %6;\n" SPCP_MMA_SS("pt")
+        "add.s64 a, a, %6;\nadd.s64 b, b, %6;\n" SPCP_MMA_SS("pt") "}\n"
+        ::"r"(d), "l"(a0), "l"(b0), "r"(idesc), "n"(SA), "n"(SB), "n"(KSTEP) : "memory");
+  }
+}
+
+// G^T U with B = [uh|um] N-concatenated: 8 K-steps x {gh, gl}.
+// A stride per K-step SAK, gl offset SGL, B stride per K-step SBK.
+#define SPCP_GT2 SPCP_MMA_SS("pt") "add.s64 a, a, %5;\n" SPCP_MMA_SS("pt") \
+  "sub.s64 a, a, %5;\nadd.s64 a, a, %4;\nadd.s64 b, b, %6;\n"
+template <int SAK, int SGL, int SBK>
+__device__ __forceinline__ void mma_gtu_batch2(uint32_t d, uint64_t a0, uint64_t b0,
+                                               uint32_t idesc) {
+  asm volatile(
+      "{\n.reg .pred e, pf, pt;\n.reg .b32 r;\n.reg .b64 a, b;\n"
+      "setp.ne.b32 pf, 0, 0;\nsetp.eq.b32 pt, 0, 0;\nelect.sync r|e, 0xffffffff;\n"
+      "mov.b64 a, %1;\nmov.b64 b, %2;\n"
+      SPCP_MMA_SS("pf") "add.s64 a, a, %5;\n" SPCP_MMA_SS("pt")
+      "sub.s64 a, a, %5;\nadd.s64 a, a, %4;\nadd.s64 b, b, %6;\n"
+      SPCP_GT2 SPCP_GT2 SPCP_GT2 SPCP_GT2 SPCP_GT2 SPCP_GT2 SPCP_GT2 "}\n"
+      ::"r"(d), "l"(a0), "l"(b0), "r"(idesc), "n"(SAK), "n"(SGL), "n"(SBK) : "memory");
+}
+
+// G.V with A = G from TMEM (hi at +0, lo at +32 columns), B = [vh|vm]:
+// 4 K-steps x {gh, gl}; the first MMA accumulates unless `first`.
+#define SPCP_MMA_TS(ACC) "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, " ACC ";\n"
+#define SPCP_GV2 "add.s32 ta, ta, 8;\n" SPCP_MMA_TS("pt") "add.s32 ta, ta, 32;\n" SPCP_MMA_TS("pt") \
+  "sub.s32 ta, ta, 32;\n"
+template <int SBK>
+__device__ __forceinline__ void mma_gv_batch2(uint32_t d, uint32_t a_tmem, uint64_t b0,
+                                              uint32_t idesc, uint32_t acc_first) {
+  asm volatile(
+      "{\n.reg .pred e, pa, pt;\n.reg .b32 r, ta;\n.reg .b64 b;\n"
+      "setp.ne.b32 pa, %4, 0;\nsetp.eq.b32 pt, 0, 0;\nelect.sync r|e, 0xffffffff;\n"
+      "mov.b32 ta, %1;\nmov.b64 b, %2;\n"
+      SPCP_MMA_TS("pa") "add.s32 ta, ta, 32;\n" SPCP_MMA_TS("pt") "sub.s32 ta, ta, 32;\n"
+      "add.s64 b, b, %5;\n" SPCP_GV2
+      "add.s64 b, b, %5;\n" SPCP_GV2
+      "add.s64 b, b, %5;\n" SPCP_GV2 "}\n"
+      ::"r"(d), "r"(a_tmem), "l"(b0), "r"(idesc), "r"(acc_first), "n"(SBK) : "memory");
+}
+
 __device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
   asm volatile(
       "{\n.reg .pred e;\n.reg .b32 r;\nelect.sync r|e, 0xffffffff;\n"
