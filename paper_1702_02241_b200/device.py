@@ -160,12 +160,21 @@ class DeviceProblem:
                                    self._out))
         return np.frombuffer(self._out, dtype=np.float64).copy()
 
-    def split_objective_host(self, u, v, dtype):
+    def split_objective_host(self, u, v, dtype, out=None):
+        """(f, grad_U, grad_V) for host float64 factors.  `out=(gu, gv)` reuses
+        caller buffers (e.g. pinned memory) instead of allocating fresh arrays."""
         u = np.ascontiguousarray(u, dtype=np.float64)
         v = np.ascontiguousarray(v, dtype=np.float64)
         k = u.shape[1]
-        gu = np.empty_like(u)
-        gv = np.empty_like(v)
+        if out is not None:
+            gu, gv = out
+            if (gu.shape != u.shape or gv.shape != v.shape or gu.dtype != np.float64
+                    or gv.dtype != np.float64 or not gu.flags.c_contiguous
+                    or not gv.flags.c_contiguous):
+                raise ValueError("out buffers must be C-contiguous float64 of the factor shapes")
+        else:
+            gu = np.empty_like(u)
+            gv = np.empty_like(v)
         val = ctypes.c_double()
         check(lib.spcp_split_objective_host(self.h, k, int(dtype),
                                             ctypes.c_void_p(u.ctypes.data),
