@@ -366,7 +366,10 @@ static int tc_build(spcp_problem* p) {
   int runs = 0, slots = 0;
   std::vector<std::vector<int32_t>> u_src(nsb), v_src(ntc);
   for (int c = 0; c < G; ++c) {
-    std::map<int, int> slot_of;  // tc -> global slot, this CTA
+    // G^T U slot per (column tile, tile parity): the two epilogue groups take
+    // alternate tiles, so every slot is written by one thread per address
+    // (program order => deterministic store-then-reduce)
+    std::map<int, int> slot_of;  // 2 * tc + parity -> global slot, this CTA
     for (int i = begin[c]; i < begin[c + 1]; ++i) {
       TcUnit& u = units[i];
       const bool first = (i == begin[c]) || units[i - 1].sb != u.sb;
@@ -377,9 +380,10 @@ static int tc_build(spcp_problem* p) {
       }
       u.gv_slot = runs - 1;
       u.flags = (first ? TCU_FIRST_OF_RUN : 0u) | (last ? TCU_LAST_OF_RUN : 0u);
-      auto it = slot_of.find(u.tc);
+      const int key = 2 * int(u.tc) + ((i - begin[c]) & 1);
+      auto it = slot_of.find(key);
       if (it == slot_of.end()) {
-        slot_of[u.tc] = slots;
+        slot_of[key] = slots;
         v_src[u.tc].push_back(slots);
         u.gt_slot = slots++;
         u.flags |= TCU_FIRST_TOUCH;

@@ -19,7 +19,7 @@
 //   warp 0      X / mask TMA producer (L2 evict-first),
 //   warp 1      residual MMA issuer (+ TMEM owner): runs ahead of the
 //               epilogue, bounded only by the S / V / U buffers,
-//   warp 2      U / V operand-image producer (L2-resident images, LSU copies),
+//   warp 2      U / V operand-image producer (L2-resident images, TMA bulk copies),
 //   warp 3      reduction MMA issuer: G^T U then G.V of each tile once its G
 //               is staged (two issuers keep the tensor pipe fed),
 //   warps 4-19  epilogue, two groups of 8 warps that take alternate tiles
@@ -40,6 +40,10 @@
 #include "tc_common.cuh"
 
 #include <utility>
+
+#ifndef SPCP_TC_XPF
+#define SPCP_TC_XPF 0  // X tiles prefetched into L2 ahead of the stage ring (measured: no gain)
+#endif
 
 namespace spcp {
 
@@ -107,14 +111,14 @@ struct TcCfg {
   static constexpr int OFF_BAR = OFF_M + (MASK ? NST * 2048 : 0);
   static constexpr int SMEM = OFF_BAR + 512;  // dynamic smem base is 1 KB aligned
   static_assert(SMEM <= 232448, "shared memory budget");
-  // TMEM columns: S [2 x 64] | GA [2 x 64: hi 32 + lo 32 packed fp16] |
-  // GV [2 x GVC*KP16] | GT [2 x GCAT*KP16]; the N-concatenated forms hold the
-  // [vh|vm] (resp. [uh|um]) halves side by side, summed at the drain
+  // TMEM columns: S [2 x 64] | GV [2 x GVC*KP16] | GT [4 x GCAT*KP16] (two
+  // per epilogue group); the N-concatenated forms hold the [vh|vm] (resp.
+  // [uh|um]) halves side by side, summed at the drain
   static constexpr int GCAT = KP16 <= 32 ? 2 : 1;
   static constexpr int GVC = KP16 <= 32 ? 2 : 1;
-  static constexpr uint32_t T_S = 0, T_GA = 128, T_GV = 256;
+  static constexpr uint32_t T_S = 0, T_GV = 128;
   static constexpr uint32_t T_GT = T_GV + 2 * GVC * KP16;
-  static_assert(T_GT + 2 * GCAT * KP16 <= 512, "TMEM budget");
+  static_assert(T_GT + 4 * GCAT * KP16 <= 512, "TMEM budget");
   static constexpr uint32_t TMEM_COLS = 512;
   static constexpr int NEPI = 16;  // epilogue warps: 2 groups x 4 quarters x 2 halves
   static constexpr int NEG = NEPI / 2;
@@ -128,9 +132,8 @@ struct TcBarriers {
   uint64_t v_full[4], v_empty[4];
   uint64_t u_full[2], u_empty[2];
   uint64_t s_full[2], s_empty[2];
-  uint64_t ga_full[2], ga_empty[2];
-  uint64_t gs_empty[2];
-  uint64_t gt_full[2], gt_empty[2];
+  uint64_t g_full[2], gs_empty[2];  // G image staged / free (per epilogue group)
+  uint64_t gt_full[4], gt_empty[4];
   uint64_t gv_full[2], gv_empty[2];
   uint32_t tmem_base;
   double phi[16];
@@ -159,7 +162,8 @@ struct UnitWindow {
   int T, base;
   uint4 cur, nxt;
   __device__ __forceinline__ uint4 load(int i) const {
-    return i < T ? __ldg(u + i) : make_uint4(0, 0, 0, 0);
+    // branch-free (clamped) so the warp stays provably converged for the MMA issue
+    return __ldg(u + max(0, min(i, T - 1)));
   }
   __device__ __forceinline__ UnitWindow(const TcUnit* units, int t_count)
       : u(reinterpret_cast<const uint4*>(units)), T(t_count), base(0) {
@@ -195,6 +199,140 @@ static_assert(sizeof(TcUnit) == 16, "TcUnit is read as one uint4");
   } while (0)
 #endif
 
+// Residual MMA issuer (one lane of warp 1): its own function, so ptxas
+// allocates it apart from the epilogue and keeps the descriptors uniform.
+template <int KP16, bool MASK>
+__device__ __noinline__ void tc_residual_issuer(unsigned char* sm, TcBarriers* bar,
+                                                const TcUnit* units, int T, int run0,
+                                                uint32_t tm, const TcParams& p) {
+  using C = TcCfg<KP16, MASK>;
+  using namespace tc;
+  constexpr uint32_t ID_RES = idesc_f16(128, 64, false, false);
+  constexpr int KS = KP16 / 16;
+  const bool do_mma = !(p.debug & 8);
+  const uint32_t u0 = smem_u32(sm + C::OFF_U), v0 = smem_u32(sm + C::OFF_V);
+  TcUnit un_next = T > 0 ? units[0] : TcUnit{};
+  const uint64_t dU_k = umma_desc(u0, 16, 8 * C::RB, C::SWK);  // residual A (K-major)
+  const uint64_t dV_k = umma_desc(v0, 16, 8 * C::RB, C::SWK);  // residual B (K-major)
+  int prev_run = -1;
+  for (int t = 0; t < T; ++t) {
+    const TcUnit un = un_next;
+    if (t + 1 < T) un_next = units[t + 1];
+    const int run = un.gv_slot - run0;
+    const int ubuf = run % C::UB;
+    if (run != prev_run) {
+      mbar_wait(&bar->u_full[ubuf], (run / C::UB) & 1);
+      prev_run = run;
+    }
+    TC_TS(t, 12);
+    const int st = t % C::NSV, b = t & 1;
+    mbar_wait(&bar->v_full[st], (t / C::NSV) & 1);
+    TC_TS(t, 13);
+    mbar_wait(&bar->s_empty[b], ((t >> 1) & 1) ^ 1);
+    TC_TS(t, 1);
+    tc_fence_after();
+    const uint64_t da = dU_k + uint64_t(ubuf * (C::U_BYTES >> 4));
+    const uint64_t db = dV_k + uint64_t(st * (C::V_BYTES >> 4));
+    if (do_mma && !(p.debug & 64)) {
+      // uh.vh + uh.vm + um.vh: product q uses U split (q == 2), V split (q == 1)
+      const uint32_t dt = tm + C::T_S + b * 64;
+      static_for<3 * KS>([&](auto I) {
+        constexpr int q = I / KS, ks = I % KS;
+        constexpr int oa = ((q == 2 ? C::U_SPLIT : 0) + ks * 32) >> 4;
+        constexpr int ob = ((q == 1 ? C::V_SPLIT : 0) + ks * 32) >> 4;
+        mma_ss_1<oa, ob>(dt, da, db, ID_RES, I != 0);
+      });
+    }
+    mma_commit(&bar->s_full[b]);
+    mma_commit(&bar->v_empty[st]);
+    if (un.flags & TCU_LAST_OF_RUN) mma_commit(&bar->u_empty[ubuf]);
+    TC_TS(t, 24);
+  }
+}
+
+// Reduction MMA issuer (one lane of warp 3): G^T U first (it releases the
+// group's G staging image), then G.V.
+template <int KP16, bool MASK>
+__device__ __noinline__ void tc_reduction_issuer(unsigned char* sm, TcBarriers* bar,
+                                                 const TcUnit* units, int T, int run0,
+                                                 uint32_t tm, const TcParams& p) {
+  using C = TcCfg<KP16, MASK>;
+  using namespace tc;
+  constexpr uint32_t ID_GV = idesc_f16(128, C::GVC * KP16, false, true);
+  constexpr uint32_t ID_GT = idesc_f16(64, C::GCAT * KP16, true, true);
+  const bool do_mma = !(p.debug & 8);
+  const uint32_t u0 = smem_u32(sm + C::OFF_U), v0 = smem_u32(sm + C::OFF_V);
+  const uint32_t g0 = smem_u32(sm + C::OFF_G);
+  TcUnit un_next = T > 0 ? units[0] : TcUnit{};
+  // G^T U: A = G image read MN-major (M = 64 tile columns), B = [uh|um]
+  const uint64_t dUn0 = umma_desc(u0, C::GCAT == 2 ? C::U_SPLIT : 8192, 8 * C::RB, C::SWK);
+  const uint64_t dGm = umma_desc(g0, 16384, 1024, SW_128);
+  // G.V: the same G image read K-major (M = 128 tile rows, K = tile columns),
+  // B = [vh|vm] MN-major
+  const uint64_t dGk = umma_desc(g0, 16, 1024, SW_128);
+  const uint64_t dVn0 = umma_desc(v0, C::GVC == 2 ? C::V_SPLIT : 8192, 8 * C::RB, C::SWK);
+  for (int t = 0; t < T; ++t) {
+    const TcUnit un = un_next;
+    if (t + 1 < T) un_next = units[t + 1];
+    const int run = un.gv_slot - run0;
+    const int ubuf = run % C::UB, b = t & 1, st = t % C::NSV, gvb = run & 1, gtb = t & 3;
+    const bool first = (un.flags & TCU_FIRST_OF_RUN) != 0;
+    TC_TS(t, 14);
+    mbar_wait(&bar->g_full[b], (t >> 1) & 1);
+    TC_TS(t, 2);
+    mbar_wait(&bar->gt_empty[gtb], ((t >> 2) & 1) ^ 1);
+    if (first) mbar_wait(&bar->gv_empty[gvb], ((run >> 1) & 1) ^ 1);
+    TC_TS(t, 3);
+    tc_fence_after();
+    const uint64_t dUn = dUn0 + uint64_t(ubuf * (C::U_BYTES >> 4));
+    const uint64_t goff = uint64_t(b * (C::G_BYTES >> 4));
+    const uint32_t gt = tm + C::T_GT + gtb * C::GCAT * KP16;
+    if (do_mma && !(p.debug & 16)) {
+      static_for<8>([&](auto I) {
+        constexpr int ks = I;
+        constexpr int uo = (ks * 16 * C::RB) >> 4, go = (2048 * ks) >> 4;
+        constexpr int gl_o = go + (C::G_SPLIT >> 4);
+        if constexpr (C::GCAT == 2) {
+          // B = [uh | um]: two N-atoms of the U image (LBO = split stride)
+          mma_ss_1<go, uo>(gt, dGm + goff, dUn, ID_GT, ks > 0);
+          mma_ss_1<gl_o, uo>(gt, dGm + goff, dUn, ID_GT, 1);
+        } else {
+          mma_ss_1<go, uo>(gt, dGm + goff, dUn, ID_GT, ks > 0);
+          mma_ss_1<go, uo + (C::U_SPLIT >> 4)>(gt, dGm + goff, dUn, ID_GT, 1);
+          mma_ss_1<gl_o, uo>(gt, dGm + goff, dUn, ID_GT, 1);
+        }
+      });
+    }
+    mma_commit(&bar->gt_full[gtb]);
+    TC_TS(t, 25);
+    const uint64_t dVn = dVn0 + uint64_t(st * (C::V_BYTES >> 4));
+    const uint32_t gv = tm + C::T_GV + gvb * C::GVC * KP16;
+    if (do_mma && !(p.debug & 32)) {
+      static_for<4>([&](auto I) {
+        constexpr int ks = I;
+        constexpr int vo = (ks * 16 * C::RB) >> 4;
+        constexpr int ao = (32 * ks) >> 4, alo = ao + (C::G_SPLIT >> 4);
+        if constexpr (C::GVC == 2) {
+          // B = [vh | vm] (N-concatenated), A = gh then gl (K-step of 16 columns)
+          mma_ss_1<ao, vo>(gv, dGk + goff, dVn, ID_GV, !(first && ks == 0));
+          mma_ss_1<alo, vo>(gv, dGk + goff, dVn, ID_GV, 1);
+        } else {
+          mma_ss_1<ao, vo>(gv, dGk + goff, dVn, ID_GV, !(first && ks == 0));
+          mma_ss_1<ao, vo + (C::V_SPLIT >> 4)>(gv, dGk + goff, dVn, ID_GV, 1);
+          mma_ss_1<alo, vo>(gv, dGk + goff, dVn, ID_GV, 1);
+        }
+      });
+    }
+    mma_commit(&bar->gs_empty[b]);
+    mma_commit(&bar->v_empty[st]);
+    if (un.flags & TCU_LAST_OF_RUN) {
+      mma_commit(&bar->gv_full[gvb]);
+      mma_commit(&bar->u_empty[ubuf]);
+    }
+    TC_TS(t, 15);
+  }
+}
+
 template <int KP16, bool MASK>
 __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
     tc_eval_kernel(const __grid_constant__ CUtensorMap xmap,
@@ -225,13 +363,14 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
       mbar_init(&bar->u_empty[i], 2);  // residual + G^T U issuers
       mbar_init(&bar->s_full[i], 1);
       mbar_init(&bar->s_empty[i], C::NEG);
-      mbar_init(&bar->ga_full[i], C::NEG);
-      mbar_init(&bar->ga_empty[i], 1);
+      mbar_init(&bar->g_full[i], C::NEG);
       mbar_init(&bar->gs_empty[i], 1);
-      mbar_init(&bar->gt_full[i], 1);
-      mbar_init(&bar->gt_empty[i], C::NEG);
       mbar_init(&bar->gv_full[i], 1);
       mbar_init(&bar->gv_empty[i], C::NEG);
+    }
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&bar->gt_full[i], 1);
+      mbar_init(&bar->gt_empty[i], C::NEG);
     }
     fence_barrier_init();
   }
@@ -248,10 +387,28 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
 
   if (warp == 0) {
     // ======================= X / mask producer (TMA) ====================
-    UnitWindow uw(units, T);
+    // X tiles are also prefetched into L2 PF tiles ahead of their shared-
+    // memory load: the bytes in flight needed to cover HBM latency then live
+    // in L2 rather than in the (small) stage ring
+    constexpr int PF = SPCP_TC_XPF;
+    UnitWindow uw(units, T), uwp(units, T);
     const uint64_t pol_x = policy_evict_first();
+    for (int tp = 0; tp < PF; ++tp) {
+      const TcUnit up = uwp.get(tp);
+      if (lane == 0 && tp < T) {
+        tma_prefetch_2d(&xmap, int(up.tc) * 64, int(up.sb) * 128);
+        tma_prefetch_2d(&xmap, int(up.tc) * 64 + 32, int(up.sb) * 128);
+      }
+    }
     for (int t = 0; t < T; ++t) {
       const TcUnit un = uw.get(t);
+      if (PF > 0) {
+        const TcUnit up = uwp.get(t + PF);
+        if (lane == 0 && t + PF < T) {
+          tma_prefetch_2d(&xmap, int(up.tc) * 64, int(up.sb) * 128);
+          tma_prefetch_2d(&xmap, int(up.tc) * 64 + 32, int(up.sb) * 128);
+        }
+      }
       if (lane == 0) {
         const int st = t % C::NST;
         mbar_wait(&bar->stage_empty[st], ((t / C::NST) & 1) ^ 1);
@@ -276,161 +433,54 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
       __syncwarp();
     }
   } else if (warp == 2) {
-    // ======================= U / V operand-image producer ===============
-    // The images are small and L2-resident; the whole warp copies them with
-    // 128-bit loads/stores (LSU path), so they never queue behind the X
-    // tensor loads in the TMA engine.
-    auto copy_img = [&](unsigned char* dst, const unsigned char* src, int bytes) {
-      const uint4* s4 = reinterpret_cast<const uint4*>(src);
-      uint4* d4 = reinterpret_cast<uint4*>(dst);
-      constexpr int UNR = 4;
-      for (int i0 = 0; i0 < bytes / 16; i0 += 32 * UNR) {
-        uint4 r[UNR];
-#pragma unroll
-        for (int j = 0; j < UNR; ++j) {
-          const int i = i0 + j * 32 + lane;
-          if (i < bytes / 16) r[j] = __ldcg(s4 + i);
+    // ======================= U / V operand-image producer (bulk copies) ==
+    // Asynchronous TMA bulk copies of the L2-resident images: several stay in
+    // flight, so their latency is hidden by the V ring and the U buffers.
+    if (lane == 0) {
+      int prev_run = -1;
+      TcUnit un_next = T > 0 ? units[0] : TcUnit{};
+      for (int t = 0; t < T; ++t) {
+        const TcUnit un = un_next;
+        if (t + 1 < T) un_next = units[t + 1];
+        const int run = un.gv_slot - run0;
+        if (run != prev_run) {
+          const int b = run % C::UB;
+          mbar_wait(&bar->u_empty[b], ((run / C::UB) & 1) ^ 1);
+          mbar_arrive_expect_tx(&bar->u_full[b], C::U_BYTES);
+          bulk_load(sm + C::OFF_U + b * C::U_BYTES, p.u_img + size_t(un.sb) * C::U_BYTES,
+                    C::U_BYTES, &bar->u_full[b]);
+          prev_run = run;
         }
-#pragma unroll
-        for (int j = 0; j < UNR; ++j) {
-          const int i = i0 + j * 32 + lane;
-          if (i < bytes / 16) d4[i] = r[j];
-        }
+        const int sv = t % C::NSV;
+        mbar_wait(&bar->v_empty[sv], ((t / C::NSV) & 1) ^ 1);
+        TC_TS(t, 11);
+        mbar_arrive_expect_tx(&bar->v_full[sv], C::V_BYTES);
+        bulk_load(sm + C::OFF_V + sv * C::V_BYTES, p.v_img + size_t(un.tc) * C::V_BYTES,
+                  C::V_BYTES, &bar->v_full[sv]);
       }
-      fence_proxy_async_smem();  // generic-proxy writes -> visible to the MMA (async proxy)
-      __syncwarp();
-    };
-    int prev_run = -1;
-    UnitWindow uw(units, T);
-    for (int t = 0; t < T; ++t) {
-      const TcUnit un = uw.get(t);
-      const int run = un.gv_slot - run0;
-      if (run != prev_run) {
-        const int b = run % C::UB;
-        mbar_wait(&bar->u_empty[b], ((run / C::UB) & 1) ^ 1);
-        copy_img(sm + C::OFF_U + b * C::U_BYTES, p.u_img + size_t(un.sb) * C::U_BYTES, C::U_BYTES);
-        if (lane == 0) mbar_arrive(&bar->u_full[b]);
-        prev_run = run;
-      }
-      const int sv = t % C::NSV;
-      mbar_wait(&bar->v_empty[sv], ((t / C::NSV) & 1) ^ 1);
-      if (lane == 0) TC_TS(t, 11);
-      copy_img(sm + C::OFF_V + sv * C::V_BYTES, p.v_img + size_t(un.tc) * C::V_BYTES, C::V_BYTES);
-      if (lane == 0) mbar_arrive(&bar->v_full[sv]);
     }
   } else if (warp == 1 || warp == 3) {
     // ======================= MMA issuers ================================
-    // Three warps issue into the one tensor pipe: warp 1 the residual of
-    // every tile (runs ahead, bounded by the S / V / U buffers), warp 3 the
-    // G^T U batch and warp 4 the G.V batch of each tile once its G is staged.
-    // Base descriptors are built once; each MMA adds a compile-time offset
-    // (descriptor address field = byte address >> 4, no carry for smem).
-    constexpr uint32_t ID_RES = idesc_f16(128, 64, false, false);
-    constexpr uint32_t ID_GV = idesc_f16(128, C::GVC * KP16, false, true);
-    constexpr uint32_t ID_GT = idesc_f16(64, C::GCAT * KP16, true, true);
-    constexpr int KS = KP16 / 16;
-    const bool do_mma = !(p.debug & 8);
-    const uint32_t u0 = smem_u32(sm + C::OFF_U), v0 = smem_u32(sm + C::OFF_V);
-    const uint32_t g0 = smem_u32(sm + C::OFF_G);
-    UnitWindow uw(units, T);
-    if (warp == 1) {
-      const uint64_t dU_k = umma_desc(u0, 16, 8 * C::RB, C::SWK);  // residual A (K-major)
-      const uint64_t dV_k = umma_desc(v0, 16, 8 * C::RB, C::SWK);  // residual B (K-major)
-      int prev_run = -1;
-      for (int t = 0; t < T; ++t) {
-        const TcUnit un = uw.get(t);
-        const int run = un.gv_slot - run0;
-        const int ubuf = run % C::UB;
-        if (run != prev_run) {
-          mbar_wait(&bar->u_full[ubuf], (run / C::UB) & 1);
-          prev_run = run;
-        }
-        if (lane == 0) TC_TS(t, 12);
-        const int st = t % C::NSV, b = t & 1;
-        mbar_wait(&bar->v_full[st], (t / C::NSV) & 1);
-        if (lane == 0) TC_TS(t, 13);
-        mbar_wait(&bar->s_empty[b], ((t >> 1) & 1) ^ 1);
-        if (lane == 0) TC_TS(t, 1);
-        tc_fence_after();
-        const uint64_t da = dU_k + uint64_t(ubuf * (C::U_BYTES >> 4));
-        const uint64_t db = dV_k + uint64_t(st * (C::V_BYTES >> 4));
-        __syncwarp();  // converged: lets ptxas keep descriptors uniform (no per-MMA ELECT)
-        if (do_mma && !(p.debug & 64)) {
-          // uh.vh + uh.vm + um.vh, K-steps of 32 B
-          mma_residual_batch<KS, (C::U_SPLIT >> 4), (C::V_SPLIT >> 4), 2>(tm + C::T_S + b * 64,
-                                                                          da, db, ID_RES);
-        }
-        mma_commit_w(&bar->s_full[b]);
-        mma_commit_w(&bar->v_empty[st]);
-        if (un.flags & TCU_LAST_OF_RUN) mma_commit_w(&bar->u_empty[ubuf]);
-        if (lane == 0) TC_TS(t, 24);
-      }
-    } else {
-      // G^T U first (it releases the group's G staging image), then G.V
-      const uint64_t dUn0 = umma_desc(u0, C::GCAT == 2 ? C::U_SPLIT : 8192, 8 * C::RB, C::SWK);
-      const uint64_t dG = umma_desc(g0, 16384, 1024, SW_128);  // A = G image (MN-major)
-      const uint64_t dVn0 = umma_desc(v0, C::GVC == 2 ? C::V_SPLIT : 8192, 8 * C::RB, C::SWK);
-      for (int t = 0; t < T; ++t) {
-        const TcUnit un = uw.get(t);
-        const int run = un.gv_slot - run0;
-        const int ubuf = run % C::UB, b = t & 1, st = t % C::NSV, gvb = run & 1;
-        const bool first = (un.flags & TCU_FIRST_OF_RUN) != 0;
-        if (lane == 0) TC_TS(t, 14);
-        mbar_wait(&bar->ga_full[b], (t >> 1) & 1);
-        if (lane == 0) TC_TS(t, 2);
-        mbar_wait(&bar->gt_empty[b], ((t >> 1) & 1) ^ 1);
-        if (first) mbar_wait(&bar->gv_empty[gvb], ((run >> 1) & 1) ^ 1);
-        if (lane == 0) TC_TS(t, 3);
-        tc_fence_after();
-        const uint64_t dUn = dUn0 + uint64_t(ubuf * (C::U_BYTES >> 4));
-        const uint64_t dgh = dG + uint64_t(b * (C::G_BYTES >> 4));
-        const uint32_t gt = tm + C::T_GT + b * C::GCAT * KP16;
-        __syncwarp();  // converged: lets ptxas keep descriptors uniform (no per-MMA ELECT)
-        if (do_mma && !(p.debug & 16)) {
-          if constexpr (C::GCAT == 2) {
-            // B = [uh | um]: two N-atoms of the U image (LBO = split stride)
-            mma_gtu_batch2<(2048 >> 4), (C::G_SPLIT >> 4), ((16 * C::RB) >> 4)>(gt, dgh, dUn,
-                                                                                ID_GT);
-          } else {
-            static_for<8>([&](auto I) {
-              constexpr int ks = I;
-              constexpr int uo = (ks * 16 * C::RB) >> 4, go = (2048 * ks) >> 4;
-              constexpr int gl_o = go + (C::G_SPLIT >> 4);
-              mma_ss_o<go, uo>(gt, dgh, dUn, ID_GT, ks > 0);
-              mma_ss_o<go, uo + (C::U_SPLIT >> 4)>(gt, dgh, dUn, ID_GT, 1);
-              mma_ss_o<gl_o, uo>(gt, dgh, dUn, ID_GT, 1);
-            });
-          }
-        }
-        mma_commit_w(&bar->gt_full[b]);
-        mma_commit_w(&bar->gs_empty[b]);
-        if (lane == 0) TC_TS(t, 25);
-        const uint64_t dVn = dVn0 + uint64_t(st * (C::V_BYTES >> 4));
-        const uint32_t gv = tm + C::T_GV + gvb * C::GVC * KP16;
-        const uint32_t ga = tm + C::T_GA + b * 64;
-        __syncwarp();  // converged: lets ptxas keep descriptors uniform (no per-MMA ELECT)
-        if (do_mma && !(p.debug & 32)) {
-          if constexpr (C::GVC == 2) {
-            // B = [vh | vm] (N-concatenated), A = gh then gl per K-step
-            mma_gv_batch2<((16 * C::RB) >> 4)>(gv, ga, dVn, ID_GV, first ? 0u : 1u);
-          } else {
-            static_for<4>([&](auto I) {
-              constexpr int ks = I;
-              constexpr int vo = (ks * 16 * C::RB) >> 4;
-              mma_ts_o<vo>(gv, ga + 8 * ks, dVn, ID_GV, !(first && ks == 0));
-              mma_ts_o<vo + (C::V_SPLIT >> 4)>(gv, ga + 8 * ks, dVn, ID_GV, 1);
-              mma_ts_o<vo>(gv, ga + 32 + 8 * ks, dVn, ID_GV, 1);
-            });
-          }
-        }
-        mma_commit_w(&bar->ga_empty[b]);
-        mma_commit_w(&bar->v_empty[st]);
-        if (un.flags & TCU_LAST_OF_RUN) {
-          mma_commit_w(&bar->gv_full[gvb]);
-          mma_commit_w(&bar->u_empty[ubuf]);
-        }
-        if (lane == 0) TC_TS(t, 15);
-      }
+    // Two warps issue into the one tensor pipe, each on a single lane (no
+    // elect: ptxas keeps the descriptors on the uniform datapath, ~6
+    // instructions per MMA): warp 1 the residual of every tile (runs ahead,
+    // bounded only by the S / V / U buffers), warp 3 the reductions (G^T U,
+    // then G.V) of each tile once its G is staged.  Base descriptors are built
+    // once; every MMA adds a compile-time offset (descriptor address field =
+    // byte address >> 4, no carry for shared memory).
+    if (lane == 0) {
+      constexpr uint32_t ID_RES = idesc_f16(128, 64, false, false);
+      constexpr uint32_t ID_GV = idesc_f16(128, C::GVC * KP16, false, true);
+      constexpr uint32_t ID_GT = idesc_f16(64, C::GCAT * KP16, true, true);
+      constexpr int KS = KP16 / 16;
+      const bool do_mma = !(p.debug & 8);
+      const uint32_t u0 = smem_u32(sm + C::OFF_U), v0 = smem_u32(sm + C::OFF_V);
+      const uint32_t g0 = smem_u32(sm + C::OFF_G);
+      TcUnit un_next = T > 0 ? units[0] : TcUnit{};
+      if (warp == 1)
+        tc_residual_issuer<KP16, MASK>(sm, bar, units, T, run0, tm, p);
+      else
+        tc_reduction_issuer<KP16, MASK>(sm, bar, units, T, run0, tm, p);
     }
   } else {
     // ======================= epilogue warps =============================
@@ -451,8 +501,8 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
 
     // G^T U of tile t2 (this group's previous tile) -> CTA-private slot
     auto drain_gt = [&](int t2, const TcUnit& u2) {
-      const int b = t2 & 1;
-      mbar_wait(&bar->gt_full[b], (t2 >> 1) & 1);
+      const int b = t2 & 3;
+      mbar_wait(&bar->gt_full[b], (t2 >> 2) & 1);
       tc_fence_after();
       if (!(p.debug & 1)) {
         float* dst = p.pright + (size_t(u2.gt_slot) * 64 + 16 * q + lane) * KP16 + h * GTC;
@@ -601,22 +651,13 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
       }
       phi_acc += double(hs2.x) + double(hs2.y);
       if (ts_w) TC_TS(t, 7);
-      // ---- deferred drains of this group's previous tile
-      if (t >= 2) {
-        drain_gt(t - 2, prev);
-        if (prev.flags & TCU_LAST_OF_RUN) drain_gv(prev);
-      }
       if (ts_w) TC_TS(t, 8);
-      // ---- G to TMEM (A of G.V) and to smem (A of G^T.U)
-      mbar_wait(&bar->ga_empty[b], ((t >> 1) & 1) ^ 1);
-#if !defined(SPCP_TC_BISECT_EPI_SKIP)
-      tmem_st16(tm + lane_addr + C::T_GA + b * 64 + 16 * h, hi);
-      tmem_st16(tm + lane_addr + C::T_GA + b * 64 + 32 + 16 * h, lo);
-#else
-      if (hi[0] == 0x12345 && lo[3] == 0x777) phi_acc += 1.0;  // keep the math alive
-#endif
+      // ---- G to smem: A of both G^T.U (MN-major view) and G.V (K-major view)
       mbar_wait(&bar->gs_empty[b], ((t >> 1) & 1) ^ 1);
       if (ts_w) TC_TS(t, 9);
+#if defined(SPCP_TC_BISECT_EPI_SKIP)
+      if (hi[0] == 0x12345 && lo[3] == 0x777) phi_acc += 1.0;  // keep the math alive
+#endif
 #if !defined(SPCP_TC_BISECT_EPI_SKIP) && !defined(SPCP_TC_BISECT_NO_SMEM)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -627,13 +668,17 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
             make_uint4(lo[4 * c], lo[4 * c + 1], lo[4 * c + 2], lo[4 * c + 3]);
       }
 #endif
-      tmem_wait_st();
       fence_proxy_async_smem();
-      tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bar->ga_full[b]);
+      if (lane == 0) mbar_arrive(&bar->g_full[b]);
       if (ts_w) TC_TS(t, 10);
       if (lane == 0) TC_TS(t, 16 + (e & 3) + 4 * h);  // per-warp arrival: quarter + 4 * half
+      // ---- deferred drains of this group's previous tile (off the G hand-off
+      // path: G^T U accumulators are double-buffered per group)
+      if (t >= 2) {
+        drain_gt(t - 2, prev);
+        if (prev.flags & TCU_LAST_OF_RUN) drain_gv(prev);
+      }
       prev = un;
     }
     // flush: this group's last tile

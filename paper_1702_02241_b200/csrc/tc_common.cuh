@@ -114,6 +114,13 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
+// L2-only prefetch of a 2-D tensor tile (no shared memory, no completion)
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
 // Same with an L2 cache policy (createpolicy) — X is streamed once: evict first.
 __device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, int c0, int c1,
                                                  uint64_t* bar, uint64_t policy) {
@@ -365,6 +372,29 @@ __device__ __forceinline__ void mma_ts_o(uint32_t d_tmem, uint32_t a_tmem, uint6
       "r"(a_tmem), "l"(b_base), "r"(idesc), "r"(accumulate), "n"(OB)
       : "memory");
 }
+// Single-thread variants (the issuing loop runs on one lane): no elect, and
+// ptxas keeps base descriptors + immediate offsets on the uniform datapath.
+template <int OA, int OB>
+__device__ __forceinline__ void mma_ss_1(uint32_t d_tmem, uint64_t a_base, uint64_t b_base,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\n.reg .b64 ad, bd;\nsetp.ne.b32 p, %4, 0;\n"
+      "add.s64 ad, %1, %5;\nadd.s64 bd, %2, %6;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], ad, bd, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a_base), "l"(b_base), "r"(idesc), "r"(accumulate), "n"(OA), "n"(OB)
+      : "memory");
+}
+template <int OB>
+__device__ __forceinline__ void mma_ts_1(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_base,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\n.reg .b64 bd;\nsetp.ne.b32 p, %4, 0;\n"
+      "add.s64 bd, %2, %5;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], bd, %3, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_base), "r"(idesc), "r"(accumulate), "n"(OB)
+      : "memory");
+}
+
 // ---- whole MMA batches in one asm block: one elect.sync per batch, the
 // descriptors stepped by immediate strides inside the block.
 

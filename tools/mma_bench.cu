@@ -267,6 +267,16 @@ __global__ void __launch_bounds__(512) bench_bg(int mode, int iters, long long* 
           bulk_load(sm + 131072 + (n & 1) * 32768, g_src + ((n * 32768) % (512u << 20)), 32768, &cb);
           mbar_wait(&cb, n & 1);
         }
+        if (mode == 12 && (threadIdx.x & 31) == 0 && warp <= 4) {  // TMA bulk writes, 2 in flight/warp
+          __shared__ uint64_t cb2[8];
+          const int w = warp - 1;
+          if (n == 0) { mbar_init(&cb2[2 * w], 1); mbar_init(&cb2[2 * w + 1], 1); fence_barrier_init(); }
+          const int slot = n & 1;
+          if (n >= 2) mbar_wait(&cb2[2 * w + slot], ((n >> 1) - 1) & 1);
+          mbar_arrive_expect_tx(&cb2[2 * w + slot], 8192);
+          bulk_load(sm + 131072 + (w * 2 + slot) * 8192, g_src + ((n * 8192 + w * 65536) % (2u << 20)), 8192,
+                    &cb2[2 * w + slot]);
+        }
         if (mode == 7) {
           float f0 = __uint_as_float(acc.x), f1 = f0 + 1.f, f2 = f0 + 2.f, f3 = f0 + 3.f;
 #pragma unroll
@@ -310,9 +320,9 @@ int main() {
   for (int v : vars) printf("%-28s %6lld cycles per group (incl. commit+wait)\n", names[v], h[v]);
   { unsigned char* src; cudaMalloc(&src, 512u << 20); cudaMemset(src, 0, 512u << 20); cudaMemcpyToSymbol(g_src, &src, sizeof(src)); }
   cudaFuncSetAttribute(bench_bg, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  const char* bgn[] = {"none", "LDS.128", "STS.128", "LDS+STS", "tcgen05.ld x16", "tcgen05.st x16", "TMEM ld+st", "FFMA issue", "STS+proxy fence", "tcgen05 fences", "mbar polling", "bulk copy HBM"};
+  const char* bgn[] = {"none", "LDS.128", "STS.128", "LDS+STS", "tcgen05.ld x16", "tcgen05.st x16", "TMEM ld+st", "FFMA issue", "STS+proxy fence", "tcgen05 fences", "mbar polling", "bulk copy HBM", "TMA bulk L2 x8"};
   for (int nw : {4, 8, 16})
-    for (int mode = 0; mode < 12; ++mode) {
+    for (int mode = 0; mode < 13; ++mode) {
       bench_bg<<<1, 32 * (1 + nw), 200 * 1024>>>(mode, 500, d);
       cudaError_t e = cudaDeviceSynchronize();
       if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
