@@ -409,6 +409,7 @@ static int tc_build(spcp_problem* p) {
   if ((rc = p->tc_begin.ensure(begin.size() * sizeof(int32_t)))) return rc;
   if ((rc = p->tc_csr.ensure(csr.size() * sizeof(int32_t)))) return rc;
   if ((rc = p->tc_scales.ensure(sizeof(TcScales)))) return rc;
+  SPCP_CUDA(cudaMemset(p->tc_scales.ptr, 0, sizeof(TcScales)));
   SPCP_CUDA(cudaMemcpy(p->tc_units.ptr, units.data(), units.size() * sizeof(TcUnit),
                        cudaMemcpyHostToDevice));
   SPCP_CUDA(cudaMemcpy(p->tc_begin.ptr, begin.data(), begin.size() * sizeof(int32_t),
@@ -442,7 +443,7 @@ static int tc_launch(spcp_problem* p, int64_t k) {
   tp.pleft = p->pleft.as<float>();
   tp.pright = p->pright.as<float>();
   tp.pphi = p->pphi.as<double>();
-  tp.kstore = int(k);
+  tp.kstore = int(round_up(k, 4));
   {
     const char* e = getenv("SPCP_TC_DEBUG");
     tp.debug = e ? atoi(e) : 0;
@@ -484,7 +485,7 @@ static int tc_images(spcp_problem* p, int64_t k, const double* z, const double* 
   const int64_t total = (p->m_pad + p->n_pad) * KP16;
   tc_images_kernel<KP16><<<grid_for(total), 256, 0, p->stream>>>(
       z, dz, alpha, p->m, p->n, k, p->m_pad, p->n_pad, p->tc_scales.as<TcScales>(),
-      p->tc_uimg.as<unsigned char>(), p->tc_vimg.as<unsigned char>());
+      p->lambda_s, p->tc_uimg.as<unsigned char>(), p->tc_vimg.as<unsigned char>());
   SPCP_CHECK_LAUNCH("tc_images");
   p->launches++;
   return SPCP_OK;
@@ -496,20 +497,19 @@ static int tc_eval(spcp_problem* p, int64_t k, const double* z, const double* dz
   if ((rc = tc_build(p))) return rc;
   const int kp16 = k <= 16 ? 16 : (k <= 32 ? 32 : 64);
   // operand scales (max |U|, |V| of the trial point -> powers of two)
+  // the maxima are zero here: zeroed at build time and reset by every fused launch
   TcScales* sc = p->tc_scales.as<TcScales>();
-  SPCP_CUDA(cudaMemsetAsync(&sc->max_bits[0], 0, 2 * sizeof(unsigned long long), p->stream));
   const int64_t nu = p->m * k, nv = p->n * k;
   tc_max_kernel<<<grid_for(nu + nv, 256, 148 * 4), 256, 0, p->stream>>>(z, dz, alpha, nu, nv, sc);
   SPCP_CHECK_LAUNCH("tc_max");
-  tc_scales_kernel<<<1, 1, 0, p->stream>>>(sc, p->lambda_s);
-  SPCP_CHECK_LAUNCH("tc_scales");
-  p->launches += 2;
+  p->launches += 1;
   rc = kp16 == 16 ? tc_images<16>(p, k, z, dz, alpha)
                   : (kp16 == 32 ? tc_images<32>(p, k, z, dz, alpha)
                                 : tc_images<64>(p, k, z, dz, alpha));
   if (rc) return rc;
-  if ((rc = p->pleft.ensure(size_t(p->tc_runs) * 128 * kp16 * sizeof(float)))) return rc;
-  if ((rc = p->pright.ensure(size_t(p->tc_slots) * 64 * kp16 * sizeof(float)))) return rc;
+  const int kst = int(round_up(k, 4));  // partials store the real rank only
+  if ((rc = p->pleft.ensure(size_t(p->tc_runs) * 128 * kst * sizeof(float)))) return rc;
+  if ((rc = p->pright.ensure(size_t(p->tc_slots) * 64 * kst * sizeof(float)))) return rc;
   if ((rc = p->pphi.ensure(size_t(p->tc_grid) * sizeof(double)))) return rc;
   if (p->masked)
     rc = kp16 == 16 ? tc_launch<16, true>(p, k)
@@ -519,7 +519,7 @@ static int tc_eval(spcp_problem* p, int64_t k, const double* z, const double* dz
                     : (kp16 == 32 ? tc_launch<32, false>(p, k) : tc_launch<64, false>(p, k));
   if (rc) return rc;
   sh.tc = 1;
-  sh.kst = kp16;
+  sh.kst = int(round_up(k, 4));
   sh.nchunks = 1;
   sh.nrb = 1;
   sh.chunk_cols = p->tc_grid;  // phi partial count

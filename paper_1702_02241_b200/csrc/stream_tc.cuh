@@ -76,7 +76,7 @@ struct TcParams {
   float* pleft;   // [gv_slots][128][kstore]
   float* pright;  // [gt_slots][64][kstore]
   double* pphi;   // [grid]
-  int kstore;
+  int kstore;  // partial row stride (floats): k rounded up to 4
   int debug;  // bisection switches (SPCP_TC_DEBUG): 1 skip GT stores, 2 skip GV stores,
               // 8 skip all MMAs (pipeline skeleton only), 16 / 32 / 64 skip the
               // G^T U / G.V / residual MMAs
@@ -90,7 +90,12 @@ struct TcCfg {
   static constexpr int NSPLIT = 2;
   // X ring (released by the epilogue as soon as it has read the tile), V ring
   // (released when the tile's G.V MMA has finished), U buffers (per run)
-  static constexpr int NST = KP16 == 16 ? (MASK ? 3 : 4) : (KP16 == 32 ? 3 : (MASK ? 2 : 3));
+#ifndef SPCP_TC_GB
+#define SPCP_TC_GB 2
+#endif
+  static constexpr int GB = SPCP_TC_GB;  // G staging images (1: shared by both groups)
+  static constexpr int NST = GB == 1 ? ((KP16 == 64 && MASK) ? 3 : 4)
+                                     : (KP16 == 16 ? (MASK ? 3 : 4) : (KP16 == 32 ? 3 : (MASK ? 2 : 3)));
   static constexpr int NSV = KP16 == 64 ? 2 : (MASK ? 3 : 4);
   static constexpr int UB = KP16 == 64 ? 1 : 2;
   static constexpr int LOOKAHEAD = NSV - 1 < 2 ? NSV - 1 : 2;  // residual issue lead (tiles)
@@ -107,7 +112,7 @@ struct TcCfg {
   static constexpr int OFF_V = OFF_X + NST * X_BYTES;
   static constexpr int OFF_U = OFF_V + NSV * V_BYTES;
   static constexpr int OFF_G = OFF_U + UB * U_BYTES;
-  static constexpr int OFF_M = OFF_G + 2 * G_BYTES;
+  static constexpr int OFF_M = OFF_G + GB * G_BYTES;
   static constexpr int OFF_BAR = OFF_M + (MASK ? NST * 2048 : 0);
   static constexpr int SMEM = OFF_BAR + 512;  // dynamic smem base is 1 KB aligned
   static_assert(SMEM <= 232448, "shared memory budget");
@@ -132,7 +137,7 @@ struct TcBarriers {
   uint64_t v_full[4], v_empty[4];
   uint64_t u_full[2], u_empty[2];
   uint64_t s_full[2], s_empty[2];
-  uint64_t g_full[2], gs_empty[2];  // G image staged / free (per epilogue group)
+  uint64_t g_full[2], gs_empty[2];  // G image staged (per group) / free (per image)
   uint64_t gt_full[4], gt_empty[4];
   uint64_t gv_full[2], gv_empty[2];
   uint32_t tmem_base;
@@ -285,7 +290,7 @@ __device__ __noinline__ void tc_reduction_issuer(unsigned char* sm, TcBarriers* 
     TC_TS(t, 3);
     tc_fence_after();
     const uint64_t dUn = dUn0 + uint64_t(ubuf * (C::U_BYTES >> 4));
-    const uint64_t goff = uint64_t(b * (C::G_BYTES >> 4));
+    const uint64_t goff = uint64_t((C::GB == 1 ? 0 : b) * (C::G_BYTES >> 4));
     const uint32_t gt = tm + C::T_GT + gtb * C::GCAT * KP16;
     if (do_mma && !(p.debug & 16)) {
       static_for<8>([&](auto I) {
@@ -323,7 +328,7 @@ __device__ __noinline__ void tc_reduction_issuer(unsigned char* sm, TcBarriers* 
         }
       });
     }
-    mma_commit(&bar->gs_empty[b]);
+    mma_commit(&bar->gs_empty[b]);  // per tile parity (see the epilogue's wait)
     mma_commit(&bar->v_empty[st]);
     if (un.flags & TCU_LAST_OF_RUN) {
       mma_commit(&bar->gv_full[gvb]);
@@ -348,6 +353,13 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
   const int T = ue - ub;
   const TcUnit* units = p.units + ub;
   const int run0 = T > 0 ? units[0].gv_slot : 0;  // CTA-local run index = gv_slot - run0
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    // the image pass (the only reader of the maxima) has completed: reset them
+    // for the next evaluation's max pass instead of a separate memset
+    TcScales* scw = const_cast<TcScales*>(p.scales);
+    scw->max_bits[0] = 0ull;
+    scw->max_bits[1] = 0ull;
+  }
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::NST; ++i) {
@@ -497,7 +509,8 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
     const float2 qc2 = make_float2(201326592.f, 201326592.f);  // 1.5 * 2^27: quantum 16
     double phi_acc = 0.0;
     constexpr int GTC = KP16 / 2;  // accumulator columns drained per warp (of KP16)
-    unsigned char* gimg = sm + C::OFF_G + grp * C::G_BYTES;
+    const int kst = p.kstore;      // partial row stride: k rounded up to 4 (<= KP16)
+    unsigned char* gimg = sm + C::OFF_G + (C::GB == 1 ? 0 : grp) * C::G_BYTES;
 
     // G^T U of tile t2 (this group's previous tile) -> CTA-private slot
     auto drain_gt = [&](int t2, const TcUnit& u2) {
@@ -505,7 +518,7 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
       mbar_wait(&bar->gt_full[b], (t2 >> 2) & 1);
       tc_fence_after();
       if (!(p.debug & 1)) {
-        float* dst = p.pright + (size_t(u2.gt_slot) * 64 + 16 * q + lane) * KP16 + h * GTC;
+        float* dst = p.pright + (size_t(u2.gt_slot) * 64 + 16 * q + lane) * kst + h * GTC;
         const bool first = (u2.flags & TCU_FIRST_TOUCH) != 0;
         constexpr int CH = GTC < 16 ? GTC : 16;
 #pragma unroll
@@ -525,6 +538,7 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
           if (lane < 16) {  // M = 64 accumulator: row j = 16 q + lane in lanes 0..15
 #pragma unroll
             for (int c = 0; c < CH; c += 4) {
+              if (h * GTC + c0 + c >= kst) continue;  // padded rank columns are not stored
               if (first)
                 *reinterpret_cast<uint4*>(dst + c0 + c) =
                     make_uint4(v[c], v[c + 1], v[c + 2], v[c + 3]);
@@ -546,7 +560,7 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
       mbar_wait(&bar->gv_full[gvb], (run >> 1) & 1);
       tc_fence_after();
       if (!(p.debug & 2)) {
-        float* dst = p.pleft + (size_t(u2.gv_slot) * 128 + row) * KP16 + h * GTC;
+        float* dst = p.pleft + (size_t(u2.gv_slot) * 128 + row) * kst + h * GTC;
         constexpr int CH = GTC < 16 ? GTC : 16;
 #pragma unroll
         for (int c0 = 0; c0 < GTC; c0 += CH) {
@@ -564,7 +578,8 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
           }
 #pragma unroll
           for (int c = 0; c < CH; c += 4)
-            *reinterpret_cast<uint4*>(dst + c0 + c) = make_uint4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+            if (h * GTC + c0 + c < kst)
+              *reinterpret_cast<uint4*>(dst + c0 + c) = make_uint4(v[c], v[c + 1], v[c + 2], v[c + 3]);
         }
       }
       tc_fence_before();
@@ -653,7 +668,14 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
       if (ts_w) TC_TS(t, 7);
       if (ts_w) TC_TS(t, 8);
       // ---- G to smem: A of both G^T.U (MN-major view) and G.V (K-major view)
-      mbar_wait(&bar->gs_empty[b], ((t >> 1) & 1) ^ 1);
+      if (C::GB == 1) {
+        // one image shared by both groups: wait for tile t-1's reductions
+        // (the other parity's barrier, phase (t-1)/2; in-order MMA completion
+        // covers tile t-2).  Per-parity barriers never lag two phases behind.
+        if (t >= 1) mbar_wait(&bar->gs_empty[(t - 1) & 1], ((t - 1) >> 1) & 1);
+      } else {
+        mbar_wait(&bar->gs_empty[b], ((t >> 1) & 1) ^ 1);
+      }
       if (ts_w) TC_TS(t, 9);
 #if defined(SPCP_TC_BISECT_EPI_SKIP)
       if (hi[0] == 0x12345 && lo[3] == 0x777) phi_acc += 1.0;  // keep the math alive
@@ -733,8 +755,8 @@ __global__ void tc_max_kernel(const double* __restrict__ z, const double* __rest
   }
 }
 
-// pass 2: power-of-two scales (one thread)
-__global__ void tc_scales_kernel(TcScales* sc, double tau) {
+// pass 2 (folded into the image pass): power-of-two scales from the maxima
+__device__ __forceinline__ TcScales tc_compute_scales(const TcScales* sc, double tau) {
   const double mu = __longlong_as_double(sc->max_bits[0]);
   const double mv = __longlong_as_double(sc->max_bits[1]);
   auto pow2_for = [](double mx) {  // largest 2^e with mx * 2^e <= 2^14
@@ -743,20 +765,22 @@ __global__ void tc_scales_kernel(TcScales* sc, double tau) {
     frexp(mx, &e);  // mx = f * 2^e, f in [0.5, 1)
     return ldexp(1.0, 14 - e);
   };
+  TcScales r{};
   const double su = pow2_for(mu), sv = pow2_for(mv);
   const double sigma = su * sv;
   const double taus = sigma * tau;
   int e;
   frexp(taus, &e);
   const double kappa = ldexp(1.0, 14 - e);
-  sc->su = su;
-  sc->sv = sv;
-  sc->sigma = float(sigma);
-  sc->tau_s = float(taus);
-  sc->kappa = float(kappa);
-  sc->gv_unscale = float(-1.0 / (kappa * sigma * sv));  // G.V partials carry gp = -G''
-  sc->gt_unscale = float(1.0 / (kappa * sigma * su));
-  sc->phi_unscale = 1.0 / (sigma * sigma);
+  r.su = su;
+  r.sv = sv;
+  r.sigma = float(sigma);
+  r.tau_s = float(taus);
+  r.kappa = float(kappa);
+  r.gv_unscale = float(-1.0 / (kappa * sigma * sv));  // G.V partials carry gp = -G''
+  r.gt_unscale = float(1.0 / (kappa * sigma * su));
+  r.phi_unscale = 1.0 / (sigma * sigma);
+  return r;
 }
 
 template <int RB>
@@ -773,10 +797,21 @@ __device__ __forceinline__ void split2_store(unsigned char* base, int split_byte
 template <int KP16>
 __global__ void tc_images_kernel(const double* __restrict__ z, const double* __restrict__ dz,
                                  double alpha, int64_t m, int64_t n, int64_t k, int64_t m_pad,
-                                 int64_t n_pad, const TcScales* sc, unsigned char* u_img,
+                                 int64_t n_pad, TcScales* sc, double tau, unsigned char* u_img,
                                  unsigned char* v_img) {
   constexpr int RB = KP16 * 2;
-  const double su = sc->su, sv = sc->sv;
+  const TcScales scl = tc_compute_scales(sc, tau);  // every block: same maxima, same scales
+  const double su = scl.su, sv = scl.sv;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // publish for the fused kernel and the reduce
+    sc->su = scl.su;
+    sc->sv = scl.sv;
+    sc->sigma = scl.sigma;
+    sc->tau_s = scl.tau_s;
+    sc->kappa = scl.kappa;
+    sc->gv_unscale = scl.gv_unscale;
+    sc->gt_unscale = scl.gt_unscale;
+    sc->phi_unscale = scl.phi_unscale;
+  }
   const int64_t total = (m_pad + n_pad) * KP16;
   for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < total;
        q += int64_t(gridDim.x) * blockDim.x) {
