@@ -137,12 +137,13 @@ struct ReduceParams {
   double* scal_out;        // U_PARTIAL: shard scalars out
   double* out;             // [8] totals (U_FULL / U_FROM_SUM)
   // tensor-core partial layout (csr_u_off != nullptr): pleft[slot][128][kst],
-  // pright[slot][64][kst], sources per 128-row sub-band / 64-column tile
+  // pright[slot][gt_rows][kst], sources per 128-row sub-band / 64-column tile
   const int32_t* csr_u_off;
   const int32_t* csr_u_idx;
   const int32_t* csr_v_off;
   const int32_t* csr_v_idx;
   int kst;                  // partial row stride (the kernel's padded rank)
+  int gt_rows;              // G^T.U slot rows: 64, or 128 = [gh part; gl part] (summed here)
   const float* tc_unscale;  // [0]: G.V partials, [1]: G^T.U partials
 };
 
@@ -196,8 +197,11 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p) {
       if (p.csr_v_off) {
         const int tcol = int(j >> 6);
         const float* prf = reinterpret_cast<const float*>(p.pright);
-        for (int e = p.csr_v_off[tcol]; e < p.csr_v_off[tcol + 1]; ++e)
-          acc += double(prf[(int64_t(p.csr_v_idx[e]) * 64 + (j & 63)) * p.kst + c]);
+        for (int e = p.csr_v_off[tcol]; e < p.csr_v_off[tcol + 1]; ++e) {
+          const float* sl = prf + int64_t(p.csr_v_idx[e]) * p.gt_rows * p.kst;
+          acc += double(sl[(j & 63) * p.kst + c]);
+          if (p.gt_rows == 128) acc += double(sl[(64 + (j & 63)) * p.kst + c]);
+        }
         acc *= double(p.tc_unscale[1]);
       } else {
         for (int b = 0; b < p.nrb; ++b) acc += double(pr[(int64_t(b) * p.n_pad + j) * p.kp + c]);

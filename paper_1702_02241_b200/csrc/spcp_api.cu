@@ -121,6 +121,7 @@ struct LaunchShape {
   int64_t chunk_cols = 0;
   int tc = 0;  // partials in the tensor-core (CSR slot) layout
   int kst = 0;
+  int gt_rows = 64;
 };
 
 template <typename T, typename TX, int KR, int PW, int MODE, bool MASK>
@@ -349,7 +350,11 @@ static int tc_build(spcp_problem* p) {
   const double per = double(U) / G;
   int side = std::max(1, int(std::lround(std::sqrt(per))));
   const int sbr = int(std::min<int64_t>(side, nsb));
-  const int sbc = int(std::min<int64_t>(std::max<int64_t>(1, std::lround(per / sbr)), ntc));
+  // an even super-block width keeps every column tile on one tile parity (one
+  // epilogue group) within a CTA, so G^T U slots need no per-parity split
+  int64_t sbc0 = std::max<int64_t>(2, std::lround(per / sbr));
+  sbc0 += sbc0 & 1;
+  const int sbc = int(std::min<int64_t>(sbc0, ntc));
   std::vector<TcUnit> units;
   units.reserve(U);
   for (int64_t r0 = 0; r0 < nsb; r0 += sbr)
@@ -369,7 +374,10 @@ static int tc_build(spcp_problem* p) {
     // G^T U slot per (column tile, tile parity): the two epilogue groups take
     // alternate tiles, so every slot is written by one thread per address
     // (program order => deterministic store-then-reduce)
-    std::map<int, int> slot_of;  // 2 * tc + parity -> global slot, this CTA
+    std::map<int, int> slot_of;  // 2 * tc (+ parity if the tile parity varies) -> slot
+    std::map<int, int> par_of;   // tc -> parity mask seen in this CTA
+    for (int i = begin[c]; i < begin[c + 1]; ++i)
+      par_of[units[i].tc] |= 1 << ((i - begin[c]) & 1);
     for (int i = begin[c]; i < begin[c + 1]; ++i) {
       TcUnit& u = units[i];
       const bool first = (i == begin[c]) || units[i - 1].sb != u.sb;
@@ -380,7 +388,7 @@ static int tc_build(spcp_problem* p) {
       }
       u.gv_slot = runs - 1;
       u.flags = (first ? TCU_FIRST_OF_RUN : 0u) | (last ? TCU_LAST_OF_RUN : 0u);
-      const int key = 2 * int(u.tc) + ((i - begin[c]) & 1);
+      const int key = 2 * int(u.tc) + (par_of[u.tc] == 3 ? ((i - begin[c]) & 1) : 0);
       auto it = slot_of.find(key);
       if (it == slot_of.end()) {
         slot_of[key] = slots;
@@ -425,10 +433,10 @@ static int tc_build(spcp_problem* p) {
   return SPCP_OK;
 }
 
-template <int KP16, bool MASK>
+template <int KP16, bool MASK, int SEG = 0>
 static int tc_launch(spcp_problem* p, int64_t k) {
-  using C = TcCfg<KP16, MASK>;
-  auto kern = tc_eval_kernel<KP16, MASK>;
+  using C = TcCfg<KP16, MASK, SEG>;
+  auto kern = tc_eval_kernel<KP16, MASK, SEG>;
   static bool attr = false;
   if (!attr) {
     SPCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -491,10 +499,71 @@ static int tc_images(spcp_problem* p, int64_t k, const double* z, const double* 
   return SPCP_OK;
 }
 
+template <int SEG>
+static int tc_images_kc(spcp_problem* p, int64_t k, const double* z, const double* dz,
+                        double alpha) {
+  constexpr int RB = TcCfg<16, false, SEG>::RB;
+  int rc;
+  if ((rc = p->tc_uimg.ensure(size_t(p->tc_nsb) * 128 * RB))) return rc;
+  if ((rc = p->tc_vimg.ensure(size_t(p->tc_ntc) * 64 * RB))) return rc;
+  const int64_t total = (p->m_pad + p->n_pad) * (RB / 2);
+  tc_images_kc_kernel<SEG><<<grid_for(total), 256, 0, p->stream>>>(
+      z, dz, alpha, p->m, p->n, k, p->m_pad, p->n_pad, p->tc_scales.as<TcScales>(),
+      p->lambda_s, p->tc_uimg.as<unsigned char>(), p->tc_vimg.as<unsigned char>());
+  SPCP_CHECK_LAUNCH("tc_images_kc");
+  p->launches++;
+  return SPCP_OK;
+}
+
+// K-concatenated layout (k <= 20): SEG = round_up(k, 4)
+static bool tc_use_kc(int64_t k) {
+  const char* e = getenv("SPCP_TC_LAYOUT");
+  return k <= 20 && !(e && std::string(e) == "split");
+}
+
+template <bool MASK>
+static int tc_launch_kc(spcp_problem* p, int64_t k) {
+  switch (int(round_up(k, 4))) {
+    case 4: return tc_launch<16, MASK, 4>(p, k);
+    case 8: return tc_launch<16, MASK, 8>(p, k);
+    case 12: return tc_launch<16, MASK, 12>(p, k);
+    case 16: return tc_launch<16, MASK, 16>(p, k);
+    default: return tc_launch<16, MASK, 20>(p, k);
+  }
+}
+
 static int tc_eval(spcp_problem* p, int64_t k, const double* z, const double* dz, double alpha,
                    LaunchShape& sh) {
   int rc;
   if ((rc = tc_build(p))) return rc;
+  if (tc_use_kc(k)) {
+    TcScales* sc = p->tc_scales.as<TcScales>();
+    const int64_t nu = p->m * k, nv = p->n * k;
+    tc_max_kernel<<<grid_for(nu + nv, 256, 148 * 4), 256, 0, p->stream>>>(z, dz, alpha, nu, nv, sc);
+    SPCP_CHECK_LAUNCH("tc_max");
+    p->launches += 1;
+    switch (int(round_up(k, 4))) {
+      case 4: rc = tc_images_kc<4>(p, k, z, dz, alpha); break;
+      case 8: rc = tc_images_kc<8>(p, k, z, dz, alpha); break;
+      case 12: rc = tc_images_kc<12>(p, k, z, dz, alpha); break;
+      case 16: rc = tc_images_kc<16>(p, k, z, dz, alpha); break;
+      default: rc = tc_images_kc<20>(p, k, z, dz, alpha); break;
+    }
+    if (rc) return rc;
+    const int kst = int(round_up(k, 4));
+    if ((rc = p->pleft.ensure(size_t(p->tc_runs) * 128 * kst * sizeof(float)))) return rc;
+    if ((rc = p->pright.ensure(size_t(p->tc_slots) * 128 * kst * sizeof(float)))) return rc;
+    if ((rc = p->pphi.ensure(size_t(p->tc_grid) * sizeof(double)))) return rc;
+    rc = p->masked ? tc_launch_kc<true>(p, k) : tc_launch_kc<false>(p, k);
+    if (rc) return rc;
+    sh.tc = 1;
+    sh.kst = kst;
+    sh.gt_rows = 128;
+    sh.nchunks = 1;
+    sh.nrb = 1;
+    sh.chunk_cols = p->tc_grid;
+    return SPCP_OK;
+  }
   const int kp16 = k <= 16 ? 16 : (k <= 32 ? 32 : 64);
   // operand scales (max |U|, |V| of the trial point -> powers of two)
   // the maxima are zero here: zeroed at build time and reset by every fused launch
@@ -742,6 +811,7 @@ static int run_reduce(spcp_problem* p, int64_t k, int kp, int part_dtype, const 
     rp.csr_v_off = csr + p->tc_csr_v_off;
     rp.csr_v_idx = csr + p->tc_csr_v_idx;
     rp.kst = sh.kst;
+    rp.gt_rows = sh.gt_rows;
     rp.tc_unscale = &p->tc_scales.as<TcScales>()->gv_unscale;
   }
   if (part_dtype == SPCP_F32)

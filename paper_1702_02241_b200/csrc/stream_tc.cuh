@@ -79,25 +79,37 @@ struct TcParams {
   int kstore;  // partial row stride (floats): k rounded up to 4
   int debug;  // bisection switches (SPCP_TC_DEBUG): 1 skip GT stores, 2 skip GV stores,
               // 8 skip all MMAs (pipeline skeleton only), 16 / 32 / 64 skip the
-              // G^T U / G.V / residual MMAs
+              // G^T U / G.V / residual MMAs, 128 epilogue ignores MMA completion
+              // (timing only: decouples the epilogue from the reduction MMAs)
   long long* dbg_ts;  // [64][16] per-tile timestamps of CTA 0 (SPCP_TC_TIMESTAMPS builds)
 };
 
-template <int KP16, bool MASK>
+template <int KP16, bool MASK, int SEG = 0>
 struct TcCfg {
-  static constexpr int RB = KP16 * 2;  // operand image row bytes (32/64/128)
+  // SEG > 0: K-concatenated single images (rank k <= SEG, SEG = round_up(k, 4) <= 20):
+  //   U row = [uh | uh | um] and V row = [vh | vm | vh], segments SEG entries
+  //   apart, so the residual uh.vh + uh.vm + um.vh is ONE K-sum of 3 SEG
+  //   entries (ceil(3 SEG / 16) MMAs), and the reductions read the same images
+  //   as N = RB / 2 wide B operands (useful columns: segment 0 and 2 for G^T U,
+  //   segment 0 and 1 for G.V).  SEG == 0: two split images [uh|um], [vh|vm].
+  static constexpr bool KC = SEG > 0;
+  static constexpr int KE = 3 * SEG;
+  static constexpr int RB = KC ? (KE <= 16 ? 32 : (KE <= 32 ? 64 : 128)) : KP16 * 2;
   static constexpr uint32_t SWK = RB == 128 ? tc::SW_128 : (RB == 64 ? tc::SW_64 : tc::SW_32);
-  static constexpr int NSPLIT = 2;
+  static constexpr int NSPLIT = KC ? 1 : 2;
+  static constexpr int RT = RB * NSPLIT;  // image bytes per row over all splits
+  static constexpr int NKS = KC ? (KE + 15) / 16 : 0;  // residual K-steps (KC)
+  static constexpr int NB = RB / 2;                    // reduction N (KC)
   // X ring (released by the epilogue as soon as it has read the tile), V ring
   // (released when the tile's G.V MMA has finished), U buffers (per run)
 #ifndef SPCP_TC_GB
 #define SPCP_TC_GB 2
 #endif
   static constexpr int GB = SPCP_TC_GB;  // G staging images (1: shared by both groups)
-  static constexpr int NST = GB == 1 ? ((KP16 == 64 && MASK) ? 3 : 4)
-                                     : (KP16 == 16 ? (MASK ? 3 : 4) : (KP16 == 32 ? 3 : (MASK ? 2 : 3)));
-  static constexpr int NSV = KP16 == 64 ? 2 : (MASK ? 3 : 4);
-  static constexpr int UB = KP16 == 64 ? 1 : 2;
+  static constexpr int NST = GB == 1 ? ((RT == 128 && MASK) ? 3 : 4)
+                                     : (RT <= 64 ? (MASK ? 3 : 4) : (RT == 128 ? 3 : (MASK ? 2 : 3)));
+  static constexpr int NSV = RT == 256 ? 2 : (MASK ? 3 : 4);
+  static constexpr int UB = RT == 256 ? 1 : 2;
   static constexpr int LOOKAHEAD = NSV - 1 < 2 ? NSV - 1 : 2;  // residual issue lead (tiles)
   static constexpr int X_BYTES = 128 * 64 * 4;
   static constexpr int V_SPLIT = 64 * RB;
@@ -116,27 +128,42 @@ struct TcCfg {
   static constexpr int OFF_BAR = OFF_M + (MASK ? NST * 2048 : 0);
   static constexpr int SMEM = OFF_BAR + 512;  // dynamic smem base is 1 KB aligned
   static_assert(SMEM <= 232448, "shared memory budget");
-  // TMEM columns: S [2 x 64] | GV [2 x GVC*KP16] | GT [4 x GCAT*KP16] (two
-  // per epilogue group); the N-concatenated forms hold the [vh|vm] (resp.
-  // [uh|um]) halves side by side, summed at the drain
+  // TMEM columns: S [2 x 64] | GV [2 x GVW] | GT [4 x GTW] (two per epilogue
+  // group); legacy: the N-concatenated forms hold the [vh|vm] (resp. [uh|um])
+  // halves side by side, summed at the drain; KC: the image segments
   static constexpr int GCAT = KP16 <= 32 ? 2 : 1;
   static constexpr int GVC = KP16 <= 32 ? 2 : 1;
-  static constexpr uint32_t T_S = 0, T_GV = 128;
-  static constexpr uint32_t T_GT = T_GV + 2 * GVC * KP16;
-  static_assert(T_GT + 4 * GCAT * KP16 <= 512, "TMEM budget");
+  static constexpr int GVW = KC ? NB : GVC * KP16;
+  static constexpr int GTW = KC ? NB : GCAT * KP16;
+  // KC: the epilogue overwrites its S columns with G (fp16 pairs: gh at +0,
+  // gl at +16 of each warp's 32 columns) and G.V reads A from TMEM; three S
+  // buffers (the next writer of a buffer is the other group's tile) and three
+  // G^T U accumulators
+  static constexpr int NSB = KC ? 3 : 2;
+  static constexpr int NGT = KC ? 3 : 4;
+  static constexpr uint32_t T_S = 0, T_GV = 64 * NSB;
+  static constexpr uint32_t T_GT = T_GV + 2 * GVW;
+  static_assert(T_GT + NGT * GTW <= 512, "TMEM budget");
   static constexpr uint32_t TMEM_COLS = 512;
   static constexpr int NEPI = 16;  // epilogue warps: 2 groups x 4 quarters x 2 halves
   static constexpr int NEG = NEPI / 2;
-  static constexpr int FIRST_EPI = 4;  // warps 0-3: X producer, residual MMA issuer,
-                                       // U/V producer, reduction MMA issuer
+#ifndef SPCP_TC_SPLIT_RED
+#define SPCP_TC_SPLIT_RED 0  // measured: no gain
+#endif
+  static constexpr bool SPLIT_RED = SPCP_TC_SPLIT_RED != 0;
+  static constexpr int FIRST_EPI = SPLIT_RED ? 5 : 4;  // warps 0-3: X producer, residual MMA
+                                                       // issuer, U/V producer, reduction MMA
+                                                       // issuer (G^T U), [4: G.V issuer]
   static constexpr int NTHREADS = 32 * (FIRST_EPI + NEPI);
+  // KC drains: output columns [0, SEG) split over the two column-half warps
+  static constexpr int CW = KC ? ((SEG / 2 + 3) / 4) * 4 : 0;
 };
 
 struct TcBarriers {
   uint64_t stage_full[4], stage_empty[4];
   uint64_t v_full[4], v_empty[4];
   uint64_t u_full[2], u_empty[2];
-  uint64_t s_full[2], s_empty[2];
+  uint64_t s_full[3], s_empty[3];
   uint64_t g_full[2], gs_empty[2];  // G image staged (per group) / free (per image)
   uint64_t gt_full[4], gt_empty[4];
   uint64_t gv_full[2], gv_empty[2];
@@ -206,11 +233,11 @@ static_assert(sizeof(TcUnit) == 16, "TcUnit is read as one uint4");
 
 // Residual MMA issuer (one lane of warp 1): its own function, so ptxas
 // allocates it apart from the epilogue and keeps the descriptors uniform.
-template <int KP16, bool MASK>
+template <int KP16, bool MASK, int SEG>
 __device__ __noinline__ void tc_residual_issuer(unsigned char* sm, TcBarriers* bar,
                                                 const TcUnit* units, int T, int run0,
                                                 uint32_t tm, const TcParams& p) {
-  using C = TcCfg<KP16, MASK>;
+  using C = TcCfg<KP16, MASK, SEG>;
   using namespace tc;
   constexpr uint32_t ID_RES = idesc_f16(128, 64, false, false);
   constexpr int KS = KP16 / 16;
@@ -230,10 +257,10 @@ __device__ __noinline__ void tc_residual_issuer(unsigned char* sm, TcBarriers* b
       prev_run = run;
     }
     TC_TS(t, 12);
-    const int st = t % C::NSV, b = t & 1;
+    const int st = t % C::NSV, b = t % C::NSB;
     mbar_wait(&bar->v_full[st], (t / C::NSV) & 1);
     TC_TS(t, 13);
-    mbar_wait(&bar->s_empty[b], ((t >> 1) & 1) ^ 1);
+    mbar_wait(&bar->s_empty[b], ((t / C::NSB) & 1) ^ 1);
     TC_TS(t, 1);
     tc_fence_after();
     const uint64_t da = dU_k + uint64_t(ubuf * (C::U_BYTES >> 4));
@@ -241,12 +268,20 @@ __device__ __noinline__ void tc_residual_issuer(unsigned char* sm, TcBarriers* b
     if (do_mma && !(p.debug & 64)) {
       // uh.vh + uh.vm + um.vh: product q uses U split (q == 2), V split (q == 1)
       const uint32_t dt = tm + C::T_S + b * 64;
-      static_for<3 * KS>([&](auto I) {
-        constexpr int q = I / KS, ks = I % KS;
-        constexpr int oa = ((q == 2 ? C::U_SPLIT : 0) + ks * 32) >> 4;
-        constexpr int ob = ((q == 1 ? C::V_SPLIT : 0) + ks * 32) >> 4;
-        mma_ss_1<oa, ob>(dt, da, db, ID_RES, I != 0);
-      });
+      if constexpr (C::KC) {
+        // one K-sum over the concatenated segments: [uh|uh|um] . [vh|vm|vh]
+        static_for<C::NKS>([&](auto I) {
+          constexpr int o = (I * 32) >> 4;
+          mma_ss_1<o, o>(dt, da, db, ID_RES, I != 0);
+        });
+      } else {
+        static_for<3 * KS>([&](auto I) {
+          constexpr int q = I / KS, ks = I % KS;
+          constexpr int oa = ((q == 2 ? C::U_SPLIT : 0) + ks * 32) >> 4;
+          constexpr int ob = ((q == 1 ? C::V_SPLIT : 0) + ks * 32) >> 4;
+          mma_ss_1<oa, ob>(dt, da, db, ID_RES, I != 0);
+        });
+      }
     }
     mma_commit(&bar->s_full[b]);
     mma_commit(&bar->v_empty[st]);
@@ -257,47 +292,55 @@ __device__ __noinline__ void tc_residual_issuer(unsigned char* sm, TcBarriers* b
 
 // Reduction MMA issuer (one lane of warp 3): G^T U first (it releases the
 // group's G staging image), then G.V.
-template <int KP16, bool MASK>
+// ROLE 0: G^T U and G.V of each tile (one issuer); 1: G^T U only; 2: G.V only
+// (two reduction issuers, SPCP_TC_SPLIT_RED: each warp blocks on its own MMA
+// issue, so the two streams feed the tensor pipe in parallel)
+template <int KP16, bool MASK, int SEG, int ROLE>
 __device__ __noinline__ void tc_reduction_issuer(unsigned char* sm, TcBarriers* bar,
                                                  const TcUnit* units, int T, int run0,
                                                  uint32_t tm, const TcParams& p) {
-  using C = TcCfg<KP16, MASK>;
+  using C = TcCfg<KP16, MASK, SEG>;
   using namespace tc;
-  constexpr uint32_t ID_GV = idesc_f16(128, C::GVC * KP16, false, true);
-  constexpr uint32_t ID_GT = idesc_f16(64, C::GCAT * KP16, true, true);
+  // KC: G^T U stacked to M = 128 (A = [gh; gl], the two G images one N-atom
+  // apart), so each K-step is ONE MMA; the accumulator's lanes 64..127 hold the
+  // gl part, kept as separate partial rows and summed by the reduce kernel
+  constexpr uint32_t ID_GV = idesc_f16(128, C::GVW, false, true);
+  constexpr uint32_t ID_GT = idesc_f16(C::KC ? 128 : 64, C::GTW, true, true);
   const bool do_mma = !(p.debug & 8);
   const uint32_t u0 = smem_u32(sm + C::OFF_U), v0 = smem_u32(sm + C::OFF_V);
   const uint32_t g0 = smem_u32(sm + C::OFF_G);
   TcUnit un_next = T > 0 ? units[0] : TcUnit{};
   // G^T U: A = G image read MN-major (M = 64 tile columns), B = [uh|um]
-  const uint64_t dUn0 = umma_desc(u0, C::GCAT == 2 ? C::U_SPLIT : 8192, 8 * C::RB, C::SWK);
+  const uint64_t dUn0 = umma_desc(u0, (C::GCAT == 2 && !C::KC) ? C::U_SPLIT : 8192, 8 * C::RB, C::SWK);
   const uint64_t dGm = umma_desc(g0, 16384, 1024, SW_128);
   // G.V: the same G image read K-major (M = 128 tile rows, K = tile columns),
   // B = [vh|vm] MN-major
   const uint64_t dGk = umma_desc(g0, 16, 1024, SW_128);
-  const uint64_t dVn0 = umma_desc(v0, C::GVC == 2 ? C::V_SPLIT : 8192, 8 * C::RB, C::SWK);
+  const uint64_t dVn0 = umma_desc(v0, (C::GVC == 2 && !C::KC) ? C::V_SPLIT : 8192, 8 * C::RB, C::SWK);
   for (int t = 0; t < T; ++t) {
     const TcUnit un = un_next;
     if (t + 1 < T) un_next = units[t + 1];
     const int run = un.gv_slot - run0;
-    const int ubuf = run % C::UB, b = t & 1, st = t % C::NSV, gvb = run & 1, gtb = t & 3;
+    const int ubuf = run % C::UB, b = t & 1, st = t % C::NSV, gvb = run & 1, gtb = t % C::NGT;
     const bool first = (un.flags & TCU_FIRST_OF_RUN) != 0;
-    TC_TS(t, 14);
+    TC_TS(t, ROLE == 2 ? 26 : 14);
     mbar_wait(&bar->g_full[b], (t >> 1) & 1);
-    TC_TS(t, 2);
-    mbar_wait(&bar->gt_empty[gtb], ((t >> 2) & 1) ^ 1);
-    if (first) mbar_wait(&bar->gv_empty[gvb], ((run >> 1) & 1) ^ 1);
-    TC_TS(t, 3);
+    TC_TS(t, ROLE == 2 ? 27 : 2);
+    if (ROLE != 2 && !(p.debug & 128)) mbar_wait(&bar->gt_empty[gtb], ((t / C::NGT) & 1) ^ 1);
+    if (ROLE != 1 && first && !(p.debug & 128)) mbar_wait(&bar->gv_empty[gvb], ((run >> 1) & 1) ^ 1);
+    TC_TS(t, ROLE == 2 ? 28 : 3);
     tc_fence_after();
     const uint64_t dUn = dUn0 + uint64_t(ubuf * (C::U_BYTES >> 4));
     const uint64_t goff = uint64_t((C::GB == 1 ? 0 : b) * (C::G_BYTES >> 4));
-    const uint32_t gt = tm + C::T_GT + gtb * C::GCAT * KP16;
-    if (do_mma && !(p.debug & 16)) {
+    const uint32_t gt = tm + C::T_GT + gtb * C::GTW;
+    if (ROLE != 2 && do_mma && !(p.debug & 16)) {
       static_for<8>([&](auto I) {
         constexpr int ks = I;
         constexpr int uo = (ks * 16 * C::RB) >> 4, go = (2048 * ks) >> 4;
         constexpr int gl_o = go + (C::G_SPLIT >> 4);
-        if constexpr (C::GCAT == 2) {
+        if constexpr (C::KC) {
+          mma_ss_1<go, uo>(gt, dGm + goff, dUn, ID_GT, ks > 0);
+        } else if constexpr (C::GCAT == 2) {
           // B = [uh | um]: two N-atoms of the U image (LBO = split stride)
           mma_ss_1<go, uo>(gt, dGm + goff, dUn, ID_GT, ks > 0);
           mma_ss_1<gl_o, uo>(gt, dGm + goff, dUn, ID_GT, 1);
@@ -308,16 +351,23 @@ __device__ __noinline__ void tc_reduction_issuer(unsigned char* sm, TcBarriers* 
         }
       });
     }
-    mma_commit(&bar->gt_full[gtb]);
-    TC_TS(t, 25);
+    if (ROLE != 2) mma_commit(&bar->gt_full[gtb]);
+    if (C::KC) mma_commit(&bar->gs_empty[b]);  // the G image is G^T U's operand only
+    TC_TS(t, ROLE == 2 ? 29 : 25);
     const uint64_t dVn = dVn0 + uint64_t(st * (C::V_BYTES >> 4));
-    const uint32_t gv = tm + C::T_GV + gvb * C::GVC * KP16;
-    if (do_mma && !(p.debug & 32)) {
+    const uint32_t gv = tm + C::T_GV + gvb * C::GVW;
+    if (ROLE != 1 && do_mma && !(p.debug & 32)) {
       static_for<4>([&](auto I) {
         constexpr int ks = I;
         constexpr int vo = (ks * 16 * C::RB) >> 4;
         constexpr int ao = (32 * ks) >> 4, alo = ao + (C::G_SPLIT >> 4);
-        if constexpr (C::GVC == 2) {
+        if constexpr (C::KC) {
+          // A = G from TMEM (the tile's S columns: 32 per half, gh then gl)
+          constexpr int ca = 32 * (ks >> 1) + 8 * (ks & 1);
+          const uint32_t sa = tm + C::T_S + (t % C::NSB) * 64 + ca;
+          mma_ts_1<vo>(gv, sa, dVn, ID_GV, !(first && ks == 0));
+          mma_ts_1<vo>(gv, sa + 16, dVn, ID_GV, 1);
+        } else if constexpr (C::GVC == 2) {
           // B = [vh | vm] (N-concatenated), A = gh then gl (K-step of 16 columns)
           mma_ss_1<ao, vo>(gv, dGk + goff, dVn, ID_GV, !(first && ks == 0));
           mma_ss_1<alo, vo>(gv, dGk + goff, dVn, ID_GV, 1);
@@ -328,21 +378,24 @@ __device__ __noinline__ void tc_reduction_issuer(unsigned char* sm, TcBarriers* 
         }
       });
     }
-    mma_commit(&bar->gs_empty[b]);  // per tile parity (see the epilogue's wait)
-    mma_commit(&bar->v_empty[st]);
+    if (!C::KC) mma_commit(&bar->gs_empty[b]);  // per tile parity (see the epilogue's wait)
+    else mma_commit(&bar->s_empty[t % C::NSB]);  // S / G columns free for the residual
+    if (ROLE != 1) mma_commit(&bar->v_empty[st]);
     if (un.flags & TCU_LAST_OF_RUN) {
-      mma_commit(&bar->gv_full[gvb]);
-      mma_commit(&bar->u_empty[ubuf]);
+      if (ROLE != 1) mma_commit(&bar->gv_full[gvb]);
+      if (ROLE != 2) mma_commit(&bar->u_empty[ubuf]);
     }
-    TC_TS(t, 15);
+    TC_TS(t, ROLE == 2 ? 30 : 15);
   }
+  // decoupled-timing mode: nobody else waited for the last reductions
+  if ((p.debug & 128) && T > 0) mbar_wait(&bar->gs_empty[(T - 1) & 1], ((T - 1) >> 1) & 1);
 }
 
-template <int KP16, bool MASK>
-__global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
+template <int KP16, bool MASK, int SEG = 0>
+__global__ void __launch_bounds__(TcCfg<KP16, MASK, SEG>::NTHREADS, 1)
     tc_eval_kernel(const __grid_constant__ CUtensorMap xmap,
                    const __grid_constant__ CUtensorMap mmap, const TcParams p) {
-  using C = TcCfg<KP16, MASK>;
+  using C = TcCfg<KP16, MASK, SEG>;
   using namespace tc;
   extern __shared__ __align__(1024) unsigned char smem_dyn[];
   unsigned char* sm = smem_dyn;
@@ -370,13 +423,15 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
       mbar_init(&bar->v_full[i], 1);
       mbar_init(&bar->v_empty[i], 2);  // residual + G.V issuers
     }
+    for (int i = 0; i < C::NSB; ++i) {
+      mbar_init(&bar->s_full[i], 1);
+      mbar_init(&bar->s_empty[i], C::KC ? 1 : C::NEG);  // KC: G.V commit; else epilogue
+    }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bar->u_full[i], 1);
       mbar_init(&bar->u_empty[i], 2);  // residual + G^T U issuers
-      mbar_init(&bar->s_full[i], 1);
-      mbar_init(&bar->s_empty[i], C::NEG);
       mbar_init(&bar->g_full[i], C::NEG);
-      mbar_init(&bar->gs_empty[i], 1);
+      mbar_init(&bar->gs_empty[i], C::SPLIT_RED ? 2 : 1);
       mbar_init(&bar->gv_full[i], 1);
       mbar_init(&bar->gv_empty[i], C::NEG);
     }
@@ -471,7 +526,7 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
                   C::V_BYTES, &bar->v_full[sv]);
       }
     }
-  } else if (warp == 1 || warp == 3) {
+  } else if (warp == 1 || warp == 3 || (C::SPLIT_RED && warp == 4)) {
     // ======================= MMA issuers ================================
     // Two warps issue into the one tensor pipe, each on a single lane (no
     // elect: ptxas keeps the descriptors on the uniform datapath, ~6
@@ -490,9 +545,13 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
       const uint32_t g0 = smem_u32(sm + C::OFF_G);
       TcUnit un_next = T > 0 ? units[0] : TcUnit{};
       if (warp == 1)
-        tc_residual_issuer<KP16, MASK>(sm, bar, units, T, run0, tm, p);
+        tc_residual_issuer<KP16, MASK, SEG>(sm, bar, units, T, run0, tm, p);
+      else if (!C::SPLIT_RED)
+        tc_reduction_issuer<KP16, MASK, SEG, 0>(sm, bar, units, T, run0, tm, p);
+      else if (warp == 3)
+        tc_reduction_issuer<KP16, MASK, SEG, 1>(sm, bar, units, T, run0, tm, p);
       else
-        tc_reduction_issuer<KP16, MASK>(sm, bar, units, T, run0, tm, p);
+        tc_reduction_issuer<KP16, MASK, SEG, 2>(sm, bar, units, T, run0, tm, p);
     }
   } else {
     // ======================= epilogue warps =============================
@@ -514,17 +573,44 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
 
     // G^T U of tile t2 (this group's previous tile) -> CTA-private slot
     auto drain_gt = [&](int t2, const TcUnit& u2) {
-      const int b = t2 & 3;
-      mbar_wait(&bar->gt_full[b], (t2 >> 2) & 1);
+      const int b = t2 % C::NGT;
+      if (!(p.debug & 128)) mbar_wait(&bar->gt_full[b], (t2 / C::NGT) & 1);
       tc_fence_after();
-      if (!(p.debug & 1)) {
+      if constexpr (C::KC) {
+        if (!(p.debug & 1)) {
+          // M = 128 stacked accumulator: lane = slot row (0..63 gh part, 64..127 gl
+          // part); output column c = D[c] (uh) + D[2 SEG + c] (um)
+          float* dst = p.pright + (size_t(u2.gt_slot) * 128 + 32 * q + lane) * kst;
+          const bool first = (u2.flags & TCU_FIRST_TOUCH) != 0;
+          const uint32_t col = tm + lane_addr + C::T_GT + b * C::GTW;
+          static_for<C::CW / 4>([&](auto I) {
+            constexpr int c = I * 4;
+            const int cc = h * C::CW + c;
+            if (cc < SEG) {  // warp-uniform
+              uint32_t v[4], w[4];
+              tmem_ld4(col + cc, v);
+              tmem_ld4(col + 2 * SEG + cc, w);
+              tmem_wait_ld();
+              const float4 o = make_float4(__uint_as_float(v[0]) + __uint_as_float(w[0]),
+                                           __uint_as_float(v[1]) + __uint_as_float(w[1]),
+                                           __uint_as_float(v[2]) + __uint_as_float(w[2]),
+                                           __uint_as_float(v[3]) + __uint_as_float(w[3]));
+              if (first)
+                *reinterpret_cast<float4*>(dst + cc) = o;
+              else
+                red_add_v4(dst + cc, __float_as_uint(o.x), __float_as_uint(o.y),
+                           __float_as_uint(o.z), __float_as_uint(o.w));
+            }
+          });
+        }
+      } else if (!(p.debug & 1)) {
         float* dst = p.pright + (size_t(u2.gt_slot) * 64 + 16 * q + lane) * kst + h * GTC;
         const bool first = (u2.flags & TCU_FIRST_TOUCH) != 0;
         constexpr int CH = GTC < 16 ? GTC : 16;
 #pragma unroll
         for (int c0 = 0; c0 < GTC; c0 += CH) {
           uint32_t v[CH], w[CH];
-          const uint32_t col = tm + lane_addr + C::T_GT + b * C::GCAT * KP16 + h * GTC + c0;
+          const uint32_t col = tm + lane_addr + C::T_GT + b * C::GTW + h * GTC + c0;
           tmem_ldn<CH>(col, v);
           if constexpr (C::GCAT == 2) {
             tmem_ldn<CH>(col + KP16, w);
@@ -557,15 +643,36 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
     auto drain_gv = [&](const TcUnit& u2) {
       const int run = u2.gv_slot - run0;
       const int gvb = run & 1;
-      mbar_wait(&bar->gv_full[gvb], (run >> 1) & 1);
+      if (!(p.debug & 128)) mbar_wait(&bar->gv_full[gvb], (run >> 1) & 1);
       tc_fence_after();
-      if (!(p.debug & 2)) {
+      if constexpr (C::KC) {
+        if (!(p.debug & 2)) {
+          // output column c = D[c] (vh) + D[SEG + c] (vm)
+          float* dst = p.pleft + (size_t(u2.gv_slot) * 128 + row) * kst;
+          const uint32_t col = tm + lane_addr + C::T_GV + gvb * C::GVW;
+          static_for<C::CW / 4>([&](auto I) {
+            constexpr int c = I * 4;
+            const int cc = h * C::CW + c;
+            if (cc < SEG) {
+              uint32_t v[4], w[4];
+              tmem_ld4(col + cc, v);
+              tmem_ld4(col + SEG + cc, w);
+              tmem_wait_ld();
+              *reinterpret_cast<float4*>(dst + cc) =
+                  make_float4(__uint_as_float(v[0]) + __uint_as_float(w[0]),
+                              __uint_as_float(v[1]) + __uint_as_float(w[1]),
+                              __uint_as_float(v[2]) + __uint_as_float(w[2]),
+                              __uint_as_float(v[3]) + __uint_as_float(w[3]));
+            }
+          });
+        }
+      } else if (!(p.debug & 2)) {
         float* dst = p.pleft + (size_t(u2.gv_slot) * 128 + row) * kst + h * GTC;
         constexpr int CH = GTC < 16 ? GTC : 16;
 #pragma unroll
         for (int c0 = 0; c0 < GTC; c0 += CH) {
           uint32_t v[CH], w[CH];
-          const uint32_t col = tm + lane_addr + C::T_GV + gvb * C::GVC * KP16 + h * GTC + c0;
+          const uint32_t col = tm + lane_addr + C::T_GV + gvb * C::GVW + h * GTC + c0;
           tmem_ldn<CH>(col, v);
           if constexpr (C::GVC == 2) {
             tmem_ldn<CH>(col + KP16, w);
@@ -592,11 +699,11 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
     for (int t = grp; t < T; t += 2) {
       const TcUnit un = un_next;
       if (t + 2 < T) un_next = units[t + 2];  // consumed next iteration: latency hidden
-      const int st = t % C::NST, b = grp;
+      const int st = t % C::NST, b = grp, sbuf = t % C::NSB;
       const bool ts_w = ((e == 0 || e == 4) && lane == 0);
       if (ts_w) TC_TS(t, 4);
       // ---- S tile and X tile (32 columns: two chunks of 16)
-      mbar_wait(&bar->s_full[b], (t >> 1) & 1);
+      mbar_wait(&bar->s_full[sbuf], (t / C::NSB) & 1);
       if (ts_w) TC_TS(t, 5);
       tc_fence_after();
       mbar_wait(&bar->stage_full[st], (t / C::NST) & 1);
@@ -615,7 +722,7 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
 #pragma unroll
         for (int c = 0; c < 16; ++c) sv[c] = c;
 #else
-        tmem_ldn<16>(tm + lane_addr + C::T_S + b * 64 + 32 * h + 16 * ch, sv);
+        tmem_ldn<16>(tm + lane_addr + C::T_S + sbuf * 64 + 32 * h + 16 * ch, sv);
 #endif
         float xv[16];
 #if defined(SPCP_TC_BISECT_EPI_SKIP) || defined(SPCP_TC_BISECT_NO_SMEM)
@@ -624,8 +731,7 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
 #else
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          const float4 f =
-              *reinterpret_cast<const float4*>(xs + Swz<128>::offset(row, (4 * ch + c) * 16));
+          const float4 f = lds128(xs + Swz<128>::offset(row, (4 * ch + c) * 16));
           xv[4 * c] = f.x;
           xv[4 * c + 1] = f.y;
           xv[4 * c + 2] = f.z;
@@ -637,7 +743,7 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
-            mbar_arrive(&bar->s_empty[b]);
+            if (!C::KC) mbar_arrive(&bar->s_empty[sbuf]);
             mbar_arrive(&bar->stage_empty[st]);
           }
         }
@@ -665,6 +771,12 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
         }
       }
       phi_acc += double(hs2.x) + double(hs2.y);
+      if constexpr (C::KC) {
+        // G over this warp's own S columns: the A operand of the TS G.V MMA
+        const uint32_t gcol = tm + lane_addr + C::T_S + sbuf * 64 + 32 * h;
+        tmem_st16(gcol, hi);
+        tmem_st16(gcol + 16, lo);
+      }
       if (ts_w) TC_TS(t, 7);
       if (ts_w) TC_TS(t, 8);
       // ---- G to smem: A of both G^T.U (MN-major view) and G.V (K-major view)
@@ -673,7 +785,7 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
         // (the other parity's barrier, phase (t-1)/2; in-order MMA completion
         // covers tile t-2).  Per-parity barriers never lag two phases behind.
         if (t >= 1) mbar_wait(&bar->gs_empty[(t - 1) & 1], ((t - 1) >> 1) & 1);
-      } else {
+      } else if (!(p.debug & 128)) {
         mbar_wait(&bar->gs_empty[b], ((t >> 1) & 1) ^ 1);
       }
       if (ts_w) TC_TS(t, 9);
@@ -691,6 +803,10 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK>::NTHREADS, 1)
       }
 #endif
       fence_proxy_async_smem();
+      if constexpr (C::KC) {
+        tmem_wait_st();
+        tc_fence_before();
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar->g_full[b]);
       if (ts_w) TC_TS(t, 10);
@@ -836,6 +952,53 @@ __global__ void tc_images_kernel(const double* __restrict__ z, const double* __r
       const int64_t tcol = j >> 6;
       split2_store<RB>(v_img + tcol * (2 * 64 * RB), 64 * RB, int(j & 63), c, w * sv);
     }
+  }
+}
+
+// pass 3 (K-concatenated layout, TcCfg<.., SEG>::KC): one fp16 image per 128-row
+// sub-band of U, rows [uh | uh | um | 0] (U negated, as above), and per 64-row
+// tile of V, rows [vh | vm | vh | 0]; segment e / SEG, rank index e % SEG
+template <int SEG>
+__global__ void tc_images_kc_kernel(const double* __restrict__ z, const double* __restrict__ dz,
+                                    double alpha, int64_t m, int64_t n, int64_t k, int64_t m_pad,
+                                    int64_t n_pad, TcScales* sc, double tau, unsigned char* u_img,
+                                    unsigned char* v_img) {
+  using C = TcCfg<16, false, SEG>;
+  constexpr int RB = C::RB, NE = RB / 2;
+  const TcScales scl = tc_compute_scales(sc, tau);
+  const double su = scl.su, sv = scl.sv;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    sc->su = scl.su;
+    sc->sv = scl.sv;
+    sc->sigma = scl.sigma;
+    sc->tau_s = scl.tau_s;
+    sc->kappa = scl.kappa;
+    sc->gv_unscale = scl.gv_unscale;
+    sc->gt_unscale = scl.gt_unscale;
+    sc->phi_unscale = scl.phi_unscale;
+  }
+  const int64_t total = (m_pad + n_pad) * NE;
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < total;
+       q += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t row = q / NE;
+    const int e = int(q % NE);
+    const int seg = e / SEG, c = e % SEG;
+    const bool is_u = row < m_pad;
+    const int64_t r = is_u ? row : row - m_pad;
+    double w = 0.0;
+    if (seg < 3 && c < k && r < (is_u ? m : n)) {
+      const int64_t o = (is_u ? 0 : m * k) + r * k + c;
+      w = z[o] + (dz ? alpha * dz[o] : 0.0);
+      w = is_u ? -w * su : w * sv;
+    }
+    const __half hh = __double2half(w);
+    const __half lo = __double2half(w - double(__half2float(hh)));
+    // U: segments (h, h, m); V: (h, m, h)
+    const bool take_lo = is_u ? (seg == 2) : (seg == 1);
+    const __half val = take_lo ? lo : hh;
+    unsigned char* base = is_u ? u_img + (r >> 7) * (128 * RB) : v_img + (r >> 6) * (64 * RB);
+    const int rr = int(is_u ? (r & 127) : (r & 63));
+    *reinterpret_cast<__half*>(base + tc::Swz<RB>::offset(rr, e * 2)) = val;
   }
 }
 

@@ -77,6 +77,16 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 
+// 16-byte shared load pinned to one LDS.128 (the compiler otherwise splits some
+// of the swizzled X reads into LDS.64 pairs, which double their wavefronts)
+__device__ __forceinline__ float4 lds128(const void* p) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(smem_u32(p)));
+  return v;
+}
+
 // ------------------------------------------------------------------ packed fp32 pairs
 // Blackwell FFMA2 / FADD2 / FMUL2 on float2 (one instruction per pair)
 __device__ __forceinline__ uint64_t f2_bits(float2 v) {

@@ -36,6 +36,8 @@ using namespace spcp::tc;
 struct Out {
   float d1[128 * 64], d2[128 * 64], d3[128 * 32], d4[128 * 32], x5[128 * 32];
   float d6[128 * 32];
+  float d7[128 * 64];
+  uint32_t cp_raw[128 * 16], st_raw[128 * 16];
 };
 
 __global__ void __launch_bounds__(128) probe(const __half* U, const __half* V, const __half* G,
@@ -120,6 +122,15 @@ __global__ void __launch_bounds__(128) probe(const __half* U, const __half* V, c
     for (int s = 0; s < 8; ++s)
       mma_ss(tm + 256, umma_desc(g0 + 2048 * s, 16384, 1024, SW_128),
              umma_desc(a0 + 1024 * s, 8192, 512, SW_64), idesc_f16(64, 32, true, true), s > 0);
+    // P7: tcgen05.cp of the K-major SW64 U image (one K-step of 16 fp16 = 8
+    // TMEM columns per copy) into cols 320.., then a TS MMA from the copy
+    for (int s = 0; s < 2; ++s)
+      asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(tm + 320 + 8 * s),
+                   "l"(umma_desc(a0 + 32 * s, 16, 512, SW_64))
+                   : "memory");
+    for (int s = 0; s < 2; ++s)
+      mma_ts(tm + 352, tm + 320 + 8 * s, umma_desc(b0 + 32 * s, 16, 512, SW_64),
+             idesc_f16(128, 64, false, false), s > 0);
     mma_commit(&bar_mma);
     // P5: TMA
     mbar_arrive_expect_tx(&bar_tma, 128 * 32 * 4);
@@ -149,6 +160,17 @@ __global__ void __launch_bounds__(128) probe(const __half* U, const __half* V, c
     tmem_wait_ld();
     for (int c = 0; c < 16; ++c) out->d6[row * 32 + c0 + c] = __uint_as_float(r[c]);
   }
+  for (int c0 = 0; c0 < 64; c0 += 16) {
+    tmem_ld16(tm + lane_base + 352 + c0, r);
+    tmem_wait_ld();
+    for (int c = 0; c < 16; ++c) out->d7[row * 64 + c0 + c] = __uint_as_float(r[c]);
+  }
+  tmem_ld16(tm + lane_base + 320, r);
+  tmem_wait_ld();
+  for (int c = 0; c < 16; ++c) out->cp_raw[row * 16 + c] = r[c];
+  tmem_ld16(tm + lane_base + 128, r);
+  tmem_wait_ld();
+  for (int c = 0; c < 16; ++c) out->st_raw[row * 16 + c] = r[c];
   for (int c = 0; c < 32; ++c) {
     const uint32_t o = Swz<128>::offset(row, c * 4);
     out->x5[row * 32 + c] = *reinterpret_cast<const float*>(reinterpret_cast<unsigned char*>(x_img) + o);
@@ -205,13 +227,15 @@ int main() {
   CK(cudaDeviceSynchronize());
   Out* h = new Out;
   CK(cudaMemcpy(h, dO, sizeof(Out), cudaMemcpyDeviceToHost));
-  int bad1 = 0, bad2 = 0, bad3 = 0, bad4 = 0, bad5 = 0;
+  int bad1 = 0, bad2 = 0, bad3 = 0, bad4 = 0, bad5 = 0, bad7 = 0, bad7r = 0;
+  for (int i = 0; i < 128 * 16; ++i) bad7r += h->cp_raw[i] != h->st_raw[i];
   for (int i = 0; i < 128; ++i)
     for (int j = 0; j < 64; ++j) {
       float e = 0;
       for (int k = 0; k < 32; ++k) e += Uf[i * 32 + k] * Vf[j * 32 + k];
       bad1 += h->d1[i * 64 + j] != e;
       bad2 += h->d2[i * 64 + j] != e;
+      bad7 += h->d7[i * 64 + j] != e;
     }
   for (int j = 0; j < 128; ++j)
     for (int c = 0; c < 32; ++c) {
@@ -247,5 +271,7 @@ int main() {
   printf("P3 ss MN-major SW128 x SW64 mismatches %d / %d\n", bad3, 128 * 32);
   printf("P4 ts A-TMEM x MN-major B   mismatches %d / %d\n", bad4, 128 * 32);
   printf("P5 TMA SW128 fp32 tile      mismatches %d / %d\n", bad5, 128 * 32);
-  return (bad1 + bad2 + bad3 + bad4 + bad5) ? 1 : 0;
+  printf("P7 tcgen05.cp U -> TMEM     raw mismatches vs tcgen05.st %d / %d, TS MMA mismatches %d / %d\n",
+         bad7r, 128 * 16, bad7, 128 * 64);
+  return (bad1 + bad2 + bad3 + bad4 + bad5 + bad7) ? 1 : 0;
 }
