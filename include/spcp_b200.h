@@ -102,6 +102,14 @@ int spcp_problem_info(spcp_problem* p, double* info);
 int spcp_eval(spcp_problem* p, int64_t k, int dtype, const double* z, const double* dz,
               double alpha, double* g_out, double* out);
 
+/* Stream-ordered spcp_eval: the same evaluation, but the 8 scalars stay on the
+ * device (copied into out_dev, device float64[8], when it is not NULL) and the
+ * call does not synchronise — for callers that keep the control flow on the
+ * device or batch several evaluations (the throughput bench).  Same reference
+ * function (split_objective solver.py:105-123). */
+int spcp_eval_async(spcp_problem* p, int64_t k, int dtype, const double* z, const double* dz,
+                    double alpha, double* g_out, double* out_dev);
+
 /* Sharded evaluation split around the grad_U all-reduce:
  * _partial writes the shard's G_p V_p (m x k, `dtype` elements) into gu_part
  * (device), 4 shard scalars [phi_p, lambda/2|V_p|^2, g_V.dz_V, |g_V|^2] into

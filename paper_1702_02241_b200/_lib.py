@@ -35,6 +35,7 @@ EXPORTS = {
     "spcp_problem_set_stream": [_vp, _vp],
     "spcp_problem_info": [_vp, _dp],
     "spcp_eval": [_vp, _i64, _i32, _vp, _vp, _d, _vp, _dp],
+    "spcp_eval_async": [_vp, _i64, _i32, _vp, _vp, _d, _vp, _vp],
     "spcp_eval_partial": [_vp, _i64, _i32, _vp, _vp, _d, _vp, _vp, _vp],
     "spcp_eval_finish": [_vp, _i64, _i32, _vp, _vp, _d, _vp, _vp, _vp, _dp],
     "spcp_split_objective_host": [_vp, _i64, _i32, _vp, _vp, _dp, _vp, _vp],

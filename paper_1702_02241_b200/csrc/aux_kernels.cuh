@@ -147,6 +147,68 @@ struct ReduceParams {
   const float* tc_unscale;  // [0]: G.V partials, [1]: G^T.U partials
 };
 
+// Block partials of the six vector sums -> the last block folds them (and the
+// phi partials) in a fixed order into the scalar outputs.
+__device__ __forceinline__ void reduce_tail(const ReduceParams& p, const double (&s)[6],
+                                            double* scratch, bool& am_last) {
+  for (int r = 0; r < 6; ++r) {
+    const double v = block_sum(s[r], scratch);
+    if (threadIdx.x == 0) p.blk[blockIdx.x * 6 + r] = v;
+  }
+  // last block folds the block partials in a fixed order
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned done = atomicAdd(p.counter, 1u);
+    am_last = (done == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  double tot[6];
+  for (int r = 0; r < 6; ++r) {
+    double v = 0.0;
+    for (int b = threadIdx.x; b < int(gridDim.x); b += blockDim.x) v += p.blk[b * 6 + r];
+    tot[r] = block_sum(v, scratch);
+  }
+  double phi = 0.0;
+  {
+    double v = 0.0;
+    for (int b = threadIdx.x; b < p.nphi; b += blockDim.x) v += p.pphi ? p.pphi[b] : 0.0;
+    phi = block_sum(v, scratch);
+  }
+  if (threadIdx.x == 0) {
+    const double half_l = 0.5 * p.lambda_l;
+    if (p.u_mode == U_PARTIAL) {
+      p.scal_out[0] = phi;
+      p.scal_out[1] = half_l * tot[5];
+      p.scal_out[2] = tot[4];
+      p.scal_out[3] = tot[3];
+    } else if (p.u_mode == U_FROM_SUM) {
+      const double regU = half_l * tot[2];
+      p.out[0] = p.scal_sum[0] + regU + p.scal_sum[1];
+      p.out[1] = p.scal_sum[0];
+      p.out[2] = regU + p.scal_sum[1];
+      p.out[3] = tot[1] + p.scal_sum[2];
+      p.out[4] = tot[0] + p.scal_sum[3];
+      p.out[5] = tot[0];
+      p.out[6] = tot[1];
+      p.out[7] = 0.0;
+    } else {
+      const double reg = half_l * (tot[2] + tot[5]);
+      p.out[0] = phi + reg;
+      p.out[1] = phi;
+      p.out[2] = reg;
+      p.out[3] = tot[1] + tot[4];
+      p.out[4] = tot[0] + tot[3];
+      p.out[5] = tot[0];
+      p.out[6] = tot[1];
+      p.out[7] = 0.0;
+    }
+    *p.counter = 0u;  // re-arm for the next launch
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p) {
   __shared__ double scratch[32];
@@ -217,62 +279,101 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p) {
       s[5] += w * w;
     }
   }
-  for (int r = 0; r < 6; ++r) {
-    const double v = block_sum(s[r], scratch);
-    if (threadIdx.x == 0) p.blk[blockIdx.x * 6 + r] = v;
-  }
-  // last block folds the block partials in a fixed order
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned done = atomicAdd(p.counter, 1u);
-    am_last = (done == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!am_last) return;
-  __threadfence();
-  double tot[6];
-  for (int r = 0; r < 6; ++r) {
-    double v = 0.0;
-    for (int b = threadIdx.x; b < int(gridDim.x); b += blockDim.x) v += p.blk[b * 6 + r];
-    tot[r] = block_sum(v, scratch);
-  }
-  double phi = 0.0;
-  {
-    double v = 0.0;
-    for (int b = threadIdx.x; b < p.nphi; b += blockDim.x) v += p.pphi ? p.pphi[b] : 0.0;
-    phi = block_sum(v, scratch);
-  }
-  if (threadIdx.x == 0) {
-    const double half_l = 0.5 * p.lambda_l;
-    if (p.u_mode == U_PARTIAL) {
-      p.scal_out[0] = phi;
-      p.scal_out[1] = half_l * tot[5];
-      p.scal_out[2] = tot[4];
-      p.scal_out[3] = tot[3];
-    } else if (p.u_mode == U_FROM_SUM) {
-      const double regU = half_l * tot[2];
-      p.out[0] = p.scal_sum[0] + regU + p.scal_sum[1];
-      p.out[1] = p.scal_sum[0];
-      p.out[2] = regU + p.scal_sum[1];
-      p.out[3] = tot[1] + p.scal_sum[2];
-      p.out[4] = tot[0] + p.scal_sum[3];
-      p.out[5] = tot[0];
-      p.out[6] = tot[1];
-      p.out[7] = 0.0;
+  reduce_tail(p, s, scratch, am_last);
+}
+
+// Tensor-core partial layout (CSR slots, TcParams): one thread per (row, 4
+// columns); the slot sources of a sub-band / column tile are read as float4
+// and summed in fp64 in the CSR's fixed order (deterministic).  U side:
+// U_FULL or U_PARTIAL; V side always.
+__global__ void __launch_bounds__(256) tc_reduce_kernel(const ReduceParams p) {
+  __shared__ double scratch[32];
+  __shared__ bool am_last;
+  const int c4n = p.kst >> 2;
+  const int64_t nu4 = p.m * c4n, nv4 = p.n * c4n;
+  double s[6] = {0, 0, 0, 0, 0, 0};
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const float* plf = reinterpret_cast<const float*>(p.pleft);
+  const float* prf = reinterpret_cast<const float*>(p.pright);
+  const float gvs = p.tc_unscale[0], gts = p.tc_unscale[1];
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < nu4 + nv4; q += stride) {
+    const bool is_u = q < nu4;
+    const int64_t qq = is_u ? q : q - nu4;
+    const int64_t r = qq / c4n;
+    const int c0 = int(qq % c4n) * 4;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    if (is_u) {
+      const int sb = int(r >> 7);
+      const int e0 = p.csr_u_off[sb], e1 = p.csr_u_off[sb + 1];
+      const float* base = plf + (r & 127) * p.kst + c0;
+      const int64_t sst = int64_t(128) * p.kst;
+      int e = e0;
+      for (; e + 4 <= e1; e += 4) {
+        const float4 v0 = *reinterpret_cast<const float4*>(base + p.csr_u_idx[e] * sst);
+        const float4 v1 = *reinterpret_cast<const float4*>(base + p.csr_u_idx[e + 1] * sst);
+        const float4 v2 = *reinterpret_cast<const float4*>(base + p.csr_u_idx[e + 2] * sst);
+        const float4 v3 = *reinterpret_cast<const float4*>(base + p.csr_u_idx[e + 3] * sst);
+        a0 += v0.x; a1 += v0.y; a2 += v0.z; a3 += v0.w;
+        a0 += v1.x; a1 += v1.y; a2 += v1.z; a3 += v1.w;
+        a0 += v2.x; a1 += v2.y; a2 += v2.z; a3 += v2.w;
+        a0 += v3.x; a1 += v3.y; a2 += v3.z; a3 += v3.w;
+      }
+      for (; e < e1; ++e) {
+        const float4 v0 = *reinterpret_cast<const float4*>(base + p.csr_u_idx[e] * sst);
+        a0 += v0.x; a1 += v0.y; a2 += v0.z; a3 += v0.w;
+      }
+      a0 *= gvs; a1 *= gvs; a2 *= gvs; a3 *= gvs;
     } else {
-      const double reg = half_l * (tot[2] + tot[5]);
-      p.out[0] = phi + reg;
-      p.out[1] = phi;
-      p.out[2] = reg;
-      p.out[3] = tot[1] + tot[4];
-      p.out[4] = tot[0] + tot[3];
-      p.out[5] = tot[0];
-      p.out[6] = tot[1];
-      p.out[7] = 0.0;
+      const int tcol = int(r >> 6);
+      const int e0 = p.csr_v_off[tcol], e1 = p.csr_v_off[tcol + 1];
+      const float* base = prf + (r & 63) * p.kst + c0;
+      const int64_t sst = int64_t(p.gt_rows) * p.kst, hoff = int64_t(64) * p.kst;
+      const bool two = p.gt_rows == 128;
+      int e = e0;
+      for (; e + 2 <= e1; e += 2) {
+        const float* b0 = base + p.csr_v_idx[e] * sst;
+        const float* b1 = base + p.csr_v_idx[e + 1] * sst;
+        const float4 v0 = *reinterpret_cast<const float4*>(b0);
+        const float4 w0 = two ? *reinterpret_cast<const float4*>(b0 + hoff) : make_float4(0, 0, 0, 0);
+        const float4 v1 = *reinterpret_cast<const float4*>(b1);
+        const float4 w1 = two ? *reinterpret_cast<const float4*>(b1 + hoff) : make_float4(0, 0, 0, 0);
+        a0 += v0.x; a1 += v0.y; a2 += v0.z; a3 += v0.w;
+        a0 += w0.x; a1 += w0.y; a2 += w0.z; a3 += w0.w;
+        a0 += v1.x; a1 += v1.y; a2 += v1.z; a3 += v1.w;
+        a0 += w1.x; a1 += w1.y; a2 += w1.z; a3 += w1.w;
+      }
+      for (; e < e1; ++e) {
+        const float* b0 = base + p.csr_v_idx[e] * sst;
+        const float4 v0 = *reinterpret_cast<const float4*>(b0);
+        const float4 w0 = two ? *reinterpret_cast<const float4*>(b0 + hoff) : make_float4(0, 0, 0, 0);
+        a0 += v0.x; a1 += v0.y; a2 += v0.z; a3 += v0.w;
+        a0 += w0.x; a1 += w0.y; a2 += w0.z; a3 += w0.w;
+      }
+      a0 *= gts; a1 *= gts; a2 *= gts; a3 *= gts;
     }
-    *p.counter = 0u;  // re-arm for the next launch
+    const double acc[4] = {a0, a1, a2, a3};
+    const int64_t obase = (is_u ? 0 : p.m * p.k) + r * p.k;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = c0 + j;
+      if (c >= p.k) break;
+      const int64_t o = obase + c;
+      if (is_u && p.u_mode == U_PARTIAL) {
+        reinterpret_cast<float*>(p.gu_part)[r * p.k + c] = float(acc[j]);
+        continue;
+      }
+      double w = p.z[o];
+      const double d = p.dz ? p.dz[o] : 0.0;
+      w += p.alpha * d;
+      const double g = acc[j] + p.lambda_l * w;
+      p.g_out[o] = g;
+      const int sidx = is_u ? 0 : 3;
+      s[sidx] += g * g;
+      s[sidx + 1] += g * d;
+      s[sidx + 2] += w * w;
+    }
   }
+  reduce_tail(p, s, scratch, am_last);
 }
 
 // Reduce apply() partials to float64 outputs (rows x b, b <= bp).

@@ -88,8 +88,11 @@ struct spcp_problem {
   double* host_out = nullptr;  // pinned [64]
   // profiling
   bool prof = false;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  bool ev_pending = false;
+  // ring of (start, end) event pairs around the fused kernel: stream-ordered
+  // evaluations keep recording; pairs are folded when the ring is full and on read
+  static constexpr int kEvRing = 64;
+  cudaEvent_t ev0[kEvRing] = {}, ev1[kEvRing] = {};
+  int ev_head = 0, ev_count = 0;
   double prof_ms = 0.0;
   int64_t prof_count = 0;
   int64_t launches = 0;
@@ -123,6 +126,19 @@ struct LaunchShape {
   int kst = 0;
   int gt_rows = 64;
 };
+
+static int prof_fold(spcp_problem* p, int n);
+static int prof_begin(spcp_problem* p) {
+  if (p->ev_count == spcp_problem::kEvRing && prof_fold(p, 1)) return SPCP_ERR_CUDA;
+  SPCP_CUDA(cudaEventRecord(p->ev0[p->ev_head], p->stream));
+  return SPCP_OK;
+}
+static int prof_end(spcp_problem* p) {
+  SPCP_CUDA(cudaEventRecord(p->ev1[p->ev_head], p->stream));
+  p->ev_head = (p->ev_head + 1) % spcp_problem::kEvRing;
+  p->ev_count++;
+  return SPCP_OK;
+}
 
 template <typename T, typename TX, int KR, int PW, int MODE, bool MASK>
 static int launch_stream(spcp_problem* p, StreamParams sp, LaunchShape& shape, bool prof) {
@@ -158,10 +174,10 @@ static int launch_stream(spcp_problem* p, StreamParams sp, LaunchShape& shape, b
   sp.pright = p->pright.ptr;
   sp.pphi = p->pphi.as<double>();
   dim3 grid{unsigned(nch), unsigned(nrb), 1u};
-  if (prof) SPCP_CUDA(cudaEventRecord(p->ev0, p->stream));
+  if (prof && prof_begin(p)) return SPCP_ERR_CUDA;
   kern<<<grid, G::NT, smem, p->stream>>>(sp);
   SPCP_CHECK_LAUNCH("stream_kernel");
-  if (prof) SPCP_CUDA(cudaEventRecord(p->ev1, p->stream));
+  if (prof && prof_end(p)) return SPCP_ERR_CUDA;
   p->launches++;
   return SPCP_OK;
 }
@@ -241,16 +257,20 @@ static int ensure_common(spcp_problem* p) {
   return SPCP_OK;
 }
 
-static int prof_collect(spcp_problem* p) {
-  if (p->prof && p->ev_pending) {
+// fold the oldest `n` recorded pairs (waits for them)
+static int prof_fold(spcp_problem* p, int n) {
+  for (int i = 0; i < n && p->ev_count > 0; ++i) {
+    const int slot = (p->ev_head - p->ev_count + spcp_problem::kEvRing) % spcp_problem::kEvRing;
     float ms = 0.f;
-    SPCP_CUDA(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+    SPCP_CUDA(cudaEventSynchronize(p->ev1[slot]));
+    SPCP_CUDA(cudaEventElapsedTime(&ms, p->ev0[slot], p->ev1[slot]));
     p->prof_ms += ms;
     p->prof_count++;
-    p->ev_pending = false;
+    p->ev_count--;
   }
   return SPCP_OK;
 }
+static int prof_collect(spcp_problem* p) { return prof_fold(p, p->ev_count); }
 
 static int check_k(spcp_problem* p, int64_t k) {
   if (k < 1 || k > std::min(p->m, p->n_total))
@@ -462,10 +482,10 @@ static int tc_launch(spcp_problem* p, int64_t k) {
     SPCP_CUDA(cudaMemsetAsync(dbg, 0, 64 * 32 * sizeof(long long), p->stream));
     tp.dbg_ts = dbg;
   }
-  if (p->prof) SPCP_CUDA(cudaEventRecord(p->ev0, p->stream));
+  if (p->prof && prof_begin(p)) return SPCP_ERR_CUDA;
   kern<<<p->tc_grid, C::NTHREADS, C::SMEM, p->stream>>>(p->tc_xmap, p->tc_mmap, tp);
   SPCP_CHECK_LAUNCH("tc_eval_kernel");
-  if (p->prof) SPCP_CUDA(cudaEventRecord(p->ev1, p->stream));
+  if (p->prof && prof_end(p)) return SPCP_ERR_CUDA;
   if (tp.debug & 4) {
     long long h[64 * 32];
     SPCP_CUDA(cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, p->stream));
@@ -506,7 +526,7 @@ static int tc_images_kc(spcp_problem* p, int64_t k, const double* z, const doubl
   int rc;
   if ((rc = p->tc_uimg.ensure(size_t(p->tc_nsb) * 128 * RB))) return rc;
   if ((rc = p->tc_vimg.ensure(size_t(p->tc_ntc) * 64 * RB))) return rc;
-  const int64_t total = (p->m_pad + p->n_pad) * (RB / 2);
+  const int64_t total = (p->m_pad + p->n_pad) * SEG;
   tc_images_kc_kernel<SEG><<<grid_for(total), 256, 0, p->stream>>>(
       z, dz, alpha, p->m, p->n, k, p->m_pad, p->n_pad, p->tc_scales.as<TcScales>(),
       p->lambda_s, p->tc_uimg.as<unsigned char>(), p->tc_vimg.as<unsigned char>());
@@ -814,7 +834,9 @@ static int run_reduce(spcp_problem* p, int64_t k, int kp, int part_dtype, const 
     rp.gt_rows = sh.gt_rows;
     rp.tc_unscale = &p->tc_scales.as<TcScales>()->gv_unscale;
   }
-  if (part_dtype == SPCP_F32)
+  if (sh.tc && (u_mode == U_FULL || u_mode == U_PARTIAL) && v_mode)
+    tc_reduce_kernel<<<nblk, 256, 0, p->stream>>>(rp);
+  else if (part_dtype == SPCP_F32)
     reduce_kernel<float><<<nblk, 256, 0, p->stream>>>(rp);
   else
     reduce_kernel<double><<<nblk, 256, 0, p->stream>>>(rp);
@@ -827,7 +849,7 @@ static int fetch_out(spcp_problem* p, double* out) {
   SPCP_CUDA(cudaMemcpyAsync(p->host_out, p->out_dev.ptr, 8 * sizeof(double),
                             cudaMemcpyDeviceToHost, p->stream));
   SPCP_CUDA(cudaStreamSynchronize(p->stream));
-  if (p->prof && p->ev_pending) prof_collect(p);
+  if (p->prof && p->ev_count) prof_collect(p);
   std::memcpy(out, p->host_out, 8 * sizeof(double));
   return SPCP_OK;
 }
@@ -971,8 +993,10 @@ int spcp_problem_create(spcp_problem** out, int device, int64_t m, int64_t n, co
     p->f_zero = h[0];
     p->n_obs = h[1];
   }
-  SPCP_CUDA(cudaEventCreate(&p->ev0));
-  SPCP_CUDA(cudaEventCreate(&p->ev1));
+  for (int i = 0; i < spcp_problem::kEvRing; ++i) {
+    SPCP_CUDA(cudaEventCreate(&p->ev0[i]));
+    SPCP_CUDA(cudaEventCreate(&p->ev1[i]));
+  }
   *out = p;
   return SPCP_OK;
 }
@@ -987,8 +1011,10 @@ int spcp_problem_destroy(spcp_problem* p) {
                     &p->scal, &p->gu_tmp, &p->vec_part, &p->small})
     b->release();
   if (p->host_out) cudaFreeHost(p->host_out);
-  if (p->ev0) cudaEventDestroy(p->ev0);
-  if (p->ev1) cudaEventDestroy(p->ev1);
+  for (int i = 0; i < spcp_problem::kEvRing; ++i) {
+    if (p->ev0[i]) cudaEventDestroy(p->ev0[i]);
+    if (p->ev1[i]) cudaEventDestroy(p->ev1[i]);
+  }
   delete p;
   return SPCP_OK;
 }
@@ -1019,7 +1045,6 @@ static int eval_impl(spcp_problem* p, int64_t k, int dtype, const double* z, con
   if ((rc = run_stream_eval(p, k, dtype, z, dz, alpha, kp, sh, pdt))) return rc;
   const bool dense = (kp == 0);
   if (dense) kp = int(round_up(k, 2));
-  p->ev_pending = p->prof && !dense;
   return run_reduce(p, k, kp, pdt, sh, dense, z, dz, alpha, u_mode, 1, nullptr, gu_part,
                     nullptr, scal, g_out);
 }
@@ -1030,6 +1055,17 @@ int spcp_eval(spcp_problem* p, int64_t k, int dtype, const double* z, const doub
   int rc = eval_impl(p, k, dtype, z, dz, alpha, g_out, U_FULL, nullptr, nullptr);
   if (rc) return rc;
   return fetch_out(p, out);
+}
+
+int spcp_eval_async(spcp_problem* p, int64_t k, int dtype, const double* z, const double* dz,
+                    double alpha, double* g_out, double* out_dev) {
+  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
+  int rc = eval_impl(p, k, dtype, z, dz, alpha, g_out, U_FULL, nullptr, nullptr);
+  if (rc) return rc;
+  if (out_dev)
+    SPCP_CUDA(cudaMemcpyAsync(out_dev, p->out_dev.ptr, 8 * sizeof(double),
+                              cudaMemcpyDeviceToDevice, p->stream));
+  return SPCP_OK;
 }
 
 int spcp_eval_partial(spcp_problem* p, int64_t k, int dtype, const double* z, const double* dz,
@@ -1398,15 +1434,17 @@ int spcp_matmul_small(spcp_problem* p, int64_t rows, int64_t pa, const double* a
 
 int spcp_prof_enable(spcp_problem* p, int on) {
   if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
+  if (p->ev_count) cudaStreamSynchronize(p->stream);
   p->prof = on != 0;
   p->prof_ms = 0.0;
   p->prof_count = 0;
-  p->ev_pending = false;
+  p->ev_count = 0;
   return SPCP_OK;
 }
 
 int spcp_prof_read(spcp_problem* p, double* ms_total, int64_t* launches, int64_t* kernels) {
   if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
+  if (p->ev_count && prof_collect(p)) return SPCP_ERR_CUDA;
   *ms_total = p->prof_ms;
   *launches = p->prof_count;
   *kernels = p->launches;

@@ -352,7 +352,7 @@ __device__ __noinline__ void tc_reduction_issuer(unsigned char* sm, TcBarriers* 
       });
     }
     if (ROLE != 2) mma_commit(&bar->gt_full[gtb]);
-    if (C::KC) mma_commit(&bar->gs_empty[b]);  // the G image is G^T U's operand only
+    if (C::KC && ROLE != 2) mma_commit(&bar->gs_empty[b]);  // the G image: G^T U's operand only
     TC_TS(t, ROLE == 2 ? 29 : 25);
     const uint64_t dVn = dVn0 + uint64_t(st * (C::V_BYTES >> 4));
     const uint32_t gv = tm + C::T_GV + gvb * C::GVW;
@@ -379,7 +379,7 @@ __device__ __noinline__ void tc_reduction_issuer(unsigned char* sm, TcBarriers* 
       });
     }
     if (!C::KC) mma_commit(&bar->gs_empty[b]);  // per tile parity (see the epilogue's wait)
-    else mma_commit(&bar->s_empty[t % C::NSB]);  // S / G columns free for the residual
+    else if (ROLE != 1) mma_commit(&bar->s_empty[t % C::NSB]);  // S / G columns: residual's
     if (ROLE != 1) mma_commit(&bar->v_empty[st]);
     if (un.flags & TCU_LAST_OF_RUN) {
       if (ROLE != 1) mma_commit(&bar->gv_full[gvb]);
@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK, SEG>::NTHREADS, 1)
       mbar_init(&bar->u_full[i], 1);
       mbar_init(&bar->u_empty[i], 2);  // residual + G^T U issuers
       mbar_init(&bar->g_full[i], C::NEG);
-      mbar_init(&bar->gs_empty[i], C::SPLIT_RED ? 2 : 1);
+      mbar_init(&bar->gs_empty[i], (C::SPLIT_RED && !C::KC) ? 2 : 1);
       mbar_init(&bar->gv_full[i], 1);
       mbar_init(&bar->gv_empty[i], C::NEG);
     }
@@ -977,28 +977,31 @@ __global__ void tc_images_kc_kernel(const double* __restrict__ z, const double* 
     sc->gt_unscale = scl.gt_unscale;
     sc->phi_unscale = scl.phi_unscale;
   }
-  const int64_t total = (m_pad + n_pad) * NE;
+  // one thread per (row, rank index c < SEG): the split is computed once and
+  // written to its three segments; the threads also clear the padding entries
+  const int64_t total = (m_pad + n_pad) * SEG;
   for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < total;
        q += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t row = q / NE;
-    const int e = int(q % NE);
-    const int seg = e / SEG, c = e % SEG;
+    const int64_t row = q / SEG;
+    const int c = int(q % SEG);
     const bool is_u = row < m_pad;
     const int64_t r = is_u ? row : row - m_pad;
     double w = 0.0;
-    if (seg < 3 && c < k && r < (is_u ? m : n)) {
+    if (c < k && r < (is_u ? m : n)) {
       const int64_t o = (is_u ? 0 : m * k) + r * k + c;
       w = z[o] + (dz ? alpha * dz[o] : 0.0);
       w = is_u ? -w * su : w * sv;
     }
     const __half hh = __double2half(w);
     const __half lo = __double2half(w - double(__half2float(hh)));
-    // U: segments (h, h, m); V: (h, m, h)
-    const bool take_lo = is_u ? (seg == 2) : (seg == 1);
-    const __half val = take_lo ? lo : hh;
     unsigned char* base = is_u ? u_img + (r >> 7) * (128 * RB) : v_img + (r >> 6) * (64 * RB);
     const int rr = int(is_u ? (r & 127) : (r & 63));
-    *reinterpret_cast<__half*>(base + tc::Swz<RB>::offset(rr, e * 2)) = val;
+    // U: segments (h, h, m); V: (h, m, h)
+    *reinterpret_cast<__half*>(base + tc::Swz<RB>::offset(rr, c * 2)) = hh;
+    *reinterpret_cast<__half*>(base + tc::Swz<RB>::offset(rr, (SEG + c) * 2)) = is_u ? hh : lo;
+    *reinterpret_cast<__half*>(base + tc::Swz<RB>::offset(rr, (2 * SEG + c) * 2)) = is_u ? lo : hh;
+    for (int e = 3 * SEG + c; e < NE; e += SEG)
+      *reinterpret_cast<__half*>(base + tc::Swz<RB>::offset(rr, e * 2)) = __half(0.f);
   }
 }
 

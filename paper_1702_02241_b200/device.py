@@ -150,6 +150,12 @@ class DeviceProblem:
                             dptr(g_out), self._out))
         return np.frombuffer(self._out, dtype=np.float64).copy()
 
+    def eval_async(self, k, dtype, z, dz, alpha, g_out, out_dev=None):
+        """Stream-ordered eval: the scalars stay on the device (out_dev, float64[8])
+        and nothing synchronises."""
+        check(lib.spcp_eval_async(self.h, int(k), int(dtype), dptr(z), dptr(dz), float(alpha),
+                                  dptr(g_out), dptr(out_dev)))
+
     def eval_partial(self, k, dtype, z, dz, alpha, gu_part, scal, g_out):
         check(lib.spcp_eval_partial(self.h, int(k), int(dtype), dptr(z), dptr(dz),
                                     float(alpha), dptr(gu_part), dptr(scal), dptr(g_out)))

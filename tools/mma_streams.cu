@@ -50,9 +50,10 @@ __device__ __forceinline__ void red_tile(uint32_t tm, uint32_t base, int t, uint
   mma_commit(bar + 2);
 }
 
-__global__ void __launch_bounds__(64) streams(int mode, int iters, long long* out) {
+__global__ void __launch_bounds__(640) streams(int mode, int iters, int bg, const float* gsrc, long long* out) {
   extern __shared__ __align__(1024) unsigned char sm[];
-  __shared__ uint64_t bar[2], dummy[8];
+  __shared__ uint64_t bar[2], dummy[8], ring_full[3];
+  __shared__ volatile int stop;
   __shared__ uint32_t tbase;
   const int warp = threadIdx.x / 32;
   for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x3c003c00u;
@@ -61,6 +62,8 @@ __global__ void __launch_bounds__(64) streams(int mode, int iters, long long* ou
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     for (int i = 0; i < 8; ++i) mbar_init(&dummy[i], 1 << 19);
+    for (int i = 0; i < 3; ++i) mbar_init(&ring_full[i], 1);
+    stop = 0;
     fence_barrier_init();
   }
   fence_proxy_async_smem();
@@ -86,6 +89,37 @@ __global__ void __launch_bounds__(64) streams(int mode, int iters, long long* ou
     mbar_wait(&bar[warp], 0);
     out[warp] = (clock64() - t0) / iters;
   }
+  if (warp < 2) {
+    __syncwarp();
+    named_bar_sync(1, 64);
+    if (threadIdx.x == 0) stop = 1;
+  } else if (warp == 2 && (bg & 1)) {
+    // bulk copies global -> smem (HBM stream like the X producer): 3 x 32 KB ring
+    if ((threadIdx.x & 31) == 0) {
+      size_t off = size_t(blockIdx.x) * 32768;
+      int i = 0;
+      for (; !stop; ++i) {
+        const int s2 = i % 3;
+        if (i >= 3) mbar_wait(&ring_full[s2], ((i / 3) - 1) & 1);
+        mbar_arrive_expect_tx(&ring_full[s2], 32768);
+        bulk_load(sm + 65536 + s2 * 32768, gsrc + off / 4, 32768, &ring_full[s2]);
+        off = (off + 148 * 32768) % (size_t(1) << 30);
+      }
+      for (int j = i - 3 < 0 ? 0 : i - 3; j < i; ++j) mbar_wait(&ring_full[j % 3], (j / 3) & 1);
+    }
+  } else if (warp >= 4 && (bg & 2)) {
+    // epilogue-like TMEM reads (tcgen05.ld 32x32b.x16, columns 448..511)
+    uint32_t acc = 0;
+    const uint32_t la = uint32_t(32 * (warp & 3)) << 16;
+    while (!stop) {
+      uint32_t r[16];
+      tmem_ld16(tm + la + 448 + 16 * (warp & 3), r);
+      tmem_wait_ld();
+      acc += r[0] ^ r[15];
+    }
+    if (acc == 12345) out[7] = acc;
+  }
+
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc(tm, 512);
@@ -94,18 +128,22 @@ __global__ void __launch_bounds__(64) streams(int mode, int iters, long long* ou
 int main() {
   long long* d;
   cudaMalloc(&d, 8 * sizeof(long long));
-  const int smem = 64 * 1024 + 1024;
+  const int smem = 64 * 1024 + 3 * 32768 + 1024;
   cudaFuncSetAttribute(streams, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  float* gsrc;
+  cudaMalloc(&gsrc, size_t(1) << 30);
+  cudaMemset(gsrc, 0, size_t(1) << 30);
   const char* nm[4] = {"residual stream alone", "reduction stream alone", "both streams (2 warps)",
                        "one warp, tile order"};
-  for (int mode = 0; mode < 4; ++mode) {
+  for (int bg = 0; bg < 4; ++bg)
+  for (int mode = 2; mode < 4; ++mode) {
     cudaMemset(d, 0, 64);
-    streams<<<1, 64, smem>>>(mode, 300, d);
+    streams<<<148, 640, smem>>>(mode, 300, bg, gsrc, d);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
     long long h[2];
     cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
-    printf("%-26s warp0 %6lld  warp1 %6lld cycles per tile\n", nm[mode], h[0], h[1]);
+    printf("bg=%d (1 bulk HBM, 2 tcgen05.ld) %-26s warp0 %6lld  warp1 %6lld cycles per tile\n", bg, nm[mode], h[0], h[1]);
   }
   return 0;
 }
