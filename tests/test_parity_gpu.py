@@ -89,6 +89,9 @@ SHAPES = [  # m, n, k, masked — multiple tiles / chunks / bands, ragged edges
     (1500, 900, 50, False),
     (640, 520, 64, True),
     (400, 350, 70, False),  # beyond the fused widths: dense fallback
+    (900, 700, 5, True),    # K-concatenated images, SEG = 8 (two K-steps)
+    (700, 1100, 16, False),  # SEG = 16
+    (5000, 260, 12, True),  # SEG = 12, tall-skinny (C3 shape class)
 ]
 
 
