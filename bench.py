@@ -67,9 +67,10 @@ class ClockSampler:
     in-process every 5 ms (the timed region is ~0.1 s), nvidia-smi as fallback."""
 
     def __init__(self):
-        self.samples = []  # (sm_mhz, max_mhz, reasons)
+        self.samples = []  # (time, sm_mhz, max_mhz, reasons)
         self._stop = threading.Event()
         self._t = None
+        self.window = (None, None)  # perf_counter bounds of the timed region
 
     def start(self):
         def run_nvml(pynvml, h):
@@ -80,7 +81,7 @@ class ClockSampler:
                 try:
                     sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
                     r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                    self.samples.append((float(sm), float(mx),
+                    self.samples.append((time.perf_counter(), float(sm), float(mx),
                                          [n for n, b in bits.items() if r & b]))
                 except Exception:
                     pass
@@ -97,7 +98,7 @@ class ClockSampler:
                                           "-i", os.environ.get("LOCAL_RANK", "0")],
                                          capture_output=True, text=True, timeout=5).stdout
                     parts = [x.strip() for x in out.strip().split(",")]
-                    self.samples.append((float(parts[0]), float(parts[1]),
+                    self.samples.append((time.perf_counter(), float(parts[0]), float(parts[1]),
                                          [n for n, v in zip(names, parts[2:6])
                                           if v.lower().startswith("active")]))
                 except Exception:
@@ -114,13 +115,22 @@ class ClockSampler:
         self._t = threading.Thread(target=target, args=args, daemon=True)
         self._t.start()
 
+    def mark(self, begin):
+        t = time.perf_counter()
+        self.window = (t, None) if begin else (self.window[0], t)
+
     def stop(self):
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
-        sm = [x[0] for x in self.samples]
-        mx = self.samples[-1][1] if self.samples else None
-        reasons = sorted({r for x in self.samples for r in x[2]})
+        t0, t1 = self.window
+        inside = [x for x in self.samples
+                  if (t0 is None or x[0] >= t0) and (t1 is None or x[0] <= t1)]
+        if not inside and self.samples:  # region shorter than the sampling period
+            inside = [min(self.samples, key=lambda x: abs(x[0] - (t0 or 0.0)))]
+        sm = [x[1] for x in inside]
+        mx = inside[-1][2] if inside else None
+        reasons = sorted({r for x in inside for r in x[3]})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
                 "sm_mhz_min": float(np.min(sm)) if sm else None,
                 "reasons": reasons, "samples": len(sm)}
@@ -221,21 +231,23 @@ def run_b200(args, rank, world):
             # synchronous call, with its host round trip, is what e2e times)
             dp.eval_async(K, SPCP_F32, z, dz, 1e-3 * (i + 1), g, out_dev)
 
+    clocks = ClockSampler()
+    clocks.start()  # NVML up before the timed region; samples kept only inside it
     for i in range(args.warmup):
         step(i)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     dp.prof_enable(True)
-    clocks = ClockSampler()
-    clocks.start()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    clocks.mark(True)
     ev0.record(dp.stream)
     for i in range(args.steps):
         step(i)
     ev1.record(dp.stream)
     torch.cuda.synchronize()
+    clocks.mark(False)
     clk = clocks.stop()
     ms_total = ev0.elapsed_time(ev1)
     k1_ms, k1_count, launches = dp.prof_read()

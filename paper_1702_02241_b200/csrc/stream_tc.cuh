@@ -231,6 +231,16 @@ static_assert(sizeof(TcUnit) == 16, "TcUnit is read as one uint4");
   } while (0)
 #endif
 
+// tcgen05.commit from a single lane (legacy issuers) or elected from the whole
+// warp (K-concatenated issuers, which run warp-wide)
+template <bool WARP>
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  if constexpr (WARP)
+    tc::mma_commit_w(bar);
+  else
+    tc::mma_commit(bar);
+}
+
 // Residual MMA issuer (one lane of warp 1): its own function, so ptxas
 // allocates it apart from the epilogue and keeps the descriptors uniform.
 template <int KP16, bool MASK, int SEG>
@@ -270,10 +280,8 @@ __device__ __noinline__ void tc_residual_issuer(unsigned char* sm, TcBarriers* b
       const uint32_t dt = tm + C::T_S + b * 64;
       if constexpr (C::KC) {
         // one K-sum over the concatenated segments: [uh|uh|um] . [vh|vm|vh]
-        static_for<C::NKS>([&](auto I) {
-          constexpr int o = (I * 32) >> 4;
-          mma_ss_1<o, o>(dt, da, db, ID_RES, I != 0);
-        });
+        // (warp-wide batch: one elect, descriptors stepped by 32 B)
+        mma_ss_batch<C::NKS, 2, 2>(dt, da, db, ID_RES, 0u);
       } else {
         static_for<3 * KS>([&](auto I) {
           constexpr int q = I / KS, ks = I % KS;
@@ -283,9 +291,9 @@ __device__ __noinline__ void tc_residual_issuer(unsigned char* sm, TcBarriers* b
         });
       }
     }
-    mma_commit(&bar->s_full[b]);
-    mma_commit(&bar->v_empty[st]);
-    if (un.flags & TCU_LAST_OF_RUN) mma_commit(&bar->u_empty[ubuf]);
+    tc_commit<C::KC>(&bar->s_full[b]);
+    tc_commit<C::KC>(&bar->v_empty[st]);
+    if (un.flags & TCU_LAST_OF_RUN) tc_commit<C::KC>(&bar->u_empty[ubuf]);
     TC_TS(t, 24);
   }
 }
@@ -333,7 +341,10 @@ __device__ __noinline__ void tc_reduction_issuer(unsigned char* sm, TcBarriers* 
     const uint64_t dUn = dUn0 + uint64_t(ubuf * (C::U_BYTES >> 4));
     const uint64_t goff = uint64_t((C::GB == 1 ? 0 : b) * (C::G_BYTES >> 4));
     const uint32_t gt = tm + C::T_GT + gtb * C::GTW;
-    if (ROLE != 2 && do_mma && !(p.debug & 16)) {
+    if (C::KC && ROLE != 2 && do_mma && !(p.debug & 16)) {
+      // stacked [gh; gl]^T U: 8 K-steps of 16 tile rows (A += 2048 B, B += 16 RB)
+      mma_ss_batch<8, 128, C::RB>(gt, dGm + goff, dUn, ID_GT, 0u);
+    } else if (ROLE != 2 && do_mma && !(p.debug & 16)) {
       static_for<8>([&](auto I) {
         constexpr int ks = I;
         constexpr int uo = (ks * 16 * C::RB) >> 4, go = (2048 * ks) >> 4;
@@ -351,12 +362,14 @@ __device__ __noinline__ void tc_reduction_issuer(unsigned char* sm, TcBarriers* 
         }
       });
     }
-    if (ROLE != 2) mma_commit(&bar->gt_full[gtb]);
-    if (C::KC && ROLE != 2) mma_commit(&bar->gs_empty[b]);  // the G image: G^T U's operand only
+    if (ROLE != 2) tc_commit<C::KC>(&bar->gt_full[gtb]);
+    if (C::KC && ROLE != 2) tc_commit<C::KC>(&bar->gs_empty[b]);  // G image: G^T U's operand only
     TC_TS(t, ROLE == 2 ? 29 : 25);
     const uint64_t dVn = dVn0 + uint64_t(st * (C::V_BYTES >> 4));
     const uint32_t gv = tm + C::T_GV + gvb * C::GVW;
-    if (ROLE != 1 && do_mma && !(p.debug & 32)) {
+    if (C::KC && ROLE != 1 && do_mma && !(p.debug & 32)) {
+      mma_gv_ts_batch<C::RB>(gv, tm + C::T_S + (t % C::NSB) * 64, dVn, ID_GV, first ? 0u : 1u);
+    } else if (ROLE != 1 && do_mma && !(p.debug & 32)) {
       static_for<4>([&](auto I) {
         constexpr int ks = I;
         constexpr int vo = (ks * 16 * C::RB) >> 4;
@@ -379,11 +392,11 @@ __device__ __noinline__ void tc_reduction_issuer(unsigned char* sm, TcBarriers* 
       });
     }
     if (!C::KC) mma_commit(&bar->gs_empty[b]);  // per tile parity (see the epilogue's wait)
-    else if (ROLE != 1) mma_commit(&bar->s_empty[t % C::NSB]);  // S / G columns: residual's
-    if (ROLE != 1) mma_commit(&bar->v_empty[st]);
+    else if (ROLE != 1) tc_commit<C::KC>(&bar->s_empty[t % C::NSB]);  // S / G columns
+    if (ROLE != 1) tc_commit<C::KC>(&bar->v_empty[st]);
     if (un.flags & TCU_LAST_OF_RUN) {
-      if (ROLE != 1) mma_commit(&bar->gv_full[gvb]);
-      if (ROLE != 2) mma_commit(&bar->u_empty[ubuf]);
+      if (ROLE != 1) tc_commit<C::KC>(&bar->gv_full[gvb]);
+      if (ROLE != 2) tc_commit<C::KC>(&bar->u_empty[ubuf]);
     }
     TC_TS(t, ROLE == 2 ? 30 : 15);
   }
@@ -535,15 +548,8 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK, SEG>::NTHREADS, 1)
     // then G.V) of each tile once its G is staged.  Base descriptors are built
     // once; every MMA adds a compile-time offset (descriptor address field =
     // byte address >> 4, no carry for shared memory).
-    if (lane == 0) {
-      constexpr uint32_t ID_RES = idesc_f16(128, 64, false, false);
-      constexpr uint32_t ID_GV = idesc_f16(128, C::GVC * KP16, false, true);
-      constexpr uint32_t ID_GT = idesc_f16(64, C::GCAT * KP16, true, true);
-      constexpr int KS = KP16 / 16;
-      const bool do_mma = !(p.debug & 8);
-      const uint32_t u0 = smem_u32(sm + C::OFF_U), v0 = smem_u32(sm + C::OFF_V);
-      const uint32_t g0 = smem_u32(sm + C::OFF_G);
-      TcUnit un_next = T > 0 ? units[0] : TcUnit{};
+    // (K-concatenated layout: the whole warp runs the issuer, one elect per batch)
+    if (C::KC || lane == 0) {
       if (warp == 1)
         tc_residual_issuer<KP16, MASK, SEG>(sm, bar, units, T, run0, tm, p);
       else if (!C::SPLIT_RED)

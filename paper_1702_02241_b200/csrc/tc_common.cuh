@@ -494,6 +494,64 @@ __device__ __forceinline__ void mma_gv_batch2(uint32_t d, uint32_t a_tmem, uint6
       ::"r"(d), "r"(a_tmem), "l"(b0), "r"(idesc), "r"(acc_first), "n"(SBK) : "memory");
 }
 
+// ---- warp-wide batches for the K-concatenated kernel: the whole (converged)
+// warp executes ONE asm block, one elect.sync, N MMAs with the descriptors
+// stepped by immediates (no per-MMA waterfall loop around a single lane).
+#define SPCP_SSB(ACC) "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, " ACC ";\n"
+#define SPCP_SSB_STEP "add.s64 a, a, %5;\nadd.s64 b, b, %6;\n"
+template <int N, int SA, int SB>
+__device__ __forceinline__ void mma_ss_batch(uint32_t d, uint64_t a0, uint64_t b0, uint32_t idesc,
+                                             uint32_t acc0) {
+  static_assert(N >= 1 && N <= 8, "batch size");
+#define SPCP_SSB_HEAD                                                                       \
+  "{\n.reg .pred e, p0, pt;\n.reg .b32 r;\n.reg .b64 a, b;\n"                               \
+  "setp.ne.b32 p0, %4, 0;\nsetp.eq.b32 pt, 0, 0;\nelect.sync r|e, 0xffffffff;\n"            \
+  "mov.b64 a, %1;\nmov.b64 b, %2;\n" SPCP_SSB("p0")
+#define SPCP_SSB_ARGS \
+  ::"r"(d), "l"(a0), "l"(b0), "r"(idesc), "r"(acc0), "n"(SA), "n"(SB) : "memory"
+  if constexpr (N == 1) {
+    asm volatile(SPCP_SSB_HEAD "}\n" SPCP_SSB_ARGS);
+  } else if constexpr (N == 2) {
+    asm volatile(SPCP_SSB_HEAD SPCP_SSB_STEP SPCP_SSB("pt") "}\n" SPCP_SSB_ARGS);
+  } else if constexpr (N == 3) {
+    asm volatile(SPCP_SSB_HEAD SPCP_SSB_STEP SPCP_SSB("pt") SPCP_SSB_STEP SPCP_SSB("pt") "}\n"
+                 SPCP_SSB_ARGS);
+  } else if constexpr (N == 4) {
+    asm volatile(SPCP_SSB_HEAD SPCP_SSB_STEP SPCP_SSB("pt") SPCP_SSB_STEP SPCP_SSB("pt")
+                     SPCP_SSB_STEP SPCP_SSB("pt") "}\n" SPCP_SSB_ARGS);
+  } else {
+    static_assert(N == 8, "batch size 1-4 or 8");
+    asm volatile(SPCP_SSB_HEAD SPCP_SSB_STEP SPCP_SSB("pt") SPCP_SSB_STEP SPCP_SSB("pt")
+                     SPCP_SSB_STEP SPCP_SSB("pt") SPCP_SSB_STEP SPCP_SSB("pt") SPCP_SSB_STEP
+                         SPCP_SSB("pt") SPCP_SSB_STEP SPCP_SSB("pt") SPCP_SSB_STEP SPCP_SSB("pt")
+                             "}\n" SPCP_SSB_ARGS);
+  }
+#undef SPCP_SSB_HEAD
+#undef SPCP_SSB_ARGS
+}
+
+// G.V with A = G from TMEM over the tile's S columns (per 32-column half: gh at
+// +0, gl at +16; K-step ks covers columns 32 (ks / 2) + 8 (ks % 2)), B = V
+// image stepped by SB per K-step: 4 K-steps x {gh, gl} = 8 TS MMAs.
+#define SPCP_TSB(ACC) "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t], b, %3, " ACC ";\n"
+template <int SB>
+__device__ __forceinline__ void mma_gv_ts_batch(uint32_t d, uint32_t s_tmem, uint64_t b0,
+                                                uint32_t idesc, uint32_t acc0) {
+  asm volatile(
+      "{\n.reg .pred e, p0, pt;\n.reg .b32 r, t;\n.reg .b64 b;\n"
+      "setp.ne.b32 p0, %4, 0;\nsetp.eq.b32 pt, 0, 0;\nelect.sync r|e, 0xffffffff;\n"
+      "mov.b64 b, %2;\n"
+      "add.s32 t, %1, 0;\n" SPCP_TSB("p0") "add.s32 t, %1, 16;\n" SPCP_TSB("pt")
+      "add.s64 b, b, %5;\n"
+      "add.s32 t, %1, 8;\n" SPCP_TSB("pt") "add.s32 t, %1, 24;\n" SPCP_TSB("pt")
+      "add.s64 b, b, %5;\n"
+      "add.s32 t, %1, 32;\n" SPCP_TSB("pt") "add.s32 t, %1, 48;\n" SPCP_TSB("pt")
+      "add.s64 b, b, %5;\n"
+      "add.s32 t, %1, 40;\n" SPCP_TSB("pt") "add.s32 t, %1, 56;\n" SPCP_TSB("pt") "}\n"
+      ::"r"(d), "r"(s_tmem), "l"(b0), "r"(idesc), "r"(acc0), "n"(SB) : "memory");
+}
+#undef SPCP_TSB
+
 __device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
   asm volatile(
       "{\n.reg .pred e;\n.reg .b32 r;\nelect.sync r|e, 0xffffffff;\n"
