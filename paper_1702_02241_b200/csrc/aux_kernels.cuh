@@ -144,6 +144,7 @@ struct ReduceParams {
   const int32_t* csr_v_idx;
   int kst;                  // partial row stride (the kernel's padded rank)
   int gt_rows;              // G^T.U slot rows: 64, or 128 = [gh part; gl part] (summed here)
+  int chunked;              // slots laid out [kst / 4][rows][4] (K-concatenated kernel)
   const float* tc_unscale;  // [0]: G.V partials, [1]: G^T.U partials
 };
 
@@ -299,13 +300,17 @@ __global__ void __launch_bounds__(256) tc_reduce_kernel(const ReduceParams p) {
   for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < nu4 + nv4; q += stride) {
     const bool is_u = q < nu4;
     const int64_t qq = is_u ? q : q - nu4;
-    const int64_t r = qq / c4n;
-    const int c0 = int(qq % c4n) * 4;
+    // chunked slots: consecutive threads take consecutive rows of one 4-column
+    // chunk (contiguous float4 reads); row-major slots: consecutive chunks of a row
+    const int64_t rows = is_u ? p.m : p.n;
+    const int64_t r = p.chunked ? qq % rows : qq / c4n;
+    const int c0 = int(p.chunked ? qq / rows : qq % c4n) * 4;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     if (is_u) {
       const int sb = int(r >> 7);
       const int e0 = p.csr_u_off[sb], e1 = p.csr_u_off[sb + 1];
-      const float* base = plf + (r & 127) * p.kst + c0;
+      const float* base = p.chunked ? plf + (int64_t(c0 >> 2) * 128 + (r & 127)) * 4
+                                    : plf + (r & 127) * p.kst + c0;
       const int64_t sst = int64_t(128) * p.kst;
       int e = e0;
       for (; e + 4 <= e1; e += 4) {
@@ -326,8 +331,10 @@ __global__ void __launch_bounds__(256) tc_reduce_kernel(const ReduceParams p) {
     } else {
       const int tcol = int(r >> 6);
       const int e0 = p.csr_v_off[tcol], e1 = p.csr_v_off[tcol + 1];
-      const float* base = prf + (r & 63) * p.kst + c0;
-      const int64_t sst = int64_t(p.gt_rows) * p.kst, hoff = int64_t(64) * p.kst;
+      const float* base = p.chunked ? prf + (int64_t(c0 >> 2) * p.gt_rows + (r & 63)) * 4
+                                    : prf + (r & 63) * p.kst + c0;
+      const int64_t sst = int64_t(p.gt_rows) * p.kst;
+      const int64_t hoff = p.chunked ? int64_t(64) * 4 : int64_t(64) * p.kst;
       const bool two = p.gt_rows == 128;
       int e = e0;
       for (; e + 2 <= e1; e += 2) {

@@ -125,6 +125,7 @@ struct LaunchShape {
   int tc = 0;  // partials in the tensor-core (CSR slot) layout
   int kst = 0;
   int gt_rows = 64;
+  int chunked = 0;
 };
 
 static int prof_fold(spcp_problem* p, int n);
@@ -579,6 +580,7 @@ static int tc_eval(spcp_problem* p, int64_t k, const double* z, const double* dz
     sh.tc = 1;
     sh.kst = kst;
     sh.gt_rows = 128;
+    sh.chunked = 1;
     sh.nchunks = 1;
     sh.nrb = 1;
     sh.chunk_cols = p->tc_grid;
@@ -832,6 +834,7 @@ static int run_reduce(spcp_problem* p, int64_t k, int kp, int part_dtype, const 
     rp.csr_v_idx = csr + p->tc_csr_v_idx;
     rp.kst = sh.kst;
     rp.gt_rows = sh.gt_rows;
+    rp.chunked = sh.chunked;
     rp.tc_unscale = &p->tc_scales.as<TcScales>()->gv_unscale;
   }
   if (sh.tc && (u_mode == U_FULL || u_mode == U_PARTIAL) && v_mode)
