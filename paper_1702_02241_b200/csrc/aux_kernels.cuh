@@ -288,19 +288,29 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p) {
 // and summed in fp64 in the CSR's fixed order (deterministic).  U side:
 // U_FULL or U_PARTIAL; V side always.
 __global__ void __launch_bounds__(256) tc_reduce_kernel(const ReduceParams p) {
+  // Four lanes per output item (row r, 4 columns): lane j sums the CSR sources
+  // e = j, j + 4, ... of the item (all its loads in flight at once), then the
+  // four partial sums are combined in a fixed order ((l0 + l1) + (l2 + l3)).
   __shared__ double scratch[32];
   __shared__ bool am_last;
   const int c4n = p.kst >> 2;
   const int64_t nu4 = p.m * c4n, nv4 = p.n * c4n;
   double s[6] = {0, 0, 0, 0, 0, 0};
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const int j = threadIdx.x & 3;
+  const int64_t stride = (int64_t(gridDim.x) * blockDim.x) >> 2;  // items per sweep
+  const int64_t gtid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   const float* plf = reinterpret_cast<const float*>(p.pleft);
   const float* prf = reinterpret_cast<const float*>(p.pright);
   const float gvs = p.tc_unscale[0], gts = p.tc_unscale[1];
-  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < nu4 + nv4; q += stride) {
+  const int64_t n_items = nu4 + nv4;
+  // warp-uniform trip count: a warp's 8 items start at (gtid >> 5) * 8
+  for (int64_t w0 = (gtid >> 5) * 8; w0 < n_items; w0 += stride) {
+    const int64_t q0 = w0 + ((threadIdx.x & 31) >> 2);
+    const bool live = q0 < n_items;  // dead lanes still join the shuffles
+    const int64_t q = live ? q0 : 0;
     const bool is_u = q < nu4;
     const int64_t qq = is_u ? q : q - nu4;
-    // chunked slots: consecutive threads take consecutive rows of one 4-column
+    // chunked slots: consecutive items take consecutive rows of one 4-column
     // chunk (contiguous float4 reads); row-major slots: consecutive chunks of a row
     const int64_t rows = is_u ? p.m : p.n;
     const int64_t r = p.chunked ? qq % rows : qq / c4n;
@@ -312,22 +322,22 @@ __global__ void __launch_bounds__(256) tc_reduce_kernel(const ReduceParams p) {
       const float* base = p.chunked ? plf + (int64_t(c0 >> 2) * 128 + (r & 127)) * 4
                                     : plf + (r & 127) * p.kst + c0;
       const int64_t sst = int64_t(128) * p.kst;
-      int e = e0;
-      for (; e + 4 <= e1; e += 4) {
-        const float4 v0 = *reinterpret_cast<const float4*>(base + p.csr_u_idx[e] * sst);
-        const float4 v1 = *reinterpret_cast<const float4*>(base + p.csr_u_idx[e + 1] * sst);
-        const float4 v2 = *reinterpret_cast<const float4*>(base + p.csr_u_idx[e + 2] * sst);
-        const float4 v3 = *reinterpret_cast<const float4*>(base + p.csr_u_idx[e + 3] * sst);
-        a0 += v0.x; a1 += v0.y; a2 += v0.z; a3 += v0.w;
-        a0 += v1.x; a1 += v1.y; a2 += v1.z; a3 += v1.w;
-        a0 += v2.x; a1 += v2.y; a2 += v2.z; a3 += v2.w;
-        a0 += v3.x; a1 += v3.y; a2 += v3.z; a3 += v3.w;
+      // batches of 8 sources per lane: the 8 index loads, then the 8 data
+      // loads are all in flight before the (in-order) adds
+      for (int eb = e0 + j; eb < e1; eb += 32) {
+        int idx[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) idx[u] = (eb + 4 * u < e1) ? __ldg(p.csr_u_idx + eb + 4 * u) : -1;
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          v[u] = idx[u] >= 0 ? *reinterpret_cast<const float4*>(base + idx[u] * sst)
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          a0 += v[u].x; a1 += v[u].y; a2 += v[u].z; a3 += v[u].w;
+        }
       }
-      for (; e < e1; ++e) {
-        const float4 v0 = *reinterpret_cast<const float4*>(base + p.csr_u_idx[e] * sst);
-        a0 += v0.x; a1 += v0.y; a2 += v0.z; a3 += v0.w;
-      }
-      a0 *= gvs; a1 *= gvs; a2 *= gvs; a3 *= gvs;
     } else {
       const int tcol = int(r >> 6);
       const int e0 = p.csr_v_off[tcol], e1 = p.csr_v_off[tcol + 1];
@@ -336,43 +346,50 @@ __global__ void __launch_bounds__(256) tc_reduce_kernel(const ReduceParams p) {
       const int64_t sst = int64_t(p.gt_rows) * p.kst;
       const int64_t hoff = p.chunked ? int64_t(64) * 4 : int64_t(64) * p.kst;
       const bool two = p.gt_rows == 128;
-      int e = e0;
-      for (; e + 2 <= e1; e += 2) {
-        const float* b0 = base + p.csr_v_idx[e] * sst;
-        const float* b1 = base + p.csr_v_idx[e + 1] * sst;
-        const float4 v0 = *reinterpret_cast<const float4*>(b0);
-        const float4 w0 = two ? *reinterpret_cast<const float4*>(b0 + hoff) : make_float4(0, 0, 0, 0);
-        const float4 v1 = *reinterpret_cast<const float4*>(b1);
-        const float4 w1 = two ? *reinterpret_cast<const float4*>(b1 + hoff) : make_float4(0, 0, 0, 0);
-        a0 += v0.x; a1 += v0.y; a2 += v0.z; a3 += v0.w;
-        a0 += w0.x; a1 += w0.y; a2 += w0.z; a3 += w0.w;
-        a0 += v1.x; a1 += v1.y; a2 += v1.z; a3 += v1.w;
-        a0 += w1.x; a1 += w1.y; a2 += w1.z; a3 += w1.w;
+      for (int eb = e0 + j; eb < e1; eb += 16) {
+        int idx[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) idx[u] = (eb + 4 * u < e1) ? __ldg(p.csr_v_idx + eb + 4 * u) : -1;
+        float4 v[4], w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float* b0 = base + (idx[u] >= 0 ? idx[u] : 0) * sst;
+          v[u] = idx[u] >= 0 ? *reinterpret_cast<const float4*>(b0) : make_float4(0.f, 0.f, 0.f, 0.f);
+          w[u] = (idx[u] >= 0 && two) ? *reinterpret_cast<const float4*>(b0 + hoff)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          a0 += v[u].x; a1 += v[u].y; a2 += v[u].z; a3 += v[u].w;
+          a0 += w[u].x; a1 += w[u].y; a2 += w[u].z; a3 += w[u].w;
+        }
       }
-      for (; e < e1; ++e) {
-        const float* b0 = base + p.csr_v_idx[e] * sst;
-        const float4 v0 = *reinterpret_cast<const float4*>(b0);
-        const float4 w0 = two ? *reinterpret_cast<const float4*>(b0 + hoff) : make_float4(0, 0, 0, 0);
-        a0 += v0.x; a1 += v0.y; a2 += v0.z; a3 += v0.w;
-        a0 += w0.x; a1 += w0.y; a2 += w0.z; a3 += w0.w;
-      }
-      a0 *= gts; a1 *= gts; a2 *= gts; a3 *= gts;
     }
-    const double acc[4] = {a0, a1, a2, a3};
+    // fixed-order combine of the four lanes
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+      a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+      a3 += __shfl_xor_sync(0xffffffffu, a3, o);
+    }
+    if (!live || j != 0) continue;
+    const double sc = is_u ? gvs : gts;
+    const double acc[4] = {a0 * sc, a1 * sc, a2 * sc, a3 * sc};
     const int64_t obase = (is_u ? 0 : p.m * p.k) + r * p.k;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int c = c0 + j;
+    for (int jj = 0; jj < 4; ++jj) {
+      const int c = c0 + jj;
       if (c >= p.k) break;
       const int64_t o = obase + c;
       if (is_u && p.u_mode == U_PARTIAL) {
-        reinterpret_cast<float*>(p.gu_part)[r * p.k + c] = float(acc[j]);
+        reinterpret_cast<float*>(p.gu_part)[r * p.k + c] = float(acc[jj]);
         continue;
       }
       double w = p.z[o];
       const double d = p.dz ? p.dz[o] : 0.0;
       w += p.alpha * d;
-      const double g = acc[j] + p.lambda_l * w;
+      const double g = acc[jj] + p.lambda_l * w;
       p.g_out[o] = g;
       const int sidx = is_u ? 0 : 3;
       s[sidx] += g * g;

@@ -611,6 +611,7 @@ static int tc_eval(spcp_problem* p, int64_t k, const double* z, const double* dz
   if (rc) return rc;
   sh.tc = 1;
   sh.kst = int(round_up(k, 4));
+  sh.chunked = 1;
   sh.nchunks = 1;
   sh.nrb = 1;
   sh.chunk_cols = p->tc_grid;  // phi partial count
@@ -837,8 +838,13 @@ static int run_reduce(spcp_problem* p, int64_t k, int kp, int part_dtype, const 
     rp.chunked = sh.chunked;
     rp.tc_unscale = &p->tc_scales.as<TcScales>()->gv_unscale;
   }
-  if (sh.tc && (u_mode == U_FULL || u_mode == U_PARTIAL) && v_mode)
-    tc_reduce_kernel<<<nblk, 256, 0, p->stream>>>(rp);
+  if (sh.tc && (u_mode == U_FULL || u_mode == U_PARTIAL) && v_mode) {
+    const int64_t items = (p->m + p->n) * (sh.kst / 4);  // 4 lanes per item
+    const int nb = int(std::min<int64_t>((items * 4 + 255) / 256, 148 * 8));
+    if ((rc = p->blk.ensure(size_t(nb) * 6 * sizeof(double)))) return rc;
+    rp.blk = p->blk.as<double>();  // (ensure may have grown the buffer)
+    tc_reduce_kernel<<<nb, 256, 0, p->stream>>>(rp);
+  }
   else if (part_dtype == SPCP_F32)
     reduce_kernel<float><<<nblk, 256, 0, p->stream>>>(rp);
   else

@@ -616,7 +616,8 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK, SEG>::NTHREADS, 1)
           });
         }
       } else if (!(p.debug & 1)) {
-        float* dst = p.pright + (size_t(u2.gt_slot) * 64 + 16 * q + lane) * kst + h * GTC;
+        // chunked slot [kst / 4][64 rows][4] (coalesced float4 stores)
+        float* dst = p.pright + size_t(u2.gt_slot) * 64 * kst + (16 * q + lane) * 4;
         const bool first = (u2.flags & TCU_FIRST_TOUCH) != 0;
         constexpr int CH = GTC < 16 ? GTC : 16;
 #pragma unroll
@@ -636,12 +637,13 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK, SEG>::NTHREADS, 1)
           if (lane < 16) {  // M = 64 accumulator: row j = 16 q + lane in lanes 0..15
 #pragma unroll
             for (int c = 0; c < CH; c += 4) {
-              if (h * GTC + c0 + c >= kst) continue;  // padded rank columns are not stored
+              const int cc = h * GTC + c0 + c;
+              if (cc >= kst) continue;  // padded rank columns are not stored
               if (first)
-                *reinterpret_cast<uint4*>(dst + c0 + c) =
+                *reinterpret_cast<uint4*>(dst + cc * 64) =
                     make_uint4(v[c], v[c + 1], v[c + 2], v[c + 3]);
               else
-                red_add_v4(dst + c0 + c, v[c], v[c + 1], v[c + 2], v[c + 3]);
+                red_add_v4(dst + cc * 64, v[c], v[c + 1], v[c + 2], v[c + 3]);
             }
           }
         }
@@ -679,7 +681,7 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK, SEG>::NTHREADS, 1)
           });
         }
       } else if (!(p.debug & 2)) {
-        float* dst = p.pleft + (size_t(u2.gv_slot) * 128 + row) * kst + h * GTC;
+        float* dst = p.pleft + size_t(u2.gv_slot) * 128 * kst + row * 4;  // [kst/4][128][4]
         constexpr int CH = GTC < 16 ? GTC : 16;
 #pragma unroll
         for (int c0 = 0; c0 < GTC; c0 += CH) {
@@ -698,7 +700,8 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK, SEG>::NTHREADS, 1)
 #pragma unroll
           for (int c = 0; c < CH; c += 4)
             if (h * GTC + c0 + c < kst)
-              *reinterpret_cast<uint4*>(dst + c0 + c) = make_uint4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+              *reinterpret_cast<uint4*>(dst + (h * GTC + c0 + c) * 128) =
+                  make_uint4(v[c], v[c + 1], v[c + 2], v[c + 3]);
         }
       }
       tc_fence_before();
