@@ -133,7 +133,8 @@ struct TcCfg {
   // halves side by side, summed at the drain; KC: the image segments
   static constexpr int GCAT = KP16 <= 32 ? 2 : 1;
   static constexpr int GVC = KP16 <= 32 ? 2 : 1;
-  static constexpr int GVW = KC ? NB : GVC * KP16;
+  // KC: G.V needs output columns [0, 2 SEG) only ([vh|vm] segments)
+  static constexpr int GVW = KC ? ((2 * SEG + 15) / 16) * 16 : GVC * KP16;
   static constexpr int GTW = KC ? NB : GCAT * KP16;
   // KC: the epilogue overwrites its S columns with G (fp16 pairs: gh at +0,
   // gl at +16 of each warp's 32 columns) and G.V reads A from TMEM; three S
@@ -143,7 +144,11 @@ struct TcCfg {
   static constexpr int NGT = KC ? 3 : 4;
   static constexpr uint32_t T_S = 0, T_GV = 64 * NSB;
   static constexpr uint32_t T_GT = T_GV + 2 * GVW;
-  static_assert(T_GT + NGT * GTW <= 512, "TMEM budget");
+  // KC: the run's U image also lives in TMEM (tcgen05.cp), so the residual is a
+  // TS MMA that reads only V from shared memory
+  static constexpr uint32_t T_U = T_GT + NGT * GTW;
+  static constexpr int U_COLS = KC ? RB / 4 : 0;
+  static_assert(T_U + U_COLS <= 512, "TMEM budget");
   static constexpr uint32_t TMEM_COLS = 512;
   static constexpr int NEPI = 16;  // epilogue warps: 2 groups x 4 quarters x 2 halves
   static constexpr int NEG = NEPI / 2;
@@ -265,6 +270,17 @@ __device__ __noinline__ void tc_residual_issuer(unsigned char* sm, TcBarriers* b
     if (run != prev_run) {
       mbar_wait(&bar->u_full[ubuf], (run / C::UB) & 1);
       prev_run = run;
+      if constexpr (C::KC) {
+        // U image -> TMEM (one copy per K-step); in issue order after the
+        // previous run's residual MMAs, which read the single TMEM copy
+        tc_fence_after();
+        const uint64_t du = dU_k + uint64_t(ubuf * (C::U_BYTES >> 4));
+        if (do_mma && !(p.debug & 64)) {
+          static_for<C::NKS>([&](auto I) {
+            tmem_cp_128x256b_w(tm + C::T_U + 8 * I, du + uint64_t(2 * I));
+          });
+        }
+      }
     }
     TC_TS(t, 12);
     const int st = t % C::NSV, b = t % C::NSB;
@@ -281,7 +297,7 @@ __device__ __noinline__ void tc_residual_issuer(unsigned char* sm, TcBarriers* b
       if constexpr (C::KC) {
         // one K-sum over the concatenated segments: [uh|uh|um] . [vh|vm|vh]
         // (warp-wide batch: one elect, descriptors stepped by 32 B)
-        mma_ss_batch<C::NKS, 2, 2>(dt, da, db, ID_RES, 0u);
+        mma_ts_batch<C::NKS, 2>(dt, tm + C::T_U, db, ID_RES, 0u);
       } else {
         static_for<3 * KS>([&](auto I) {
           constexpr int q = I / KS, ks = I % KS;

@@ -552,6 +552,47 @@ __device__ __forceinline__ void mma_gv_ts_batch(uint32_t d, uint32_t s_tmem, uin
 }
 #undef SPCP_TSB
 
+// smem -> TMEM copy of one 128-row x 32-byte K-step of a K-major operand image
+// (lane i <- row i, 8 columns of fp16 pairs: the A-from-TMEM layout; verified
+// against tcgen05.st by tools/tc_probe.cu P7).  Warp-wide, one elected issuer.
+__device__ __forceinline__ void tmem_cp_128x256b_w(uint32_t taddr, uint64_t desc) {
+  asm volatile(
+      "{\n.reg .pred e;\n.reg .b32 r;\nelect.sync r|e, 0xffffffff;\n"
+      "@e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n}\n" ::"r"(taddr),
+      "l"(desc)
+      : "memory");
+}
+
+// N TS MMAs (A from TMEM, stepped by 8 columns = one fp16 K-step of 16; B
+// descriptor stepped by SB units), warp-wide with one elect.
+#define SPCP_TSN(ACC) "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t], b, %3, " ACC ";\n"
+#define SPCP_TSN_STEP "add.s32 t, t, 8;\nadd.s64 b, b, %5;\n"
+template <int N, int SB>
+__device__ __forceinline__ void mma_ts_batch(uint32_t d, uint32_t a_tmem, uint64_t b0,
+                                             uint32_t idesc, uint32_t acc0) {
+  static_assert(N >= 1 && N <= 4, "batch size");
+#define SPCP_TSN_HEAD                                                                   \
+  "{\n.reg .pred e, p0, pt;\n.reg .b32 r, t;\n.reg .b64 b;\n"                           \
+  "setp.ne.b32 p0, %4, 0;\nsetp.eq.b32 pt, 0, 0;\nelect.sync r|e, 0xffffffff;\n"        \
+  "mov.b32 t, %1;\nmov.b64 b, %2;\n" SPCP_TSN("p0")
+#define SPCP_TSN_ARGS ::"r"(d), "r"(a_tmem), "l"(b0), "r"(idesc), "r"(acc0), "n"(SB) : "memory"
+  if constexpr (N == 1) {
+    asm volatile(SPCP_TSN_HEAD "}\n" SPCP_TSN_ARGS);
+  } else if constexpr (N == 2) {
+    asm volatile(SPCP_TSN_HEAD SPCP_TSN_STEP SPCP_TSN("pt") "}\n" SPCP_TSN_ARGS);
+  } else if constexpr (N == 3) {
+    asm volatile(SPCP_TSN_HEAD SPCP_TSN_STEP SPCP_TSN("pt") SPCP_TSN_STEP SPCP_TSN("pt") "}\n"
+                 SPCP_TSN_ARGS);
+  } else {
+    asm volatile(SPCP_TSN_HEAD SPCP_TSN_STEP SPCP_TSN("pt") SPCP_TSN_STEP SPCP_TSN("pt")
+                     SPCP_TSN_STEP SPCP_TSN("pt") "}\n" SPCP_TSN_ARGS);
+  }
+#undef SPCP_TSN_HEAD
+#undef SPCP_TSN_ARGS
+}
+#undef SPCP_TSN
+#undef SPCP_TSN_STEP
+
 __device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
   asm volatile(
       "{\n.reg .pred e;\n.reg .b32 r;\nelect.sync r|e, 0xffffffff;\n"
