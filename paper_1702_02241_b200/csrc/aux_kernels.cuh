@@ -287,25 +287,27 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p) {
 // columns); the slot sources of a sub-band / column tile are read as float4
 // and summed in fp64 in the CSR's fixed order (deterministic).  U side:
 // U_FULL or U_PARTIAL; V side always.
+template <int LPI>
 __global__ void __launch_bounds__(256) tc_reduce_kernel(const ReduceParams p) {
-  // Four lanes per output item (row r, 4 columns): lane j sums the CSR sources
-  // e = j, j + 4, ... of the item (all its loads in flight at once), then the
-  // four partial sums are combined in a fixed order ((l0 + l1) + (l2 + l3)).
+  // LPI lanes per output item (row r, 4 columns): lane j sums the CSR sources
+  // e = j, j + LPI, ... of the item (all its loads in flight at once), then the
+  // LPI partial sums are combined in a fixed butterfly order.
   __shared__ double scratch[32];
   __shared__ bool am_last;
   const int c4n = p.kst >> 2;
   const int64_t nu4 = p.m * c4n, nv4 = p.n * c4n;
   double s[6] = {0, 0, 0, 0, 0, 0};
-  const int j = threadIdx.x & 3;
-  const int64_t stride = (int64_t(gridDim.x) * blockDim.x) >> 2;  // items per sweep
+  constexpr int IPW = 32 / LPI;  // items per warp
+  const int j = threadIdx.x & (LPI - 1);
+  const int64_t stride = (int64_t(gridDim.x) * blockDim.x) / LPI;  // items per sweep
   const int64_t gtid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   const float* plf = reinterpret_cast<const float*>(p.pleft);
   const float* prf = reinterpret_cast<const float*>(p.pright);
   const float gvs = p.tc_unscale[0], gts = p.tc_unscale[1];
   const int64_t n_items = nu4 + nv4;
-  // warp-uniform trip count: a warp's 8 items start at (gtid >> 5) * 8
-  for (int64_t w0 = (gtid >> 5) * 8; w0 < n_items; w0 += stride) {
-    const int64_t q0 = w0 + ((threadIdx.x & 31) >> 2);
+  // warp-uniform trip count: a warp's IPW items start at (gtid >> 5) * IPW
+  for (int64_t w0 = (gtid >> 5) * IPW; w0 < n_items; w0 += stride) {
+    const int64_t q0 = w0 + ((threadIdx.x & 31) / LPI);
     const bool live = q0 < n_items;  // dead lanes still join the shuffles
     const int64_t q = live ? q0 : 0;
     const bool is_u = q < nu4;
@@ -324,10 +326,11 @@ __global__ void __launch_bounds__(256) tc_reduce_kernel(const ReduceParams p) {
       const int64_t sst = int64_t(128) * p.kst;
       // batches of 8 sources per lane: the 8 index loads, then the 8 data
       // loads are all in flight before the (in-order) adds
-      for (int eb = e0 + j; eb < e1; eb += 32) {
+      for (int eb = e0 + j; eb < e1; eb += 8 * LPI) {
         int idx[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) idx[u] = (eb + 4 * u < e1) ? __ldg(p.csr_u_idx + eb + 4 * u) : -1;
+        for (int u = 0; u < 8; ++u)
+          idx[u] = (eb + LPI * u < e1) ? __ldg(p.csr_u_idx + eb + LPI * u) : -1;
         float4 v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u)
@@ -346,10 +349,11 @@ __global__ void __launch_bounds__(256) tc_reduce_kernel(const ReduceParams p) {
       const int64_t sst = int64_t(p.gt_rows) * p.kst;
       const int64_t hoff = p.chunked ? int64_t(64) * 4 : int64_t(64) * p.kst;
       const bool two = p.gt_rows == 128;
-      for (int eb = e0 + j; eb < e1; eb += 16) {
+      for (int eb = e0 + j; eb < e1; eb += 4 * LPI) {
         int idx[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) idx[u] = (eb + 4 * u < e1) ? __ldg(p.csr_v_idx + eb + 4 * u) : -1;
+        for (int u = 0; u < 4; ++u)
+          idx[u] = (eb + LPI * u < e1) ? __ldg(p.csr_v_idx + eb + LPI * u) : -1;
         float4 v[4], w[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -365,9 +369,9 @@ __global__ void __launch_bounds__(256) tc_reduce_kernel(const ReduceParams p) {
         }
       }
     }
-    // fixed-order combine of the four lanes
+    // fixed-order combine of the LPI lanes
 #pragma unroll
-    for (int o = 1; o <= 2; o <<= 1) {
+    for (int o = 1; o < LPI; o <<= 1) {
       a0 += __shfl_xor_sync(0xffffffffu, a0, o);
       a1 += __shfl_xor_sync(0xffffffffu, a1, o);
       a2 += __shfl_xor_sync(0xffffffffu, a2, o);

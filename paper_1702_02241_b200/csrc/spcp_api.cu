@@ -839,11 +839,15 @@ static int run_reduce(spcp_problem* p, int64_t k, int kp, int part_dtype, const 
     rp.tc_unscale = &p->tc_scales.as<TcScales>()->gv_unscale;
   }
   if (sh.tc && (u_mode == U_FULL || u_mode == U_PARTIAL) && v_mode) {
-    const int64_t items = (p->m + p->n) * (sh.kst / 4);  // 4 lanes per item
-    const int nb = int(std::min<int64_t>((items * 4 + 255) / 256, 148 * 8));
+#ifndef SPCP_REDUCE_LPI
+#define SPCP_REDUCE_LPI 2
+#endif
+    constexpr int LPI = SPCP_REDUCE_LPI;  // lanes per output item
+    const int64_t items = (p->m + p->n) * (sh.kst / 4);
+    const int nb = int(std::min<int64_t>((items * LPI + 255) / 256, 148 * 8));
     if ((rc = p->blk.ensure(size_t(nb) * 6 * sizeof(double)))) return rc;
     rp.blk = p->blk.as<double>();  // (ensure may have grown the buffer)
-    tc_reduce_kernel<<<nb, 256, 0, p->stream>>>(rp);
+    tc_reduce_kernel<LPI><<<nb, 256, 0, p->stream>>>(rp);
   }
   else if (part_dtype == SPCP_F32)
     reduce_kernel<float><<<nblk, 256, 0, p->stream>>>(rp);
