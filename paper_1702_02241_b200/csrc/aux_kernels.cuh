@@ -6,6 +6,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "tc_common.cuh"
 
 namespace spcp {
 
@@ -289,6 +290,8 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p) {
 // U_FULL or U_PARTIAL; V side always.
 template <int LPI>
 __global__ void __launch_bounds__(256) tc_reduce_kernel(const ReduceParams p) {
+  tc::pdl_wait();  // the fused pass's partial slots are complete
+  tc::pdl_launch_next();
   // LPI lanes per output item (row r, 4 columns): lane j sums the CSR sources
   // e = j, j + LPI, ... of the item (all its loads in flight at once), then the
   // LPI partial sums are combined in a fixed butterfly order.

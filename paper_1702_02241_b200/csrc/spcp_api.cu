@@ -24,6 +24,34 @@
 
 namespace spcp {
 
+// Launch with programmatic stream serialization (PDL): the kernel may start
+// launching while its predecessor drains; it calls griddepcontrol.wait before
+// touching the predecessor's results.  SPCP_PDL=0 turns it off.
+static bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("SPCP_PDL");
+    on = (e && std::string(e) == "0") ? 0 : 1;
+  }
+  return on == 1;
+}
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+
 static thread_local std::string g_last_error;
 
 void set_error(const std::string& msg) { g_last_error = msg; }
@@ -484,7 +512,8 @@ static int tc_launch(spcp_problem* p, int64_t k) {
     tp.dbg_ts = dbg;
   }
   if (p->prof && prof_begin(p)) return SPCP_ERR_CUDA;
-  kern<<<p->tc_grid, C::NTHREADS, C::SMEM, p->stream>>>(p->tc_xmap, p->tc_mmap, tp);
+  SPCP_CUDA(launch_pdl(kern, dim3(p->tc_grid), dim3(C::NTHREADS), C::SMEM, p->stream, p->tc_xmap,
+                       p->tc_mmap, tp));
   SPCP_CHECK_LAUNCH("tc_eval_kernel");
   if (p->prof && prof_end(p)) return SPCP_ERR_CUDA;
   if (tp.debug & 4) {
@@ -528,9 +557,10 @@ static int tc_images_kc(spcp_problem* p, int64_t k, const double* z, const doubl
   if ((rc = p->tc_uimg.ensure(size_t(p->tc_nsb) * 128 * RB))) return rc;
   if ((rc = p->tc_vimg.ensure(size_t(p->tc_ntc) * 64 * RB))) return rc;
   const int64_t total = (p->m_pad + p->n_pad) * SEG;
-  tc_images_kc_kernel<SEG><<<grid_for(total), 256, 0, p->stream>>>(
-      z, dz, alpha, p->m, p->n, k, p->m_pad, p->n_pad, p->tc_scales.as<TcScales>(),
-      p->lambda_s, p->tc_uimg.as<unsigned char>(), p->tc_vimg.as<unsigned char>());
+  SPCP_CUDA(launch_pdl(tc_images_kc_kernel<SEG>, dim3(grid_for(total)), dim3(256), 0, p->stream,
+                       z, dz, alpha, p->m, p->n, k, p->m_pad, p->n_pad,
+                       p->tc_scales.as<TcScales>(), p->lambda_s, p->tc_uimg.as<unsigned char>(),
+                       p->tc_vimg.as<unsigned char>()));
   SPCP_CHECK_LAUNCH("tc_images_kc");
   p->launches++;
   return SPCP_OK;
@@ -560,7 +590,8 @@ static int tc_eval(spcp_problem* p, int64_t k, const double* z, const double* dz
   if (tc_use_kc(k)) {
     TcScales* sc = p->tc_scales.as<TcScales>();
     const int64_t nu = p->m * k, nv = p->n * k;
-    tc_max_kernel<<<grid_for(nu + nv, 256, 148 * 4), 256, 0, p->stream>>>(z, dz, alpha, nu, nv, sc);
+    SPCP_CUDA(launch_pdl(tc_max_kernel, dim3(grid_for(nu + nv, 256, 148 * 4)), dim3(256), 0,
+                         p->stream, z, dz, alpha, nu, nv, sc));
     SPCP_CHECK_LAUNCH("tc_max");
     p->launches += 1;
     switch (int(round_up(k, 4))) {
@@ -847,7 +878,7 @@ static int run_reduce(spcp_problem* p, int64_t k, int kp, int part_dtype, const 
     const int nb = int(std::min<int64_t>((items * LPI + 255) / 256, 148 * 8));
     if ((rc = p->blk.ensure(size_t(nb) * 6 * sizeof(double)))) return rc;
     rp.blk = p->blk.as<double>();  // (ensure may have grown the buffer)
-    tc_reduce_kernel<LPI><<<nb, 256, 0, p->stream>>>(rp);
+    SPCP_CUDA(launch_pdl(tc_reduce_kernel<LPI>, dim3(nb), dim3(256), 0, p->stream, rp));
   }
   else if (part_dtype == SPCP_F32)
     reduce_kernel<float><<<nblk, 256, 0, p->stream>>>(rp);

@@ -435,6 +435,8 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK, SEG>::NTHREADS, 1)
   const int T = ue - ub;
   const TcUnit* units = p.units + ub;
   const int run0 = T > 0 ? units[0].gv_slot : 0;  // CTA-local run index = gv_slot - run0
+  pdl_wait();  // the operand images / scales of this evaluation are complete
+  pdl_launch_next();  // the reduce kernel's CTAs queue for the SMs as they free up
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     // the image pass (the only reader of the maxima) has completed: reset them
     // for the next evaluation's max pass instead of a separate memset
@@ -878,6 +880,8 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK, SEG>::NTHREADS, 1)
 // non-negative doubles order like unsigned integers).
 __global__ void tc_max_kernel(const double* __restrict__ z, const double* __restrict__ dz,
                               double alpha, int64_t nu, int64_t nv, TcScales* sc) {
+  tc::pdl_wait();
+  tc::pdl_launch_next();
   unsigned long long mu = 0, mv = 0;
   for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < nu + nv;
        q += int64_t(gridDim.x) * blockDim.x) {
@@ -996,6 +1000,8 @@ __global__ void tc_images_kc_kernel(const double* __restrict__ z, const double* 
                                     unsigned char* v_img) {
   using C = TcCfg<16, false, SEG>;
   constexpr int RB = C::RB, NE = RB / 2;
+  tc::pdl_wait();
+  tc::pdl_launch_next();
   const TcScales scl = tc_compute_scales(sc, tau);
   const double su = scl.su, sv = scl.sv;
   if (blockIdx.x == 0 && threadIdx.x == 0) {

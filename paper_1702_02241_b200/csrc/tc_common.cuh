@@ -87,6 +87,14 @@ __device__ __forceinline__ float4 lds128(const void* p) {
   return v;
 }
 
+// Programmatic dependent launch: wait for the preceding grid (a no-op unless
+// this kernel was launched with programmatic stream serialization) / let the
+// next one start launching its CTAs.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_next() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ------------------------------------------------------------------ packed fp32 pairs
 // Blackwell FFMA2 / FADD2 / FMUL2 on float2 (one instruction per pair)
 __device__ __forceinline__ uint64_t f2_bits(float2 v) {
