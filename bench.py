@@ -359,6 +359,7 @@ def time_to_certificate(dev):
            "verdict": "certified" if cert.gap_bound <= 1e-2 * max(1.0, abs(rep.objective))
            else "flagged", "t4_method": cert.info.get("t4_method"),
            "sigma_p_max": cert.info.get("sigma_p_max"),
+           "t4_iters": cert.info.get("iters"), "t4_bound": cert.info.get("t4_bound"),
            "fp64_switch_iter": rep.extra.get("fp64_switch_iter")}
     spec.release_device()
     del x

@@ -117,12 +117,21 @@ class _ProjectedOperator:
         return self._proj(self.v1, w.mul_(-1.0 / self.lam))
 
 
-def _subspace_sigmas(op, n, m, r, block=16, max_iter=60, tol=1e-9, seed=0):
+_SUBSPACE_TOL = 1e-9
+
+
+def _q_bound(n, eps=0.5, fail=1e-6):
+    """Iterations after which 1.648 sqrt(n) e^(-eps (2q - 1)) <= fail."""
+    return int(math.ceil((math.log(1.648 * math.sqrt(max(n, 1)) / fail) / eps + 1.0) / 2.0))
+
+
+def _subspace_sigmas(op, n, m, r, block=16, max_iter=60, tol=None, seed=0):
     """Top singular values of P by randomized block subspace iteration with
     Rayleigh-Ritz; the block doubles until its smallest Ritz value < 1."""
     import torch
 
     dp = op.dp
+    tol = _SUBSPACE_TOL if tol is None else tol
     cap = max(1, min(m, n) - r)
     b = min(block, cap)
     iters_total = 0
@@ -142,6 +151,17 @@ def _subspace_sigmas(op, n, m, r, block=16, max_iter=60, tol=1e-9, seed=0):
             if prev is not None and abs(sig[0] - prev[0]) <= tol * max(1.0, sig[0]) and \
                     abs(t4 - prev[1]) <= tol * max(1.0, t4):
                 break
+            # t4 only needs sigma(P) against 1.  After q steps from a Gaussian start
+            # the top Ritz value theta of the subspace (power) iteration on P^T P
+            # satisfies P[theta^2 < (1 - eps) sigma_max^2] <= 1.648 sqrt(n)
+            # e^(-eps (2q - 1)) (Kuczynski & Wozniakowski 1992).  With eps = 1/2 and
+            # q >= _Q_BOUND(n) that is < 1e-6, so sqrt(2) theta < 1 proves every
+            # sigma(P) < 1 and t4 = 0 exactly (the reference's dense SVD value).
+            if it + 1 >= _q_bound(n) and math.sqrt(2.0) * sig[0] < 1.0:
+                return sig, {"t4_method": "subspace", "block": b, "iters": iters_total,
+                             "sigma_p_max": float(sig[0]),
+                             "t4_bound": "sigma_max(P) < sqrt(2) theta_max < 1 "
+                                         "(failure prob < 1e-6)"}
             prev = (sig[0], t4)
             q, _ = device_thin_qr(dp, wz)
         if sig[-1] < 1.0 or b >= cap:
