@@ -146,6 +146,14 @@ int spcp_apply(spcp_problem* p, int64_t k, const double* z, int64_t b,
                const double* w_right, double* left_out, const double* w_left,
                double* right_out);
 
+/* spcp_apply with fp32 streaming products (fp32 X copy, fp32 operands, fp64
+ * outputs): for the certificate's subspace iteration, which only compares
+ * sigma(P) against 1.  Falls back to spcp_apply when no fp32 copy of X is
+ * stored or k exceeds the fused widths. */
+int spcp_apply_f32(spcp_problem* p, int64_t k, const double* z, int64_t b,
+                   const double* w_right, double* left_out, const double* w_left,
+                   double* right_out);
+
 /* ---- final L and S (solver.py:313-320) --------------------------------------
  * Rows [row0, row0+rows) of L = U V^T and S* = shrink(X - L) on Omega, float64,
  * written to device or host buffers (row-major, n columns); either may be NULL. */

@@ -41,6 +41,7 @@ EXPORTS = {
     "spcp_split_objective_host": [_vp, _i64, _i32, _vp, _vp, _dp, _vp, _vp],
     "spcp_phi_dense_host": [_vp, _vp, _dp, _vp, _vp],
     "spcp_apply": [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp],
+    "spcp_apply_f32": [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp],
     "spcp_materialize": [_vp, _i64, _vp, _i64, _i64, _vp, _vp, _i32],
     "spcp_materialize_grad": [_vp, _i64, _vp, _vp, _i64],
     "spcp_vec_multidot": [_vp, _i64, _i32, _pp, _pp, _dp],

@@ -106,14 +106,17 @@ class _ProjectedOperator:
         c = self.dp.gram(basis, w)
         return w - self.dp.matmul_small(basis, c)
 
+    # The subspace iteration only compares sigma(P) against 1, so its D
+    # products stream X in fp32 (spcp_apply_f32; fp64 when no fp32 copy of X is
+    # stored).  The cross terms t1..t3 keep the fp64 products.
     def right(self, w):  # P w, w: n x b
         w = self._proj(self.v1, w)
-        y, _ = self.dp.apply(self.k, self.z, w_right=w.contiguous())
+        y, _ = self.dp.apply(self.k, self.z, w_right=w.contiguous(), precision="fp32")
         return self._proj(self.u1, y.mul_(-1.0 / self.lam))
 
     def left(self, y):  # P^T y, y: m x b
         y = self._proj(self.u1, y)
-        _, w = self.dp.apply(self.k, self.z, w_left=y.contiguous())
+        _, w = self.dp.apply(self.k, self.z, w_left=y.contiguous(), precision="fp32")
         return self._proj(self.v1, w.mul_(-1.0 / self.lam))
 
 

@@ -113,6 +113,20 @@ __global__ void pad_operand_kernel(const double* __restrict__ w, int64_t rows, i
   }
 }
 
+// Columns [c0, c0 + bw) of a row-major float64 (rows x ld) matrix into a
+// zero-padded (rows_pad x pw) operand of type T (the apply passes' W / Y).
+template <typename T>
+__global__ void stage_cols_kernel(const double* __restrict__ w, int64_t ld, int64_t c0, int64_t bw,
+                                  int64_t rows, int64_t rows_pad, int pw, T* out) {
+  const int64_t total = rows_pad * pw;
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < total;
+       q += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = q / pw;
+    const int c = int(q % pw);
+    out[q] = (r < rows && c < bw) ? T(w[r * ld + c0 + c]) : T(0);
+  }
+}
+
 // ------------------------------------------------------------------ reduce
 enum UMode { U_SKIP = 0, U_FULL = 1, U_PARTIAL = 2, U_FROM_SUM = 3 };
 

@@ -15,6 +15,7 @@
 #include <mutex>
 #include <string>
 #include <tuple>
+#include <type_traits>
 #include <vector>
 
 #include "aux_kernels.cuh"
@@ -252,12 +253,12 @@ static int apply_kr(int64_t k) {
   return -1;
 }
 
-template <typename TX, bool MASK>
+template <typename T, typename TX, bool MASK>
 static int dispatch_apply(spcp_problem* p, int kr, int pw, StreamParams sp, LaunchShape& sh) {
-#define SPCP_AP(KR, PW)                                                                 \
-  if (kr == KR && pw == PW)                                                           \
-    return KR == 0 ? launch_stream<double, TX, 0, PW, MODE_RAW, MASK>(p, sp, sh, false) \
-                   : launch_stream<double, TX, KR, PW, MODE_APPLY, MASK>(p, sp, sh, false);
+#define SPCP_AP(KR, PW)                                                            \
+  if (kr == KR && pw == PW)                                                      \
+    return KR == 0 ? launch_stream<T, TX, 0, PW, MODE_RAW, MASK>(p, sp, sh, false) \
+                   : launch_stream<T, TX, KR, PW, MODE_APPLY, MASK>(p, sp, sh, false);
   SPCP_AP(0, 8)
   SPCP_AP(0, 32)
   SPCP_AP(8, 8)
@@ -902,6 +903,105 @@ static int fetch_out(spcp_problem* p, double* out) {
 
 using namespace spcp;
 
+template <typename T>
+static int apply_impl(spcp_problem* p, int64_t k, const double* z, int64_t b,
+                      const double* w_right, double* left_out, const double* w_left,
+                      double* right_out) {
+  int rc;
+  if (k < 0 || b < 1) return fail(SPCP_ERR_DIMENSION, "bad apply shape");
+  SPCP_CUDA(cudaSetDevice(p->device));
+  const bool x64 = p->x64.ptr != nullptr;
+  int kr = apply_kr(k);
+  // residual operands (T)
+  if (kr > 0) {
+    if ((rc = prep<T>(p, k, kr, z, nullptr, 0.0))) return rc;
+  } else if (kr < 0) {
+    // large rank bound: materialise G once, then RAW products over it
+    const int64_t len = (p->m + p->n) * k;
+    (void)len;
+    if ((rc = p->gu_tmp.ensure(size_t(p->m_pad) * p->ldx * sizeof(double)))) return rc;
+    double* gmat = p->gu_tmp.as<double>();
+    SPCP_CUDA(cudaMemsetAsync(gmat, 0, size_t(p->m_pad) * p->ldx * sizeof(double), p->stream));
+    const int64_t nbx = ceil_div(p->n, 64), nby = ceil_div(p->m, 64);
+    if ((rc = p->pphi.ensure(size_t(nbx * nby) * sizeof(double)))) return rc;
+    rc = x64 ? launch_dense<double>(p, 1, k, z, 0, p->m, gmat, nullptr, p->ldx, p->pphi.as<double>())
+             : launch_dense<float>(p, 1, k, z, 0, p->m, gmat, nullptr, p->ldx, p->pphi.as<double>());
+    if (rc) return rc;
+  }
+  for (int64_t c0 = 0; c0 < b; c0 += 32) {
+    const int64_t bw = std::min<int64_t>(32, b - c0);
+    const int pw = bw <= 8 ? 8 : 32;
+    if (w_right) {
+      if ((rc = p->wr.ensure(size_t(p->n_pad) * pw * sizeof(T)))) return rc;
+      stage_cols_kernel<T><<<grid_for(p->n_pad * pw), 256, 0, p->stream>>>(
+          w_right, b, c0, bw, p->n, p->n_pad, pw, p->wr.as<T>());
+      SPCP_CHECK_LAUNCH("stage_cols");
+    }
+    if (w_left) {
+      if ((rc = p->wl.ensure(size_t(p->m_pad) * pw * sizeof(T)))) return rc;
+      stage_cols_kernel<T><<<grid_for(p->m_pad * pw), 256, 0, p->stream>>>(
+          w_left, b, c0, bw, p->m, p->m_pad, pw, p->wl.as<T>());
+      SPCP_CHECK_LAUNCH("stage_cols");
+    }
+    StreamParams sp{};
+    sp.m_pad = p->m_pad;
+    sp.n_pad = p->n_pad;
+    sp.ldx = p->ldx;
+    sp.ldm = p->ldm;
+    sp.tau = p->lambda_s;
+    sp.uc = p->uc.ptr;
+    sp.vc = p->vc.ptr;
+    sp.wr = p->wr.ptr;
+    sp.wl = p->wl.ptr;
+    sp.do_left = w_right != nullptr;
+    sp.do_right = w_left != nullptr;
+    LaunchShape sh;
+    if (kr < 0) {
+      sp.x = p->gu_tmp.ptr;
+      sp.mbits = nullptr;
+      rc = pw == 8 ? launch_stream<double, double, 0, 8, MODE_RAW, false>(p, sp, sh, false)
+                   : launch_stream<double, double, 0, 32, MODE_RAW, false>(p, sp, sh, false);
+    } else {
+      sp.x = x64 ? p->x64.ptr : p->x32.ptr;
+      sp.mbits = p->masked ? p->mbits.as<uint32_t>() : nullptr;
+      if (std::is_same<T, float>::value) {
+        sp.x = p->x32.ptr;
+        rc = p->masked ? dispatch_apply<T, float, true>(p, kr, pw, sp, sh)
+                       : dispatch_apply<T, float, false>(p, kr, pw, sp, sh);
+      } else if (x64) {
+        rc = p->masked ? dispatch_apply<T, double, true>(p, kr, pw, sp, sh)
+                       : dispatch_apply<T, double, false>(p, kr, pw, sp, sh);
+      } else {
+        rc = p->masked ? dispatch_apply<T, float, true>(p, kr, pw, sp, sh)
+                       : dispatch_apply<T, float, false>(p, kr, pw, sp, sh);
+      }
+    }
+    if (rc) return rc;
+    if ((rc = p->small.ensure(size_t(std::max(p->m, p->n)) * 32 * sizeof(double)))) return rc;
+    if (w_right) {
+      reduce_apply_kernel<T><<<grid_for(p->m * bw), 256, 0, p->stream>>>(
+          p->pleft.as<T>(), sh.nchunks, p->m, p->m_pad, pw, bw, p->small.as<double>());
+      SPCP_CHECK_LAUNCH("reduce_apply");
+      p->launches++;
+      SPCP_CUDA(cudaMemcpy2DAsync(left_out + c0, b * sizeof(double), p->small.ptr,
+                                  bw * sizeof(double), bw * sizeof(double), p->m,
+                                  cudaMemcpyDeviceToDevice, p->stream));
+    }
+    if (w_left) {
+      reduce_apply_kernel<T><<<grid_for(p->n * bw), 256, 0, p->stream>>>(
+          p->pright.as<T>(), sh.nrb, p->n, p->n_pad, pw, bw, p->small.as<double>());
+      SPCP_CHECK_LAUNCH("reduce_apply");
+      p->launches++;
+      SPCP_CUDA(cudaMemcpy2DAsync(right_out + c0, b * sizeof(double), p->small.ptr,
+                                  bw * sizeof(double), bw * sizeof(double), p->n,
+                                  cudaMemcpyDeviceToDevice, p->stream));
+    }
+  }
+  SPCP_CUDA(cudaStreamSynchronize(p->stream));
+  return SPCP_OK;
+}
+
+
 // ====================================================================== ABI
 extern "C" {
 
@@ -1212,93 +1312,17 @@ int spcp_phi_dense_host(spcp_problem* p, const double* l, double* value, double*
 int spcp_apply(spcp_problem* p, int64_t k, const double* z, int64_t b, const double* w_right,
                double* left_out, const double* w_left, double* right_out) {
   if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
-  int rc;
-  if (k < 0 || b < 1) return fail(SPCP_ERR_DIMENSION, "bad apply shape");
-  SPCP_CUDA(cudaSetDevice(p->device));
-  const bool x64 = p->x64.ptr != nullptr;
-  int kr = apply_kr(k);
-  // residual operands (float64)
-  if (kr > 0) {
-    if ((rc = prep<double>(p, k, kr, z, nullptr, 0.0))) return rc;
-  } else if (kr < 0) {
-    // large rank bound: materialise G once, then RAW products over it
-    const int64_t len = (p->m + p->n) * k;
-    (void)len;
-    if ((rc = p->gu_tmp.ensure(size_t(p->m_pad) * p->ldx * sizeof(double)))) return rc;
-    double* gmat = p->gu_tmp.as<double>();
-    SPCP_CUDA(cudaMemsetAsync(gmat, 0, size_t(p->m_pad) * p->ldx * sizeof(double), p->stream));
-    const int64_t nbx = ceil_div(p->n, 64), nby = ceil_div(p->m, 64);
-    if ((rc = p->pphi.ensure(size_t(nbx * nby) * sizeof(double)))) return rc;
-    rc = x64 ? launch_dense<double>(p, 1, k, z, 0, p->m, gmat, nullptr, p->ldx, p->pphi.as<double>())
-             : launch_dense<float>(p, 1, k, z, 0, p->m, gmat, nullptr, p->ldx, p->pphi.as<double>());
-    if (rc) return rc;
-  }
-  for (int64_t c0 = 0; c0 < b; c0 += 32) {
-    const int64_t bw = std::min<int64_t>(32, b - c0);
-    const int pw = bw <= 8 ? 8 : 32;
-    if (w_right) {
-      if ((rc = p->wr.ensure(size_t(p->n_pad) * pw * sizeof(double)))) return rc;
-      SPCP_CUDA(cudaMemsetAsync(p->wr.ptr, 0, size_t(p->n_pad) * pw * sizeof(double), p->stream));
-      SPCP_CUDA(cudaMemcpy2DAsync(p->wr.ptr, pw * sizeof(double), w_right + c0, b * sizeof(double),
-                                  bw * sizeof(double), p->n, cudaMemcpyDeviceToDevice, p->stream));
-    }
-    if (w_left) {
-      if ((rc = p->wl.ensure(size_t(p->m_pad) * pw * sizeof(double)))) return rc;
-      SPCP_CUDA(cudaMemsetAsync(p->wl.ptr, 0, size_t(p->m_pad) * pw * sizeof(double), p->stream));
-      SPCP_CUDA(cudaMemcpy2DAsync(p->wl.ptr, pw * sizeof(double), w_left + c0, b * sizeof(double),
-                                  bw * sizeof(double), p->m, cudaMemcpyDeviceToDevice, p->stream));
-    }
-    StreamParams sp{};
-    sp.m_pad = p->m_pad;
-    sp.n_pad = p->n_pad;
-    sp.ldx = p->ldx;
-    sp.ldm = p->ldm;
-    sp.tau = p->lambda_s;
-    sp.uc = p->uc.ptr;
-    sp.vc = p->vc.ptr;
-    sp.wr = p->wr.ptr;
-    sp.wl = p->wl.ptr;
-    sp.do_left = w_right != nullptr;
-    sp.do_right = w_left != nullptr;
-    LaunchShape sh;
-    if (kr < 0) {
-      sp.x = p->gu_tmp.ptr;
-      sp.mbits = nullptr;
-      rc = pw == 8 ? launch_stream<double, double, 0, 8, MODE_RAW, false>(p, sp, sh, false)
-                   : launch_stream<double, double, 0, 32, MODE_RAW, false>(p, sp, sh, false);
-    } else {
-      sp.x = x64 ? p->x64.ptr : p->x32.ptr;
-      sp.mbits = p->masked ? p->mbits.as<uint32_t>() : nullptr;
-      if (x64)
-        rc = p->masked ? dispatch_apply<double, true>(p, kr, pw, sp, sh)
-                       : dispatch_apply<double, false>(p, kr, pw, sp, sh);
-      else
-        rc = p->masked ? dispatch_apply<float, true>(p, kr, pw, sp, sh)
-                       : dispatch_apply<float, false>(p, kr, pw, sp, sh);
-    }
-    if (rc) return rc;
-    if ((rc = p->small.ensure(size_t(std::max(p->m, p->n)) * 32 * sizeof(double)))) return rc;
-    if (w_right) {
-      reduce_apply_kernel<double><<<grid_for(p->m * bw), 256, 0, p->stream>>>(
-          p->pleft.as<double>(), sh.nchunks, p->m, p->m_pad, pw, bw, p->small.as<double>());
-      SPCP_CHECK_LAUNCH("reduce_apply");
-      p->launches++;
-      SPCP_CUDA(cudaMemcpy2DAsync(left_out + c0, b * sizeof(double), p->small.ptr,
-                                  bw * sizeof(double), bw * sizeof(double), p->m,
-                                  cudaMemcpyDeviceToDevice, p->stream));
-    }
-    if (w_left) {
-      reduce_apply_kernel<double><<<grid_for(p->n * bw), 256, 0, p->stream>>>(
-          p->pright.as<double>(), sh.nrb, p->n, p->n_pad, pw, bw, p->small.as<double>());
-      SPCP_CHECK_LAUNCH("reduce_apply");
-      p->launches++;
-      SPCP_CUDA(cudaMemcpy2DAsync(right_out + c0, b * sizeof(double), p->small.ptr,
-                                  bw * sizeof(double), bw * sizeof(double), p->n,
-                                  cudaMemcpyDeviceToDevice, p->stream));
-    }
-  }
-  SPCP_CUDA(cudaStreamSynchronize(p->stream));
-  return SPCP_OK;
+  return apply_impl<double>(p, k, z, b, w_right, left_out, w_left, right_out);
+}
+
+int spcp_apply_f32(spcp_problem* p, int64_t k, const double* z, int64_t b,
+                   const double* w_right, double* left_out, const double* w_left,
+                   double* right_out) {
+  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
+  // fp32 streaming products need the fp32 copy of X and the fused widths
+  if (!p->x32.ptr || apply_kr(k) < 0)
+    return apply_impl<double>(p, k, z, b, w_right, left_out, w_left, right_out);
+  return apply_impl<float>(p, k, z, b, w_right, left_out, w_left, right_out);
 }
 
 int spcp_materialize(spcp_problem* p, int64_t k, const double* z, int64_t row0, int64_t rows,

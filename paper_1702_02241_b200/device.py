@@ -201,9 +201,10 @@ class DeviceProblem:
         return float(val.value), g, s
 
     # ------------------------------------------------------------ operators
-    def apply(self, k, z, w_right=None, w_left=None):
+    def apply(self, k, z, w_right=None, w_left=None, precision="fp64"):
         """(G @ w_right, G^T @ w_left) as float64 device matrices; G = grad phi at
-        U V^T (k >= 1) or the zero-filled observed X (k == 0)."""
+        U V^T (k >= 1) or the zero-filled observed X (k == 0).  precision="fp32"
+        streams the fp32 copy of X with fp32 operands (spcp_apply_f32)."""
         torch = torch_mod()
         b = int((w_right if w_right is not None else w_left).shape[1])
         left = right = None
@@ -213,8 +214,9 @@ class DeviceProblem:
         if w_left is not None:
             w_left = w_left.contiguous()
             right = torch.empty((self.n, b), dtype=torch.float64, device=self.device)
-        check(lib.spcp_apply(self.h, int(k), dptr(z), b, dptr(w_right), dptr(left),
-                             dptr(w_left), dptr(right)))
+        fn = lib.spcp_apply_f32 if precision == "fp32" else lib.spcp_apply
+        check(fn(self.h, int(k), dptr(z), b, dptr(w_right), dptr(left), dptr(w_left),
+                 dptr(right)))
         return left, right
 
     def materialize(self, k, z, row0=0, rows=None, want_l=True, want_s=True):
