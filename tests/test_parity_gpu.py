@@ -212,3 +212,28 @@ def test_materialize_l_s(api, oracle):
     _, _, s_ref = oracle.phi_value_grad(u @ v.T, x, 0.45, mask)
     np.testing.assert_allclose(s, s_ref, rtol=0, atol=1e-12)
     assert (s[~mask] == 0).all()
+
+
+@pytest.mark.parametrize("k,b,masked", [(6, 13, True), (20, 40, False), (32, 8, True)])
+def test_apply_f32_products(api, oracle, k, b, masked):
+    """spcp_apply_f32 (the certificate's subspace-iteration products): fp32
+    streaming over the fp32 copy of X, within the fp32 tolerance of numpy."""
+    import torch
+
+    from paper_1702_02241_b200.device import DeviceProblem
+
+    rng = np.random.default_rng(100 + k)
+    m, n = 900, 700
+    x = f32(rng.standard_normal((m, n)) * 2.0)
+    mask = rng.random((m, n)) < 0.6 if masked else None
+    dp = DeviceProblem(x, 1.3, 0.5, mask=mask, store=("f32", "f64"))
+    u = f32(rng.standard_normal((m, k)) / np.sqrt(k))
+    v = f32(rng.standard_normal((n, k)) / np.sqrt(k))
+    z = torch.from_numpy(np.r_[u.ravel(), v.ravel()]).cuda()
+    wr = rng.standard_normal((n, b))
+    wl = rng.standard_normal((m, b))
+    _, g, _ = oracle.phi_value_grad(u @ v.T, x, 0.5, mask)
+    left, right = dp.apply(k, z, w_right=torch.from_numpy(wr).cuda(),
+                           w_left=torch.from_numpy(wl).cuda(), precision="fp32")
+    assert rel(left.cpu().numpy(), g @ wr) <= FP32_TOL
+    assert rel(right.cpu().numpy(), g.T @ wl) <= FP32_TOL
