@@ -237,3 +237,55 @@ def test_apply_f32_products(api, oracle, k, b, masked):
                            w_left=torch.from_numpy(wl).cuda(), precision="fp32")
     assert rel(left.cpu().numpy(), g @ wr) <= FP32_TOL
     assert rel(right.cpu().numpy(), g.T @ wl) <= FP32_TOL
+
+
+@pytest.mark.parametrize("k,masked", [(12, False), (20, True), (30, False)])
+def test_sharded_partial_finish_on_one_gpu(api, k, masked):
+    """The column-sharded C ABI (spcp_eval_partial -> all-reduce -> spcp_eval_finish,
+    SURVEY §8(e)) with two column shards on one GPU and the all-reduce done by
+    hand: f, g.dz and the gradient match the unsharded evaluation."""
+    import torch
+
+    from paper_1702_02241_b200._lib import SPCP_F32, SPCP_F64
+    from paper_1702_02241_b200.device import DeviceProblem
+
+    rng = np.random.default_rng(500 + k)
+    m, n = 1100, 900
+    x = f32(rng.standard_normal((m, n)) * 2.0)
+    mask = rng.random((m, n)) < 0.7 if masked else None
+    ll, ls = 1.7, 0.4
+    u = rng.standard_normal((m, k)) / np.sqrt(k)
+    v = rng.standard_normal((n, k)) / np.sqrt(k)
+    du = rng.standard_normal((m, k)) * 1e-2
+    dv = rng.standard_normal((n, k)) * 1e-2
+    alpha = 0.3
+    full = DeviceProblem(x, ll, ls, mask=mask, store=("f32", "f64"))
+    z = torch.from_numpy(np.r_[u.ravel(), v.ravel()]).cuda()
+    dz = torch.from_numpy(np.r_[du.ravel(), dv.ravel()]).cuda()
+    cut = 413
+    shards = [(0, cut), (cut, n)]
+    for code, tol in ((SPCP_F64, FP64_TOL), (SPCP_F32, FP32_TOL)):
+        g_full = torch.empty_like(z)
+        out_full = full.eval(k, code, z, dz, alpha, g_full)
+        gu_dtype = torch.float32 if code == SPCP_F32 else torch.float64
+        parts = []
+        for c0, c1 in shards:
+            dp = DeviceProblem(np.ascontiguousarray(x[:, c0:c1]), ll, ls,
+                               mask=None if mask is None else np.ascontiguousarray(mask[:, c0:c1]),
+                               store=("f32", "f64"), n_total=n, col0=c0)
+            zs = torch.cat([z[: m * k], z[m * k + c0 * k: m * k + c1 * k]])
+            dzs = torch.cat([dz[: m * k], dz[m * k + c0 * k: m * k + c1 * k]])
+            gu = torch.empty((m, k), dtype=gu_dtype, device="cuda")
+            scal = torch.empty(4, dtype=torch.float64, device="cuda")
+            gs = torch.empty_like(zs)
+            dp.eval_partial(k, code, zs, dzs, alpha, gu, scal, gs)
+            parts.append((dp, zs, dzs, gu, scal, gs, c0, c1))
+        gu_sum = sum(pt[3].double() for pt in parts).to(gu_dtype)
+        scal_sum = sum(pt[4] for pt in parts)
+        for dp, zs, dzs, _, _, gs, c0, c1 in parts:
+            out = dp.eval_finish(k, code, zs, dzs, alpha, gu_sum, scal_sum, gs)
+            assert abs(out[0] - out_full[0]) <= tol * abs(out_full[0])
+            assert out[3] == pytest.approx(out_full[3], rel=10 * tol, abs=1e-12)
+            assert rel(gs[: m * k].cpu().numpy(), g_full[: m * k].cpu().numpy()) <= tol
+            assert rel(gs[m * k:].cpu().numpy(),
+                       g_full[m * k + c0 * k: m * k + c1 * k].cpu().numpy()) <= tol
