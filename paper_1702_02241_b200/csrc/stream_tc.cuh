@@ -140,8 +140,12 @@ struct TcCfg {
   // gl at +16 of each warp's 32 columns) and G.V reads A from TMEM; three S
   // buffers (the next writer of a buffer is the other group's tile) and three
   // G^T U accumulators
-  static constexpr int NSB = KC ? 3 : 2;
-  static constexpr int NGT = KC ? 3 : 4;
+#ifndef SPCP_TC_NSB
+#define SPCP_TC_NSB 3  // measured: 3 (0.339 ms) beats 4 with two G^T U buffers (0.347 ms)
+#endif
+  static constexpr int NSB = KC ? SPCP_TC_NSB : 2;
+  static_assert(NSB <= 4, "TcBarriers holds four S buffers");
+  static constexpr int NGT = KC ? (SPCP_TC_NSB >= 4 ? 2 : 3) : 4;
   static constexpr uint32_t T_S = 0, T_GV = 64 * NSB;
   static constexpr uint32_t T_GT = T_GV + 2 * GVW;
   // KC: the run's U image also lives in TMEM (tcgen05.cp), so the residual is a
@@ -168,13 +172,14 @@ struct TcBarriers {
   uint64_t stage_full[4], stage_empty[4];
   uint64_t v_full[4], v_empty[4];
   uint64_t u_full[2], u_empty[2];
-  uint64_t s_full[3], s_empty[3];
+  uint64_t s_full[4], s_empty[4];
   uint64_t g_full[2], gs_empty[2];  // G image staged (per group) / free (per image)
   uint64_t gt_full[4], gt_empty[4];
   uint64_t gv_full[2], gv_empty[2];
   uint32_t tmem_base;
   double phi[16];
 };
+static_assert(sizeof(TcBarriers) <= 512, "barrier block exceeds its shared-memory slot");
 
 __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
   __half2 h = __floats2half2_rn(lo, hi);
@@ -822,6 +827,14 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK, SEG>::NTHREADS, 1)
         mbar_wait(&bar->gs_empty[b], ((t >> 1) & 1) ^ 1);
       }
       if (ts_w) TC_TS(t, 9);
+      // KC: drain G^T U of this group's previous tile BEFORE handing over G(t).
+      // Its completion is the event just waited for (gs_empty is committed right
+      // after G^T U), so this adds no wait; in exchange the accumulator is free
+      // before the reduction issuer can reach tile t (two G^T U buffers suffice,
+      // and the issuer never waits on gt_empty).
+      if constexpr (C::KC) {
+        if (t >= 2) drain_gt(t - 2, prev);
+      }
 #if defined(SPCP_TC_BISECT_EPI_SKIP)
       if (hi[0] == 0x12345 && lo[3] == 0x777) phi_acc += 1.0;  // keep the math alive
 #endif
@@ -847,7 +860,7 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK, SEG>::NTHREADS, 1)
       // ---- deferred drains of this group's previous tile (off the G hand-off
       // path: G^T U accumulators are double-buffered per group)
       if (t >= 2) {
-        drain_gt(t - 2, prev);
+        if constexpr (!C::KC) drain_gt(t - 2, prev);
         if (prev.flags & TCU_LAST_OF_RUN) drain_gv(prev);
       }
       prev = un;
