@@ -302,8 +302,10 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p) {
 // columns); the slot sources of a sub-band / column tile are read as float4
 // and summed in fp64 in the CSR's fixed order (deterministic).  U side:
 // U_FULL or U_PARTIAL; V side always.
+// Balanced source counts (square-ish super-blocks, e.g. C2): one item space over
+// both sides, LPI lanes per item.
 template <int LPI>
-__global__ void __launch_bounds__(256) tc_reduce_kernel(const ReduceParams p) {
+__global__ void __launch_bounds__(256) tc_reduce_lpi_kernel(const ReduceParams p) {
   tc::pdl_wait();  // the fused pass's partial slots are complete
   tc::pdl_launch_next();
   // LPI lanes per output item (row r, 4 columns): lane j sums the CSR sources
@@ -418,6 +420,103 @@ __global__ void __launch_bounds__(256) tc_reduce_kernel(const ReduceParams p) {
       s[sidx + 2] += w * w;
     }
   }
+  reduce_tail(p, s, scratch, am_last);
+}
+
+// One side of the tensor-core partial fold: `lp` lanes per output item (row r,
+// 4 columns); lane j sums the item's CSR sources e = j, j + lp, ... in batches
+// of 4 (all loads in flight), then the lp partial sums are combined by a fixed
+// butterfly.  lp is chosen per side from its source count (tall-skinny shapes
+// have many G^T U sources per column tile and few G.V sources per sub-band).
+__device__ __forceinline__ void tc_reduce_side(const ReduceParams& p, bool is_u, int lp,
+                                               double (&s)[6]) {
+  const int c4n = p.kst >> 2;
+  const int64_t rows = is_u ? p.m : p.n;
+  const int64_t n_items = rows * c4n;
+  const int ipw = 32 / lp;  // items per warp
+  const int j = threadIdx.x & (lp - 1);
+  const int64_t gtid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const int64_t stride = (int64_t(gridDim.x) * blockDim.x >> 5) * ipw;  // items per sweep
+  const float* part = reinterpret_cast<const float*>(is_u ? p.pleft : p.pright);
+  const int* off = is_u ? p.csr_u_off : p.csr_v_off;
+  const int* idxs = is_u ? p.csr_u_idx : p.csr_v_idx;
+  const int slot_rows = is_u ? 128 : p.gt_rows;
+  const int tile_rows = is_u ? 128 : 64;
+  const int tile_shift = is_u ? 7 : 6;
+  const bool two = !is_u && p.gt_rows == 128;  // gh part + gl part rows
+  const int64_t sst = int64_t(slot_rows) * p.kst;
+  const int64_t hoff = p.chunked ? int64_t(64) * 4 : int64_t(64) * p.kst;
+  const double sc = double(p.tc_unscale[is_u ? 0 : 1]);
+  for (int64_t w0 = (gtid >> 5) * ipw; w0 < n_items; w0 += stride) {
+    const int64_t q0 = w0 + ((threadIdx.x & 31) / lp);
+    const bool live = q0 < n_items;  // dead lanes still join the shuffles
+    const int64_t qq = live ? q0 : 0;
+    // chunked slots: consecutive items take consecutive rows of one chunk
+    const int64_t r = p.chunked ? qq % rows : qq / c4n;
+    const int c0 = int(p.chunked ? qq / rows : qq % c4n) * 4;
+    const int tile = int(r >> tile_shift);
+    const int e0 = off[tile], e1 = off[tile + 1];
+    const int64_t rr = r & (tile_rows - 1);
+    const float* base = p.chunked ? part + (int64_t(c0 >> 2) * slot_rows + rr) * 4
+                                  : part + rr * p.kst + c0;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (int eb = e0 + j; eb < e1; eb += 4 * lp) {
+      int id[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) id[u] = (eb + lp * u < e1) ? __ldg(idxs + eb + lp * u) : -1;
+      float4 v[4], w[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float* b0 = base + (id[u] >= 0 ? id[u] : 0) * sst;
+        v[u] = id[u] >= 0 ? *reinterpret_cast<const float4*>(b0) : make_float4(0.f, 0.f, 0.f, 0.f);
+        w[u] = (id[u] >= 0 && two) ? *reinterpret_cast<const float4*>(b0 + hoff)
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a0 += v[u].x; a1 += v[u].y; a2 += v[u].z; a3 += v[u].w;
+        a0 += w[u].x; a1 += w[u].y; a2 += w[u].z; a3 += w[u].w;
+      }
+    }
+    for (int o = 1; o < lp; o <<= 1) {
+      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+      a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+      a3 += __shfl_xor_sync(0xffffffffu, a3, o);
+    }
+    if (!live || j != 0) continue;
+    const double acc[4] = {a0 * sc, a1 * sc, a2 * sc, a3 * sc};
+    const int64_t obase = (is_u ? 0 : p.m * p.k) + r * p.k;
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int c = c0 + jj;
+      if (c >= p.k) break;
+      const int64_t o = obase + c;
+      if (is_u && p.u_mode == U_PARTIAL) {
+        reinterpret_cast<float*>(p.gu_part)[r * p.k + c] = float(acc[jj]);
+        continue;
+      }
+      double wv = p.z[o];
+      const double d = p.dz ? p.dz[o] : 0.0;
+      wv += p.alpha * d;
+      const double g = acc[jj] + p.lambda_l * wv;
+      p.g_out[o] = g;
+      const int sidx = is_u ? 0 : 3;
+      s[sidx] += g * g;
+      s[sidx + 1] += g * d;
+      s[sidx + 2] += wv * wv;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256, 4) tc_reduce_kernel(const ReduceParams p, int lp_u, int lp_v) {
+  tc::pdl_wait();  // the fused pass's partial slots are complete
+  tc::pdl_launch_next();
+  __shared__ double scratch[32];
+  __shared__ bool am_last;
+  double s[6] = {0, 0, 0, 0, 0, 0};
+  tc_reduce_side(p, true, lp_u, s);
+  tc_reduce_side(p, false, lp_v, s);
   reduce_tail(p, s, scratch, am_last);
 }
 

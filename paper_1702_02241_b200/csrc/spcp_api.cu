@@ -132,6 +132,7 @@ struct spcp_problem {
   CUtensorMap tc_xmap, tc_mmap;
   spcp::DevBuf tc_units, tc_begin, tc_csr, tc_uimg, tc_vimg, tc_scales;
   int64_t tc_csr_u_off = 0, tc_csr_u_idx = 0, tc_csr_v_off = 0, tc_csr_v_idx = 0;
+  int64_t tc_max_u_src = 0, tc_max_v_src = 0;  // largest CSR source lists (reduce sizing)
 };
 
 namespace spcp {
@@ -450,6 +451,10 @@ static int tc_build(spcp_problem* p) {
       }
     }
   }
+  p->tc_max_u_src = 0;
+  p->tc_max_v_src = 0;
+  for (auto& v : u_src) p->tc_max_u_src = std::max<int64_t>(p->tc_max_u_src, int64_t(v.size()));
+  for (auto& v : v_src) p->tc_max_v_src = std::max<int64_t>(p->tc_max_v_src, int64_t(v.size()));
   std::vector<int32_t> csr;
   p->tc_csr_u_off = 0;
   csr.push_back(0);
@@ -871,15 +876,32 @@ static int run_reduce(spcp_problem* p, int64_t k, int kp, int part_dtype, const 
     rp.tc_unscale = &p->tc_scales.as<TcScales>()->gv_unscale;
   }
   if (sh.tc && (u_mode == U_FULL || u_mode == U_PARTIAL) && v_mode) {
-#ifndef SPCP_REDUCE_LPI
-#define SPCP_REDUCE_LPI 2
-#endif
-    constexpr int LPI = SPCP_REDUCE_LPI;  // lanes per output item
+// lanes per output item from the largest source count of each side:
+    // about four partial loads per lane, a power of two in [1, 32]
+    auto lanes = [](int64_t loads) {
+      int lp = 1;
+      while (lp < 32 && loads > 4 * lp) lp <<= 1;
+      return lp;
+    };
+    const int lp_u = lanes(p->tc_max_u_src);
+    const int lp_v = lanes(p->tc_max_v_src * (sh.gt_rows == 128 ? 2 : 1));
     const int64_t items = (p->m + p->n) * (sh.kst / 4);
-    const int nb = int(std::min<int64_t>((items * LPI + 255) / 256, 148 * 8));
+    const int lp = std::max(lp_u, lp_v);
+    // balanced sources: one item space at 2 lanes per item (measured best for
+    // C2); skewed sources (tall-skinny C3 / C5 shards): per-side lane counts
+#ifdef SPCP_REDUCE_FORCE_LPI2
+    const bool skewed = false;
+#else
+    const bool skewed = std::max(lp_u, lp_v) >= 8 * std::min(lp_u, lp_v);  // C3: 1 vs 32
+#endif
+    const int lanes_used = skewed ? lp : 2;
+    const int nb = int(std::min<int64_t>((items * lanes_used + 255) / 256, 148 * 8));
     if ((rc = p->blk.ensure(size_t(nb) * 6 * sizeof(double)))) return rc;
     rp.blk = p->blk.as<double>();  // (ensure may have grown the buffer)
-    SPCP_CUDA(launch_pdl(tc_reduce_kernel<LPI>, dim3(nb), dim3(256), 0, p->stream, rp));
+    if (skewed)
+      SPCP_CUDA(launch_pdl(tc_reduce_kernel, dim3(nb), dim3(256), 0, p->stream, rp, lp_u, lp_v));
+    else
+      SPCP_CUDA(launch_pdl(tc_reduce_lpi_kernel<2>, dim3(nb), dim3(256), 0, p->stream, rp));
   }
   else if (part_dtype == SPCP_F32)
     reduce_kernel<float><<<nblk, 256, 0, p->stream>>>(rp);
