@@ -55,9 +55,15 @@ enum spcp_status {
   SPCP_ERR_NUMERICAL = 3,   /* NumericalError    (errors.py:12-13) */
   SPCP_ERR_CUDA = 4,        /* NumericalError subclass DeviceError: CUDA failure */
   SPCP_ERR_UNSUPPORTED = 5, /* ValueError: option not built into this library */
+  /* matrix files (matrixio.py:94-125, errors.py:29-44) */
+  SPCP_ERR_IO = 6,               /* MatrixIOError, code "io_error" (OS error) */
+  SPCP_ERR_MALFORMED_HEADER = 7, /* MalformedHeaderError "malformed_header" */
+  SPCP_ERR_TRUNCATED = 8,        /* TruncatedPayloadError "truncated_payload" */
+  SPCP_ERR_NONFINITE = 9,        /* NonFiniteDataError "non_finite_data" */
+  SPCP_ERR_NOT_FOUND = 10,       /* FileNotFoundError (open / mkstemp ENOENT) */
 };
 
-enum spcp_dtype { SPCP_F32 = 0, SPCP_F64 = 1 };
+enum spcp_dtype { SPCP_F32 = 0, SPCP_F64 = 1, SPCP_U8 = 2 /* mask bytes, SLRM reads only */ };
 
 /* storage flags for spcp_problem_create */
 #define SPCP_STORE_F32 1u
@@ -194,6 +200,33 @@ int spcp_matmul_small(spcp_problem* p, int64_t rows, int64_t pa, const double* a
 int spcp_prof_enable(spcp_problem* p, int on);
 int spcp_prof_read(spcp_problem* p, double* ms_total, int64_t* launches,
                    int64_t* kernels_launched);
+
+/* ---- SLRM matrix files straight to / from HBM (matrixio.py:25-113) --------
+ * Format: "SLRM", version u32 = 1, rows u64, cols u64 (little endian), then
+ * the row-major float64 payload.  The reader validates the header and the
+ * payload length before touching data (matrixio.py:94-109) and rejects NaN /
+ * Inf after the read (matrixio.py:124-125); writes go to a temp file in the
+ * target directory and are renamed into place (matrixio.py:40-50).
+ *
+ * header: rows / cols of an SLRM file (read_matrix's shape, matrixio.py:98).
+ * read_device: the window [row0, row0+rows) x [col0, col0+cols) (rows / cols
+ *   < 0 = to the end) into a device matrix dst (row stride ld elements) as
+ *   SPCP_F32, SPCP_F64 or SPCP_U8 (1 where the entry is non-zero: the CLI's
+ *   mask semantics, cli.py:165-167).  Row chunks are double-buffered through
+ *   pinned memory; a column window is how a rank reads its shard (§8(e)).
+ * write_device: a device matrix (SPCP_F32 widened, or SPCP_F64) to a file.
+ * write_product: L = U V^T and S* = shrink(X - L) on Omega (solver.py:313-320,
+ *   the decompose command's --output-l / --output-s, cli.py:256-259) streamed
+ *   from the problem to files (either path may be NULL); nnz_s (may be NULL)
+ *   receives the trace's "nnz_s" (cli.py:268). */
+int spcp_slrm_header(const char* path, int64_t* rows, int64_t* cols);
+int spcp_slrm_read_device(const char* path, int device, int64_t row0, int64_t rows,
+                          int64_t col0, int64_t cols, void* dst, int dst_dtype, int64_t ld,
+                          void* stream);
+int spcp_slrm_write_device(const char* path, int device, const void* src, int src_dtype,
+                           int64_t rows, int64_t cols, int64_t ld, void* stream);
+int spcp_slrm_write_product(spcp_problem* p, int64_t k, const double* z, const char* l_path,
+                            const char* s_path, int64_t* nnz_s);
 
 #ifdef __cplusplus
 }

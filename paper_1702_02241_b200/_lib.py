@@ -8,16 +8,25 @@ importing the compute path raises immediately.
 import ctypes
 import os
 
-from .errors import DeviceError, DimensionError, NumericalError
+from .errors import (
+    DeviceError,
+    DimensionError,
+    MalformedHeaderError,
+    MatrixIOError,
+    NonFiniteDataError,
+    NumericalError,
+    TruncatedPayloadError,
+)
 
-__all__ = ["lib", "check", "LIB_PATH", "SPCP_F32", "SPCP_F64", "STORE_F32", "STORE_F64",
-           "EXPORTS"]
+__all__ = ["lib", "check", "LIB_PATH", "SPCP_F32", "SPCP_F64", "SPCP_U8", "STORE_F32",
+           "STORE_F64", "EXPORTS"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libspcp_b200.so")
 
 SPCP_OK, SPCP_ERR_VALUE, SPCP_ERR_DIMENSION, SPCP_ERR_NUMERICAL, SPCP_ERR_CUDA, \
-    SPCP_ERR_UNSUPPORTED = range(6)
-SPCP_F32, SPCP_F64 = 0, 1
+    SPCP_ERR_UNSUPPORTED, SPCP_ERR_IO, SPCP_ERR_MALFORMED_HEADER, SPCP_ERR_TRUNCATED, \
+    SPCP_ERR_NONFINITE, SPCP_ERR_NOT_FOUND = range(11)
+SPCP_F32, SPCP_F64, SPCP_U8 = 0, 1, 2
 STORE_F32, STORE_F64 = 1, 2
 
 _i64, _i32, _u32 = ctypes.c_int64, ctypes.c_int, ctypes.c_uint
@@ -51,6 +60,12 @@ EXPORTS = {
     "spcp_matmul_small": [_vp, _i64, _i64, _vp, _i64, _dp, _vp],
     "spcp_prof_enable": [_vp, _i32],
     "spcp_prof_read": [_vp, _dp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)],
+    "spcp_slrm_header": [ctypes.c_char_p, ctypes.POINTER(_i64), ctypes.POINTER(_i64)],
+    "spcp_slrm_read_device": [ctypes.c_char_p, _i32, _i64, _i64, _i64, _i64, _vp, _i32, _i64,
+                              _vp],
+    "spcp_slrm_write_device": [ctypes.c_char_p, _i32, _vp, _i32, _i64, _i64, _i64, _vp],
+    "spcp_slrm_write_product": [_vp, _i64, _vp, ctypes.c_char_p, ctypes.c_char_p,
+                                ctypes.POINTER(_i64)],
 }
 
 
@@ -83,4 +98,10 @@ def check(rc):
         raise ValueError(msg)
     if rc == SPCP_ERR_CUDA:
         raise DeviceError(msg)
+    if rc == SPCP_ERR_NOT_FOUND:
+        raise FileNotFoundError(msg)
+    io = {SPCP_ERR_IO: MatrixIOError, SPCP_ERR_MALFORMED_HEADER: MalformedHeaderError,
+          SPCP_ERR_TRUNCATED: TruncatedPayloadError, SPCP_ERR_NONFINITE: NonFiniteDataError}
+    if rc in io:
+        raise io[rc](msg)
     raise NumericalError(msg)

@@ -1545,3 +1545,4 @@ int spcp_prof_read(spcp_problem* p, double* ms_total, int64_t* launches, int64_t
 }
 
 }  // extern "C"
+#include "slrm_io.cuh"

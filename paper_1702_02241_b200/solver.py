@@ -357,6 +357,10 @@ def solve_split_spcp(spec, k, cfg=None, init="rsvd", iter_hook=None, timer=None,
              "precision": precision}
     if switches:
         extra["fp64_switch_iter"] = switches
-    return SolveReport(solver="split", termination=best["termination"], iterations=records,
-                       l=dense("l"), s=dense("s"), objective=best["objective"],
-                       factors=factors, extra=extra)
+    report = SolveReport(solver="split", termination=best["termination"], iterations=records,
+                         l=dense("l"), s=dense("s"), objective=best["objective"],
+                         factors=factors, extra=extra)
+    # the device iterate stays reachable so L and S can be streamed to files
+    # without host m x n arrays (matrixio.write_decomposition)
+    report.device_state = (dp, kf, zf)
+    return report

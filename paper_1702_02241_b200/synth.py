@@ -22,7 +22,8 @@ import math
 
 import numpy as np
 
-__all__ = ["gen_low_rank_plus_sparse_device", "factor_draw"]
+__all__ = ["gen_low_rank_plus_sparse", "gen_mask", "gen_low_rank_plus_sparse_device",
+           "factor_draw"]
 
 
 def factor_draw(m, n_total, rank, seed):
@@ -31,6 +32,54 @@ def factor_draw(m, n_total, rank, seed):
     a = gen.standard_normal((m, rank))
     b = gen.standard_normal((n_total, rank))
     return a, b
+
+
+def gen_low_rank_plus_sparse(m, n, rank, sparse_frac, noise_rel, seed=0):
+    """(x, l_ref, s_ref) on the host, byte-identical to synth.py:13-57 for a
+    seed: the same PCG64 draws in the same order (A, B, outlier positions and
+    values, noise field) and the exact noise ratio, from the positive root of
+    |a z|^2 = rho^2 |clean + a z|^2.  Feeds the CLI's `synth` command; the
+    benchmark shapes use the device generator below."""
+    m, n, rank = int(m), int(n), int(rank)
+    if rank < 0 or rank > min(m, n):
+        raise ValueError(f"rank={rank} out of range [0, {min(m, n)}]")
+    if not 0.0 <= sparse_frac <= 1.0:
+        raise ValueError(f"sparse_frac={sparse_frac} out of range [0, 1]")
+    if not 0.0 <= noise_rel < 1.0:
+        raise ValueError(f"noise_rel={noise_rel} out of range [0, 1)")
+    gen = np.random.default_rng(seed)
+    a = gen.standard_normal((m, rank))
+    b = gen.standard_normal((n, rank))
+    l_ref = a @ b.T
+    s_ref = np.zeros((m, n))
+    count = int(round(sparse_frac * m * n))
+    if count:
+        where = gen.choice(m * n, size=count, replace=False)
+        s_ref.reshape(-1)[where] = gen.standard_normal(count)
+    clean = l_ref + s_ref
+    if noise_rel == 0.0:
+        return clean.copy(), l_ref, s_ref
+    noise = gen.standard_normal((m, n))
+    r2 = noise_rel * noise_rel
+    nn = float(np.sum(noise * noise))
+    nc = float(np.sum(clean * noise))
+    cc = float(np.sum(clean * clean))
+    qa, qb, qc = nn * (1.0 - r2), -2.0 * r2 * nc, -r2 * cc
+    scale = (-qb + np.sqrt(qb * qb - 4.0 * qa * qc)) / (2.0 * qa)
+    return clean + scale * noise, l_ref, s_ref
+
+
+def gen_mask(m, n, observe_frac, seed=0):
+    """Exactly round(observe_frac m n) observed positions, uniform without
+    replacement (synth.py:60-73)."""
+    m, n = int(m), int(n)
+    if not 0.0 < observe_frac <= 1.0:
+        raise ValueError(f"observe_frac={observe_frac} out of range (0, 1]")
+    hits = np.random.default_rng(seed).choice(m * n, size=int(round(observe_frac * m * n)),
+                                              replace=False)
+    mask = np.zeros(m * n, dtype=bool)
+    mask[hits] = True
+    return mask.reshape(m, n)
 
 
 def gen_low_rank_plus_sparse_device(m, n, rank, sparse_frac, noise_rel, seed=0, col0=0,

@@ -202,8 +202,75 @@ def gen_synth(spcp):
                         mask=mask, rsvd_u=u, rsvd_s=s, rsvd_v=v)
 
 
+def gen_io(spcp):
+    """SLRM / CSV bytes written by the reference writer, and reference CLI runs
+    (decompose with trace + outputs, certify) on small synthetic problems."""
+    import contextlib
+    import io
+    import json
+    import tempfile
+
+    from spcp import cli as refcli
+
+    out = {}
+    awk = np.array([[0.0, -0.0, 1e-308], [np.pi, -2**53 + 1.0, 5e300]])
+    rnd = np.random.default_rng(110).standard_normal((7, 3))
+    with tempfile.TemporaryDirectory() as td:
+        for tag, a in (("awk", awk), ("rnd", rnd)):
+            for ext in ("bin", "csv"):
+                path = os.path.join(td, f"{tag}.{ext}")
+                spcp.write_matrix(a, path)
+                out[f"{tag}_{ext}"] = np.frombuffer(open(path, "rb").read(), np.uint8)
+            out[f"{tag}_mat"] = a
+        runs = {
+            "full": dict(m=80, n=60, rank=3, obs=None, lam_l=2.0, k=5, cert="final"),
+            "mask": dict(m=80, n=60, rank=3, obs=0.6, lam_l=1.0, k=4, cert="every:3"),
+        }
+        for tag, r in runs.items():
+            xp = os.path.join(td, f"{tag}_x.bin")
+            argv = ["synth", "--m", str(r["m"]), "--n", str(r["n"]), "--rank", str(r["rank"]),
+                    "--sparse-frac", "0.05", "--noise-rel", "1e-3", "--seed", "0",
+                    "--output-x", xp]
+            if r["obs"]:
+                argv += ["--observe-frac", str(r["obs"]), "--output-mask",
+                         os.path.join(td, f"{tag}_m.bin")]
+            assert refcli.main(argv) == 0
+            dec = ["decompose", "--input", xp, "--lambda-l", str(r["lam_l"]), "--lambda-s",
+                   "0.1", "--k", str(r["k"]), "--certificate", r["cert"],
+                   "--output-l", os.path.join(td, f"{tag}_l.bin"),
+                   "--output-s", os.path.join(td, f"{tag}_s.bin"),
+                   "--trace", os.path.join(td, f"{tag}_trace.json")]
+            if r["obs"]:
+                dec += ["--mask", os.path.join(td, f"{tag}_m.bin")]
+            buf = io.StringIO()
+            with contextlib.redirect_stdout(buf):
+                code = refcli.main(dec)
+            out[f"{tag}_x"] = np.frombuffer(open(xp, "rb").read(), np.uint8)
+            out[f"{tag}_exit"] = np.array(code)
+            out[f"{tag}_stdout"] = np.array(buf.getvalue())
+            out[f"{tag}_args"] = np.array(json.dumps(dec[3:]).replace(td + "/", ""))
+            out[f"{tag}_l"] = spcp.read_matrix(os.path.join(td, f"{tag}_l.bin"))
+            out[f"{tag}_s"] = spcp.read_matrix(os.path.join(td, f"{tag}_s.bin"))
+            out[f"{tag}_trace"] = np.array(open(os.path.join(td, f"{tag}_trace.json")).read())
+            if r["obs"]:
+                out[f"{tag}_m"] = np.frombuffer(
+                    open(os.path.join(td, f"{tag}_m.bin"), "rb").read(), np.uint8)
+            cj = os.path.join(td, f"{tag}_cert.json")
+            cert = ["certify", "--input", xp, "--lambda-l", str(r["lam_l"]), "--lambda-s", "0.1",
+                    "--l", os.path.join(td, f"{tag}_l.bin"), "--output", cj]
+            if r["obs"]:
+                cert += ["--mask", os.path.join(td, f"{tag}_m.bin")]
+            with contextlib.redirect_stdout(io.StringIO()):
+                assert refcli.main(cert) == 0
+            out[f"{tag}_cert"] = np.array(open(cj).read())
+    np.savez_compressed(os.path.join(OUT, "io.npz"), **out)
+
+
 if __name__ == "__main__":
     ref = _ref()
-    for fn in (gen_phi, gen_split, gen_lbfgs, gen_solve, gen_cert, gen_synth, gen_c1):
+    only = sys.argv[1:]
+    for fn in (gen_phi, gen_split, gen_lbfgs, gen_solve, gen_cert, gen_synth, gen_c1, gen_io):
+        if only and fn.__name__ not in only:
+            continue
         fn(ref)
         print("wrote", fn.__name__)
