@@ -342,6 +342,16 @@ def time_to_certificate(dev):
     from paper_1702_02241_b200 import ProblemSpec, SolverConfig, certificate, solve_split_spcp
     from paper_1702_02241_b200.synth import gen_low_rank_plus_sparse_device
 
+    # one-time library/workspace initialisation (cuSOLVER/cuBLAS handles, the
+    # certificate's fp32 product workspaces) on a separate small problem that
+    # still takes the mixed-precision solve and subspace-certificate paths; the
+    # C2 problem itself is not touched before the clock starts
+    xw = gen_low_rank_plus_sparse_device(4200, 4200, 5, 0.05, 1e-3, seed=1)
+    sw = ProblemSpec(x=xw, lambda_l=4.0, lambda_s=LAM_S)
+    rw = solve_split_spcp(sw, 5, SolverConfig(max_iter=20))
+    certificate(rw.factors, sw, f_bound_hint=rw.best_objective)
+    sw.release_device()
+    del xw, sw, rw
     x = gen_low_rank_plus_sparse_device(M, N_COLS, RANK, 0.05, 1e-3, seed=0)
     spec = ProblemSpec(x=x, lambda_l=LAM_L, lambda_s=LAM_S)
     spec.device("mixed")

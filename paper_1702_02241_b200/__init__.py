@@ -8,6 +8,9 @@ The compute path is libspcp_b200.so (CUDA, sm_100a); importing a compute
 entry point without the built library raises — there is no CPU fallback.
 """
 
+import sys as _sys
+import types as _types
+
 from .errors import (
     DeviceError,
     DimensionError,
@@ -46,6 +49,20 @@ __all__ = sorted(list(_LAZY) + [
     "NonFiniteDataError", "NumericalError", "PowerIterationError", "SpcpError",
     "TruncatedPayloadError", "IterateState", "IterationRecord", "SolveReport", "WorkTimer",
     "as_mask", "as_matrix", "check_rank_bound"])
+
+
+class _Package(_types.ModuleType):
+    """The `certificate` submodule shares its name with the `certificate`
+    function (the reference package exports the function); importing the
+    submodule must not replace the package attribute with the module."""
+
+    def __setattr__(self, name, value):
+        if name == "certificate" and isinstance(value, _types.ModuleType):
+            value = value.certificate
+        super().__setattr__(name, value)
+
+
+_sys.modules[__name__].__class__ = _Package
 
 
 def __getattr__(name):

@@ -252,3 +252,14 @@ def test_cli_threads_env(monkeypatch):
     monkeypatch.setenv("SPCP_NUM_THREADS", "3")
     cli._threads_from_env()
     assert os.environ["OMP_NUM_THREADS"] == "3" and os.environ["OPENBLAS_NUM_THREADS"] == "3"
+
+
+def test_certificate_attribute_is_the_function_after_submodule_import():
+    import importlib
+    import inspect
+
+    importlib.import_module("paper_1702_02241_b200.certificate")
+    import paper_1702_02241_b200 as api
+
+    assert inspect.isfunction(api.certificate)
+    assert api.certificate.__name__ == "certificate"

@@ -8,7 +8,8 @@ import torch
 
 sys.path.insert(0, ".")
 from paper_1702_02241_b200 import ProblemSpec, SolverConfig, certificate, solve_split_spcp  # noqa
-from paper_1702_02241_b200 import certificate as cmod  # noqa
+import importlib  # noqa
+cmod = importlib.import_module("paper_1702_02241_b200.certificate")  # noqa
 from paper_1702_02241_b200.synth import gen_low_rank_plus_sparse_device  # noqa
 
 x = gen_low_rank_plus_sparse_device(20000, 20000, 20, 0.05, 1e-3, seed=0)
