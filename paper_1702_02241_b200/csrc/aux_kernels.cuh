@@ -165,11 +165,25 @@ struct ReduceParams {
 
 // Block partials of the six vector sums -> the last block folds them (and the
 // phi partials) in a fixed order into the scalar outputs.
+// `scratch` holds 6 * 32 doubles.  The six block sums share one barrier; each
+// follows block_sum's tree (warp butterfly, then warp 0 over the warp sums).
 __device__ __forceinline__ void reduce_tail(const ReduceParams& p, const double (&s)[6],
                                             double* scratch, bool& am_last) {
-  for (int r = 0; r < 6; ++r) {
-    const double v = block_sum(s[r], scratch);
-    if (threadIdx.x == 0) p.blk[blockIdx.x * 6 + r] = v;
+  {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int r = 0; r < 6; ++r) {
+      const double v = warp_sum(s[r]);
+      if (lane == 0) scratch[r * 32 + w] = v;
+    }
+    __syncthreads();
+    if (w == 0) {
+#pragma unroll
+      for (int r = 0; r < 6; ++r) {
+        const double v = warp_sum(lane < nw ? scratch[r * 32 + lane] : 0.0);
+        if (lane == 0) p.blk[blockIdx.x * 6 + r] = v;
+      }
+    }
   }
   // last block folds the block partials in a fixed order
   __threadfence();
@@ -227,7 +241,7 @@ __device__ __forceinline__ void reduce_tail(const ReduceParams& p, const double 
 
 template <typename T>
 __global__ void __launch_bounds__(256) reduce_kernel(const ReduceParams p) {
-  __shared__ double scratch[32];
+  __shared__ double scratch[6 * 32];
   __shared__ bool am_last;
   const int64_t nu = p.m * p.k, nv = p.n * p.k;
   double s[6] = {0, 0, 0, 0, 0, 0};
@@ -311,7 +325,7 @@ __global__ void __launch_bounds__(256) tc_reduce_lpi_kernel(const ReduceParams p
   // LPI lanes per output item (row r, 4 columns): lane j sums the CSR sources
   // e = j, j + LPI, ... of the item (all its loads in flight at once), then the
   // LPI partial sums are combined in a fixed butterfly order.
-  __shared__ double scratch[32];
+  __shared__ double scratch[6 * 32];
   __shared__ bool am_last;
   const int c4n = p.kst >> 2;
   const int64_t nu4 = p.m * c4n, nv4 = p.n * c4n;
@@ -512,7 +526,7 @@ __device__ __forceinline__ void tc_reduce_side(const ReduceParams& p, bool is_u,
 __global__ void __launch_bounds__(256, 4) tc_reduce_kernel(const ReduceParams p, int lp_u, int lp_v) {
   tc::pdl_wait();  // the fused pass's partial slots are complete
   tc::pdl_launch_next();
-  __shared__ double scratch[32];
+  __shared__ double scratch[6 * 32];
   __shared__ bool am_last;
   double s[6] = {0, 0, 0, 0, 0, 0};
   tc_reduce_side(p, true, lp_u, s);

@@ -895,7 +895,20 @@ static int run_reduce(spcp_problem* p, int64_t k, int kp, int part_dtype, const 
     const bool skewed = std::max(lp_u, lp_v) >= 8 * std::min(lp_u, lp_v);  // C3: 1 vs 32
 #endif
     const int lanes_used = skewed ? lp : 2;
-    const int nb = int(std::min<int64_t>((items * lanes_used + 255) / 256, 148 * 8));
+    // one wave of resident blocks (grid-stride over the items): a partial
+    // second wave left ~1/3 of the SM time idle (ncu, C2)
+    static int resident[2] = {0, 0};
+    int& res = resident[skewed ? 1 : 0];
+    if (!res) {
+      int per_sm = 0;
+      cudaError_t e = skewed ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                                   &per_sm, tc_reduce_kernel, 256, 0)
+                             : cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                                   &per_sm, tc_reduce_lpi_kernel<2>, 256, 0);
+      if (e != cudaSuccess || per_sm < 1) per_sm = 4;
+      res = per_sm * kSMs;
+    }
+    const int nb = int(std::min<int64_t>((items * lanes_used + 255) / 256, res));
     if ((rc = p->blk.ensure(size_t(nb) * 6 * sizeof(double)))) return rc;
     rp.blk = p->blk.as<double>();  // (ensure may have grown the buffer)
     if (skewed)
