@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(256) tc_reduce_lpi_kernel(const ReduceParams p
   for (int64_t w0 = (gtid >> 5) * IPW; w0 < n_items; w0 += stride) {
     const int64_t q0 = w0 + ((threadIdx.x & 31) / LPI);
     const bool live = q0 < n_items;  // dead lanes still join the shuffles
-    const int64_t q = live ? q0 : 0;
+    const int64_t q = live ? q0 : w0;  // dead lanes shadow lane 0's item
     const bool is_u = q < nu4;
     const int64_t qq = is_u ? q : q - nu4;
     // chunked slots: consecutive items take consecutive rows of one 4-column
@@ -350,20 +350,39 @@ __global__ void __launch_bounds__(256) tc_reduce_lpi_kernel(const ReduceParams p
     const int64_t rows = is_u ? p.m : p.n;
     const int64_t r = p.chunked ? qq % rows : qq / c4n;
     const int c0 = int(p.chunked ? qq / rows : qq % c4n) * 4;
+    // warp-uniform source list (every item of the warp in one sub-band / one
+    // column tile, <= 32 sources): one coalesced load of the CSR indices, then
+    // shuffles, so each batch is a single dependent memory round trip
+    const int tile = is_u ? int(r >> 7) : int(r >> 6);
+    const int* coff = is_u ? p.csr_u_off : p.csr_v_off;
+    const int e0 = coff[tile], e1 = coff[tile + 1];
+    const int key = is_u ? tile : -1 - tile;
+    const bool uni = __all_sync(0xffffffffu, key == __shfl_sync(0xffffffffu, key, 0)) &&
+                     e1 - e0 <= 32;
+    int lidx = -1;
+    if (uni) {
+      const int lane = threadIdx.x & 31;
+      lidx = lane < e1 - e0 ? __ldg((is_u ? p.csr_u_idx : p.csr_v_idx) + e0 + lane) : -1;
+    }
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     if (is_u) {
-      const int sb = int(r >> 7);
-      const int e0 = p.csr_u_off[sb], e1 = p.csr_u_off[sb + 1];
       const float* base = p.chunked ? plf + (int64_t(c0 >> 2) * 128 + (r & 127)) * 4
                                     : plf + (r & 127) * p.kst + c0;
       const int64_t sst = int64_t(128) * p.kst;
       // batches of 8 sources per lane: the 8 index loads, then the 8 data
-      // loads are all in flight before the (in-order) adds
-      for (int eb = e0 + j; eb < e1; eb += 8 * LPI) {
+      // loads are all in flight before the (in-order) adds.  Uniform warps run
+      // the same trip count on every lane (shuffles need all 32 lanes).
+      const int ebeg = uni ? e0 : e0 + j;
+      for (int eb = ebeg; eb < e1; eb += 8 * LPI) {
         int idx[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-          idx[u] = (eb + LPI * u < e1) ? __ldg(p.csr_u_idx + eb + LPI * u) : -1;
+        {
+          // source e (absolute CSR position) of this lane's batch slot
+          const int e = eb + (uni ? j : 0) + LPI * u;
+          const int sh = uni ? __shfl_sync(0xffffffffu, lidx, (e - e0) & 31) : -1;
+          idx[u] = e < e1 ? (uni ? sh : __ldg(p.csr_u_idx + e)) : -1;
+        }
         float4 v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u)
@@ -375,18 +394,22 @@ __global__ void __launch_bounds__(256) tc_reduce_lpi_kernel(const ReduceParams p
         }
       }
     } else {
-      const int tcol = int(r >> 6);
-      const int e0 = p.csr_v_off[tcol], e1 = p.csr_v_off[tcol + 1];
       const float* base = p.chunked ? prf + (int64_t(c0 >> 2) * p.gt_rows + (r & 63)) * 4
                                     : prf + (r & 63) * p.kst + c0;
       const int64_t sst = int64_t(p.gt_rows) * p.kst;
       const int64_t hoff = p.chunked ? int64_t(64) * 4 : int64_t(64) * p.kst;
       const bool two = p.gt_rows == 128;
-      for (int eb = e0 + j; eb < e1; eb += 4 * LPI) {
+      const int ebeg = uni ? e0 : e0 + j;
+      for (int eb = ebeg; eb < e1; eb += 4 * LPI) {
         int idx[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-          idx[u] = (eb + LPI * u < e1) ? __ldg(p.csr_v_idx + eb + LPI * u) : -1;
+        {
+          // source e (absolute CSR position) of this lane's batch slot
+          const int e = eb + (uni ? j : 0) + LPI * u;
+          const int sh = uni ? __shfl_sync(0xffffffffu, lidx, (e - e0) & 31) : -1;
+          idx[u] = e < e1 ? (uni ? sh : __ldg(p.csr_v_idx + e)) : -1;
+        }
         float4 v[4], w[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
