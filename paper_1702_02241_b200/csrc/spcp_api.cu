@@ -1291,8 +1291,11 @@ int spcp_split_objective_host(spcp_problem* p, int64_t k, int dtype, const doubl
     z = z2;
     g = z2 + nu + nv;
   }
-  if ((rc = spcp_eval(p, k, dtype, z, nullptr, 0.0, g, out))) return rc;
-  *value = out[0];
+  // one stream synchronisation per call: the scalars and both gradient blocks
+  // are queued behind the evaluation together (no host round trip between)
+  if ((rc = eval_impl(p, k, dtype, z, nullptr, 0.0, g, U_FULL, nullptr, nullptr))) return rc;
+  SPCP_CUDA(cudaMemcpyAsync(p->host_out, p->out_dev.ptr, 8 * sizeof(double),
+                            cudaMemcpyDeviceToHost, p->stream));
   if (grad_u)
     SPCP_CUDA(cudaMemcpyAsync(grad_u, g, size_t(nu) * sizeof(double), cudaMemcpyDeviceToHost,
                               p->stream));
@@ -1300,6 +1303,9 @@ int spcp_split_objective_host(spcp_problem* p, int64_t k, int dtype, const doubl
     SPCP_CUDA(cudaMemcpyAsync(grad_v, g + nu, size_t(nv) * sizeof(double),
                               cudaMemcpyDeviceToHost, p->stream));
   SPCP_CUDA(cudaStreamSynchronize(p->stream));
+  if (p->prof && p->ev_count && prof_collect(p)) return SPCP_ERR_CUDA;
+  std::memcpy(out, p->host_out, 8 * sizeof(double));
+  *value = out[0];
   return SPCP_OK;
 }
 
