@@ -194,3 +194,48 @@ def test_write_decomposition_streams_what_report_holds(tmp_path):
     assert read_matrix(tmp_path / "s.bin").tobytes() == rep.s.tobytes()
     assert nnz == int(np.count_nonzero(rep.s))
     assert write_decomposition(rep) == nnz
+
+
+def test_column_shards_read_from_file_match_unsharded(torch, tmp_path):
+    """Each rank of the column-sharded mode reads only its own
+    X / mask columns from the SLRM files (`col0` / `cols` windows, streamed to
+    HBM) and the partial -> all-reduce (by hand, one GPU) -> finish evaluation
+    matches the unsharded problem read whole."""
+    from paper_1702_02241_b200._lib import SPCP_F32
+    from paper_1702_02241_b200.device import DeviceProblem
+    from paper_1702_02241_b200.matrixio import read_mask, read_matrix, write_matrix
+
+    rng = np.random.default_rng(77)
+    m, n, k = 900, 1000, 12
+    x = rng.standard_normal((m, n)).astype(np.float32).astype(np.float64) * 2.0
+    mask = rng.random((m, n)) < 0.6
+    write_matrix(x, tmp_path / "x.bin")
+    write_matrix(mask.astype(float), tmp_path / "m.bin")
+    ll, ls = 1.3, 0.3
+    full = DeviceProblem(read_matrix(tmp_path / "x.bin", device="cuda", dtype=torch.float32),
+                         ll, ls, mask=read_mask(tmp_path / "m.bin", device="cuda"))
+    z = torch.from_numpy(rng.standard_normal((m + n) * k) / np.sqrt(k)).cuda()
+    dz = torch.from_numpy(rng.standard_normal((m + n) * k) * 1e-2).cuda()
+    g_full = torch.empty_like(z)
+    out_full = full.eval(k, SPCP_F32, z, dz, 0.25, g_full)
+    parts = []
+    for c0, c1 in ((0, 384), (384, 700), (700, n)):
+        xs = read_matrix(tmp_path / "x.bin", device="cuda", dtype=torch.float32, col0=c0,
+                         cols=c1 - c0)
+        ms = read_mask(tmp_path / "m.bin", device="cuda", col0=c0, cols=c1 - c0)
+        dp = DeviceProblem(xs, ll, ls, mask=ms, n_total=n, col0=c0)
+        zs = torch.cat([z[: m * k], z[m * k + c0 * k: m * k + c1 * k]])
+        dzs = torch.cat([dz[: m * k], dz[m * k + c0 * k: m * k + c1 * k]])
+        gu = torch.empty((m, k), dtype=torch.float32, device="cuda")
+        scal = torch.empty(4, dtype=torch.float64, device="cuda")
+        gs = torch.empty_like(zs)
+        dp.eval_partial(k, SPCP_F32, zs, dzs, 0.25, gu, scal, gs)
+        parts.append((dp, zs, dzs, gu, scal, gs, c0, c1))
+    gu_sum = sum(pt[3].double() for pt in parts).float()
+    scal_sum = sum(pt[4] for pt in parts)
+    for dp, zs, dzs, _, _, gs, c0, c1 in parts:
+        out = dp.eval_finish(k, SPCP_F32, zs, dzs, 0.25, gu_sum, scal_sum, gs)
+        assert out[0] == pytest.approx(out_full[0], rel=1e-5)
+        assert rel(gs[: m * k].cpu().numpy(), g_full[: m * k].cpu().numpy()) <= 1e-5
+        assert rel(gs[m * k:].cpu().numpy(),
+                   g_full[m * k + c0 * k: m * k + c1 * k].cpu().numpy()) <= 1e-5
