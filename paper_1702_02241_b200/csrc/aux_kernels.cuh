@@ -348,8 +348,12 @@ __global__ void __launch_bounds__(256) tc_reduce_lpi_kernel(const ReduceParams p
     // chunked slots: consecutive items take consecutive rows of one 4-column
     // chunk (contiguous float4 reads); row-major slots: consecutive chunks of a row
     const int64_t rows = is_u ? p.m : p.n;
-    const int64_t r = p.chunked ? qq % rows : qq / c4n;
-    const int c0 = int(p.chunked ? qq / rows : qq % c4n) * 4;
+    // 32-bit index split (items < 2^31: the TC path caps m, n at 65535 tiles):
+    // a 64-bit div/mod pair per item was a large share of the instructions
+    const uint32_t q32 = uint32_t(qq), d32 = p.chunked ? uint32_t(rows) : uint32_t(c4n);
+    const uint32_t quo = q32 / d32, rem = q32 - quo * d32;
+    const int64_t r = p.chunked ? rem : quo;
+    const int c0 = int(p.chunked ? quo : rem) * 4;
     // warp-uniform source list (every item of the warp in one sub-band / one
     // column tile, <= 32 sources): one coalesced load of the CSR indices, then
     // shuffles, so each batch is a single dependent memory round trip
@@ -489,8 +493,12 @@ __device__ __forceinline__ void tc_reduce_side(const ReduceParams& p, bool is_u,
     const bool live = q0 < n_items;  // dead lanes still join the shuffles
     const int64_t qq = live ? q0 : 0;
     // chunked slots: consecutive items take consecutive rows of one chunk
-    const int64_t r = p.chunked ? qq % rows : qq / c4n;
-    const int c0 = int(p.chunked ? qq / rows : qq % c4n) * 4;
+    // 32-bit index split (items < 2^31: the TC path caps m, n at 65535 tiles):
+    // a 64-bit div/mod pair per item was a large share of the instructions
+    const uint32_t q32 = uint32_t(qq), d32 = p.chunked ? uint32_t(rows) : uint32_t(c4n);
+    const uint32_t quo = q32 / d32, rem = q32 - quo * d32;
+    const int64_t r = p.chunked ? rem : quo;
+    const int c0 = int(p.chunked ? quo : rem) * 4;
     const int tile = int(r >> tile_shift);
     const int e0 = off[tile], e1 = off[tile + 1];
     const int64_t rr = r & (tile_rows - 1);
