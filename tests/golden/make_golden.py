@@ -225,9 +225,14 @@ def gen_io(spcp):
         runs = {
             "full": dict(m=80, n=60, rank=3, obs=None, lam_l=2.0, k=5, cert="final"),
             "mask": dict(m=80, n=60, rank=3, obs=0.6, lam_l=1.0, k=4, cert="every:3"),
+            # cli.py rank growth (test_cli.py:164-183 shape) and a CSV input/output run
+            "grow": dict(m=60, n=48, rank=3, obs=None, lam_l=1.5, k=1, cert="final",
+                         extra=["--rank-growth", "--max-k", "5", "--max-iter", "2000"]),
+            "csv": dict(m=40, n=30, rank=2, obs=None, lam_l=1.0, k=3, cert="final", ext="csv"),
         }
         for tag, r in runs.items():
-            xp = os.path.join(td, f"{tag}_x.bin")
+            ext = r.get("ext", "bin")
+            xp = os.path.join(td, f"{tag}_x.{ext}")
             argv = ["synth", "--m", str(r["m"]), "--n", str(r["n"]), "--rank", str(r["rank"]),
                     "--sparse-frac", "0.05", "--noise-rel", "1e-3", "--seed", "0",
                     "--output-x", xp]
@@ -237,9 +242,9 @@ def gen_io(spcp):
             assert refcli.main(argv) == 0
             dec = ["decompose", "--input", xp, "--lambda-l", str(r["lam_l"]), "--lambda-s",
                    "0.1", "--k", str(r["k"]), "--certificate", r["cert"],
-                   "--output-l", os.path.join(td, f"{tag}_l.bin"),
-                   "--output-s", os.path.join(td, f"{tag}_s.bin"),
-                   "--trace", os.path.join(td, f"{tag}_trace.json")]
+                   "--output-l", os.path.join(td, f"{tag}_l.{ext}"),
+                   "--output-s", os.path.join(td, f"{tag}_s.{ext}"),
+                   "--trace", os.path.join(td, f"{tag}_trace.json")] + r.get("extra", [])
             if r["obs"]:
                 dec += ["--mask", os.path.join(td, f"{tag}_m.bin")]
             buf = io.StringIO()
@@ -249,15 +254,15 @@ def gen_io(spcp):
             out[f"{tag}_exit"] = np.array(code)
             out[f"{tag}_stdout"] = np.array(buf.getvalue())
             out[f"{tag}_args"] = np.array(json.dumps(dec[3:]).replace(td + "/", ""))
-            out[f"{tag}_l"] = spcp.read_matrix(os.path.join(td, f"{tag}_l.bin"))
-            out[f"{tag}_s"] = spcp.read_matrix(os.path.join(td, f"{tag}_s.bin"))
+            out[f"{tag}_l"] = spcp.read_matrix(os.path.join(td, f"{tag}_l.{ext}"))
+            out[f"{tag}_s"] = spcp.read_matrix(os.path.join(td, f"{tag}_s.{ext}"))
             out[f"{tag}_trace"] = np.array(open(os.path.join(td, f"{tag}_trace.json")).read())
             if r["obs"]:
                 out[f"{tag}_m"] = np.frombuffer(
                     open(os.path.join(td, f"{tag}_m.bin"), "rb").read(), np.uint8)
             cj = os.path.join(td, f"{tag}_cert.json")
             cert = ["certify", "--input", xp, "--lambda-l", str(r["lam_l"]), "--lambda-s", "0.1",
-                    "--l", os.path.join(td, f"{tag}_l.bin"), "--output", cj]
+                    "--l", os.path.join(td, f"{tag}_l.{ext}"), "--output", cj]
             if r["obs"]:
                 cert += ["--mask", os.path.join(td, f"{tag}_m.bin")]
             with contextlib.redirect_stdout(io.StringIO()):

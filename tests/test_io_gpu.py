@@ -122,25 +122,28 @@ def _run(argv):
     return code, out.getvalue(), err.getvalue()
 
 
-@pytest.mark.parametrize("tag", ["full", "mask"])
+@pytest.mark.parametrize("tag", ["full", "mask", "grow", "csv"])
 def test_cli_decompose_matches_reference_run(golden, tmp_path, tag):
+    """full / mask: certificate final / every:3; grow: --rank-growth from k=1
+    (test_cli.py:164-183); csv: CSV input and outputs (host parse, upload)."""
     from paper_1702_02241_b200.matrixio import read_matrix
 
     d = golden("io")
-    (tmp_path / f"{tag}_x.bin").write_bytes(d[f"{tag}_x"].tobytes())
+    ext = "csv" if tag == "csv" else "bin"
+    (tmp_path / f"{tag}_x.{ext}").write_bytes(d[f"{tag}_x"].tobytes())
     if f"{tag}_m" in d:
         (tmp_path / f"{tag}_m.bin").write_bytes(d[f"{tag}_m"].tobytes())
     args = json.loads(str(d[f"{tag}_args"]))
-    args = [str(tmp_path / a) if a.endswith((".bin", ".json")) else a for a in args]
-    code, out, err = _run(["decompose", "--input", str(tmp_path / f"{tag}_x.bin")] + args)
+    args = [str(tmp_path / a) if a.endswith((".bin", ".csv", ".json")) else a for a in args]
+    code, out, err = _run(["decompose", "--input", str(tmp_path / f"{tag}_x.{ext}")] + args)
     assert code == int(d[f"{tag}_exit"]), err
     ref_out = str(d[f"{tag}_stdout"])
     assert out.split(",")[0] == ref_out.split(",")[0]  # "split: converged"
     obj = float(out.rsplit(" ", 1)[1])
     assert obj == pytest.approx(float(ref_out.rsplit(" ", 1)[1]), rel=1e-7)
     assert "warning" not in err
-    l_dev = read_matrix(tmp_path / f"{tag}_l.bin")
-    s_dev = read_matrix(tmp_path / f"{tag}_s.bin")
+    l_dev = read_matrix(tmp_path / f"{tag}_l.{ext}")
+    s_dev = read_matrix(tmp_path / f"{tag}_s.{ext}")
     assert rel(l_dev, d[f"{tag}_l"]) < 1e-4
     assert rel(s_dev, d[f"{tag}_s"]) < 1e-4
     ref_tr = json.loads(str(d[f"{tag}_trace"]))
@@ -152,12 +155,16 @@ def test_cli_decompose_matches_reference_run(golden, tmp_path, tag):
     assert abs(tr["final"]["nnz_s"] - ref_tr["final"]["nnz_s"]) <= 2
     assert tr["final"]["cert"]["rank"] == ref_tr["final"]["cert"]["rank"]
     assert set(tr["iterations"][0]) >= set(ref_tr["iterations"][0]) - {"cert"}
+    assert tr["k_final"] == ref_tr["k_final"]
+    assert tr["columns_grown"] == ref_tr["columns_grown"]
+    ranks = [r["rank"] for r in tr["iterations"]]
+    assert ranks == sorted(ranks)
     if "every" in ref_tr["config"]["certificate"]:
         every = ref_tr["config"]["cert_every"]
         assert all(("cert" in r) == (r["iter"] % every == 0) for r in tr["iterations"])
 
 
-@pytest.mark.parametrize("tag", ["full", "mask"])
+@pytest.mark.parametrize("tag", ["full", "mask", "grow"])
 def test_cli_certify_matches_reference(golden, tmp_path, tag):
     d = golden("io")
     from paper_1702_02241_b200.matrixio import write_matrix
