@@ -373,9 +373,51 @@ def time_to_certificate(dev):
            "fp64_switch_iter": rep.extra.get("fp64_switch_iter")}
     out["first_certified"] = first_certified(spec)
     spec.release_device()
+    out["from_file"] = ttc_from_file(x)
     del x
     torch.cuda.empty_cache()
     return out
+
+
+def ttc_from_file(x):
+    """SURVEY §8(d) 'also reported including H2D': the same C2 solve and
+    certificate, with the clock started before X is read from an SLRM file
+    (float64, 3.2 GB, page cache warm) and streamed into HBM as float32
+    (exact: the synthetic X is fp32) by the native reader."""
+    import shutil
+    import tempfile
+
+    import torch
+
+    from paper_1702_02241_b200 import ProblemSpec, SolverConfig, certificate, solve_split_spcp
+    from paper_1702_02241_b200.matrixio import read_matrix, write_matrix
+
+    tmp = tempfile.mkdtemp(prefix="spcp_ttc_")
+    try:
+        path = os.path.join(tmp, "x.bin")
+        write_matrix(x, path)  # untimed: the file exists before the run
+        del x
+        torch.cuda.empty_cache()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        xd = read_matrix(path, device="cuda", dtype=torch.float32)
+        spec = ProblemSpec(x=xd, lambda_l=LAM_L, lambda_s=LAM_S)
+        spec.device("mixed")
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        rep = solve_split_spcp(spec, K, SolverConfig())
+        cert = certificate(rep.factors, spec, f_bound_hint=rep.best_objective)
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        res = {"seconds": t2 - t0, "ingest_s": t1 - t0, "file_bytes": os.path.getsize(path),
+               "objective": rep.objective, "e_norm": cert.e_norm,
+               "path": "read_matrix(device=cuda) -> ProblemSpec -> solve -> certificate"}
+        spec.release_device()
+        return res
+    except Exception as exc:  # disk trouble must not void the bench line
+        return {"error": f"{type(exc).__name__}: {exc}"}
+    finally:
+        shutil.rmtree(tmp, ignore_errors=True)
 
 
 class _Certified(Exception):
