@@ -20,7 +20,9 @@
 #include <sys/stat.h>
 #include <unistd.h>
 
+#include <atomic>
 #include <cstdio>
+#include <thread>
 
 namespace spcp {
 
@@ -94,10 +96,11 @@ static int read_fully(int fd, void* buf, size_t bytes, off_t off, size_t* got) {
   return 0;
 }
 
-static int write_fully(int fd, const void* buf, size_t bytes) {
+static int write_fully(int fd, const void* buf, size_t bytes, off_t off) {
   size_t done = 0;
   while (done < bytes) {
-    const ssize_t w = write(fd, static_cast<const char*>(buf) + done, bytes - done);
+    const ssize_t w =
+        pwrite(fd, static_cast<const char*>(buf) + done, bytes - done, off + off_t(done));
     if (w < 0) {
       if (errno == EINTR) continue;
       return errno;
@@ -105,6 +108,47 @@ static int write_fully(int fd, const void* buf, size_t bytes) {
     done += size_t(w);
   }
   return 0;
+}
+
+// Page-cache copies run at a few GB/s per thread: large chunk transfers are
+// split over up to kIoThreads threads (pread / pwrite at disjoint offsets).
+static constexpr int kIoThreads = 4;
+static constexpr size_t kIoSplitMin = size_t(8) << 20;
+
+template <typename Fn>
+static int par_io(size_t bytes, Fn&& part) {
+  const int nt = int(std::min<size_t>(kIoThreads, std::max<size_t>(1, bytes / kIoSplitMin)));
+  if (nt == 1) return part(size_t(0), bytes);
+  const size_t step = ((bytes + nt - 1) / nt + 4095) & ~size_t(4095);
+  std::vector<std::thread> th;
+  std::vector<int> rc(nt, 0);
+  for (int t = 0; t < nt; ++t) {
+    const size_t b0 = std::min(bytes, t * step), b1 = std::min(bytes, b0 + step);
+    th.emplace_back([&, t, b0, b1] { rc[t] = b1 > b0 ? part(b0, b1 - b0) : 0; });
+  }
+  for (auto& x : th) x.join();
+  for (int r : rc)
+    if (r) return r;
+  return 0;
+}
+
+// pread of [off, off + bytes) into buf; *got < bytes only at end of file
+static int par_read(int fd, void* buf, size_t bytes, off_t off, size_t* got) {
+  std::atomic<size_t> total{0};
+  const int e = par_io(bytes, [&](size_t b0, size_t n) {
+    size_t g = 0;
+    const int r = read_fully(fd, static_cast<char*>(buf) + b0, n, off + off_t(b0), &g);
+    total += g;
+    return r;
+  });
+  *got = total.load();
+  return e;
+}
+
+static int par_write(int fd, const void* buf, size_t bytes, off_t off) {
+  return par_io(bytes, [&](size_t b0, size_t n) {
+    return write_fully(fd, static_cast<const char*>(buf) + b0, n, off + off_t(b0));
+  });
 }
 
 struct Fd {
@@ -187,8 +231,10 @@ struct AtomicFile {
     std::memcpy(h + 16, &c, 8);
     return put(h, kSlrmHeader);
   }
+  off_t pos = 0;
   int put(const void* buf, size_t bytes) {
-    if (int e = write_fully(f.fd, buf, bytes)) return io_fail(e, tmp);
+    if (int e = par_write(f.fd, buf, bytes, pos)) return io_fail(e, tmp);
+    pos += off_t(bytes);
     return SPCP_OK;
   }
   int commit() {
@@ -266,16 +312,28 @@ int spcp_slrm_read_device(const char* path, int device, int64_t row0, int64_t ro
     size_t got = 0;
     if (full_rows) {
       const size_t want = size_t(nr) * cols * 8;
-      if (int e = read_fully(f.fd, hp, want, base, &got)) return io_fail(e, std::string(path));
+      if (int e = par_read(f.fd, hp, want, base, &got)) return io_fail(e, std::string(path));
       if (got != want) return fail(SPCP_ERR_TRUNCATED, std::string(path) + ": short payload");
     } else {
-      for (int64_t q = 0; q < nr; ++q) {
-        const size_t want = size_t(cols) * 8;
-        if (int e = read_fully(f.fd, hp + q * want, want,
-                               base + off_t(q) * off_t(fc) * 8 + off_t(col0) * 8, &got))
-          return io_fail(e, std::string(path));
-        if (got != want) return fail(SPCP_ERR_TRUNCATED, std::string(path) + ": short payload");
-      }
+      // one pread per row of the window, rows split over the I/O threads
+      const size_t want = size_t(cols) * 8;
+      std::atomic<int64_t> short_rows{0};
+      const int e = par_io(size_t(nr) * want, [&](size_t b0, size_t n) {
+        const int64_t q0 = int64_t(b0 / want), q1 = int64_t((b0 + n + want - 1) / want);
+        for (int64_t q = q0; q < std::min(q1, nr); ++q) {
+          // a part boundary may split a row: each part reads whole rows whose
+          // first byte lies in it
+          if (size_t(q) * want < b0) continue;
+          size_t g = 0;
+          if (int r = read_fully(f.fd, hp + q * want, want,
+                                 base + off_t(q) * off_t(fc) * 8 + off_t(col0) * 8, &g))
+            return r;
+          if (g != want) ++short_rows;
+        }
+        return 0;
+      });
+      if (e) return io_fail(e, std::string(path));
+      if (short_rows) return fail(SPCP_ERR_TRUNCATED, std::string(path) + ": short payload");
     }
     SPCP_CUDA(cudaMemcpyAsync(stage.ptr, hp, size_t(nr) * cols * 8, cudaMemcpyHostToDevice, st));
     SPCP_CUDA(cudaEventRecord(ev.ev[b], st));
