@@ -894,25 +894,36 @@ static int run_reduce(spcp_problem* p, int64_t k, int kp, int part_dtype, const 
 #else
     const bool skewed = std::max(lp_u, lp_v) >= 8 * std::min(lp_u, lp_v);  // C3: 1 vs 32
 #endif
-    const int lanes_used = skewed ? lp : 2;
+    // balanced: SPCP_REDUCE_LPI = 2 (default) or 4 lanes per item
+    static int lpi_env = -1;
+    if (lpi_env < 0) {
+      const char* e = getenv("SPCP_REDUCE_LPI");
+      lpi_env = (e && std::string(e) == "4") ? 4 : 2;
+    }
+    const int lanes_used = skewed ? lp : lpi_env;
+    const int kind = skewed ? 2 : (lpi_env == 4 ? 1 : 0);
     // one wave of resident blocks (grid-stride over the items): a partial
     // second wave left ~1/3 of the SM time idle (ncu, C2)
-    static int resident[2] = {0, 0};
-    int& res = resident[skewed ? 1 : 0];
+    static int resident[3] = {0, 0, 0};
+    int& res = resident[kind];
     if (!res) {
       int per_sm = 0;
-      cudaError_t e = skewed ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                                   &per_sm, tc_reduce_kernel, 256, 0)
-                             : cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                                   &per_sm, tc_reduce_lpi_kernel<2>, 256, 0);
+      cudaError_t e = kind == 2 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                                      &per_sm, tc_reduce_kernel, 256, 0)
+                    : kind == 1 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                                      &per_sm, tc_reduce_lpi_kernel<4>, 256, 0)
+                                : cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                                      &per_sm, tc_reduce_lpi_kernel<2>, 256, 0);
       if (e != cudaSuccess || per_sm < 1) per_sm = 4;
       res = per_sm * kSMs;
     }
     const int nb = int(std::min<int64_t>((items * lanes_used + 255) / 256, res));
     if ((rc = p->blk.ensure(size_t(nb) * 6 * sizeof(double)))) return rc;
     rp.blk = p->blk.as<double>();  // (ensure may have grown the buffer)
-    if (skewed)
+    if (kind == 2)
       SPCP_CUDA(launch_pdl(tc_reduce_kernel, dim3(nb), dim3(256), 0, p->stream, rp, lp_u, lp_v));
+    else if (kind == 1)
+      SPCP_CUDA(launch_pdl(tc_reduce_lpi_kernel<4>, dim3(nb), dim3(256), 0, p->stream, rp));
     else
       SPCP_CUDA(launch_pdl(tc_reduce_lpi_kernel<2>, dim3(nb), dim3(256), 0, p->stream, rp));
   }
