@@ -896,15 +896,28 @@ __global__ void tc_max_kernel(const double* __restrict__ z, const double* __rest
   tc::pdl_wait();
   tc::pdl_launch_next();
   unsigned long long mu = 0, mv = 0;
-  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < nu + nv;
-       q += int64_t(gridDim.x) * blockDim.x) {
-    double w = z[q];
-    if (dz) w += alpha * dz[q];
-    const unsigned long long bits = __double_as_longlong(fabs(w));
-    if (q < nu)
-      mu = bits > mu ? bits : mu;
-    else
-      mv = bits > mv ? bits : mv;
+  const int64_t tot = nu + nv, stride = int64_t(gridDim.x) * blockDim.x;
+  // four elements per thread per sweep, all loads in flight before the maxima
+  for (int64_t q0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q0 < tot;
+       q0 += 4 * stride) {
+    double zv[4], dv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t q = q0 + u * stride;
+      zv[u] = q < tot ? __ldg(z + q) : 0.0;
+      dv[u] = (dz && q < tot) ? __ldg(dz + q) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t q = q0 + u * stride;
+      double w = zv[u];
+      if (dz) w += alpha * dv[u];
+      const unsigned long long bits = q < tot ? __double_as_longlong(fabs(w)) : 0ull;
+      if (q < nu)
+        mu = bits > mu ? bits : mu;
+      else
+        mv = bits > mv ? bits : mv;
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
