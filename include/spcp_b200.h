@@ -24,6 +24,11 @@
  *   spcp_vec_*               <- the L-BFGS vector algebra  lbfgs.py:152-188
  *   spcp_gram / spcp_matmul_small  <- thin_qr/factor_svd factor-space algebra
  *                               linalg.py:43-59, certificate.py:50-67
+ *   spcp_slrm_header /
+ *   spcp_slrm_read_device    <- read_matrix (binary)        matrixio.py:94-126
+ *   spcp_slrm_write_device /
+ *   spcp_slrm_write_product  <- write_matrix (binary)       matrixio.py:53-71
+ *                               of the decompose outputs    cli.py:256-270
  *
  * Conventions:
  *   - every function returns an int status; 0 = SPCP_OK.  The Python layer

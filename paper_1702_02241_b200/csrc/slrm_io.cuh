@@ -124,7 +124,12 @@ static int par_io(size_t bytes, Fn&& part) {
   std::vector<int> rc(nt, 0);
   for (int t = 0; t < nt; ++t) {
     const size_t b0 = std::min(bytes, t * step), b1 = std::min(bytes, b0 + step);
-    th.emplace_back([&, t, b0, b1] { rc[t] = b1 > b0 ? part(b0, b1 - b0) : 0; });
+    auto job = [&, t, b0, b1] { rc[t] = b1 > b0 ? part(b0, b1 - b0) : 0; };
+    try {
+      th.emplace_back(job);
+    } catch (...) {  // no thread available: do this part on the calling thread
+      job();
+    }
   }
   for (auto& x : th) x.join();
   for (int r : rc)
