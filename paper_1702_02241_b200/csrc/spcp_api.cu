@@ -377,9 +377,18 @@ static int tc_build(spcp_problem* p) {
     cuuint64_t strides[1] = {cuuint64_t(p->ldx) * 4};
     cuuint32_t box[2] = {32, 128};
     cuuint32_t es[2] = {1, 1};
+    // SPCP_X_L2PROMO = none | 64 | 128 | 256 (default): L2 promotion of the X stream
+    CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    if (const char* e = getenv("SPCP_X_L2PROMO")) {
+      const std::string v(e);
+      promo = v == "none" ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+              : v == "64" ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+              : v == "128" ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                           : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    }
     CUresult r = enc(&p->tc_xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, p->x32.ptr, dims, strides,
-                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(SPCP_ERR_CUDA, "tensor map (X) encode failed");
   }
   if (p->masked) {
