@@ -246,3 +246,24 @@ def test_column_shards_read_from_file_match_unsharded(torch, tmp_path):
         assert rel(gs[: m * k].cpu().numpy(), g_full[: m * k].cpu().numpy()) <= 1e-5
         assert rel(gs[m * k:].cpu().numpy(),
                    g_full[m * k + c0 * k: m * k + c1 * k].cpu().numpy()) <= 1e-5
+
+
+def test_csv_device_read_and_decomposition_csv_outputs(torch, tmp_path):
+    """CSV files take the host parser and are uploaded (read_matrix(device=));
+    CSV decomposition outputs go through the device-materialised arrays."""
+    import paper_1702_02241_b200 as api
+    from paper_1702_02241_b200.matrixio import read_matrix, write_decomposition, write_matrix
+    from paper_1702_02241_b200.synth import gen_low_rank_plus_sparse
+
+    x, _, _ = gen_low_rank_plus_sparse(50, 40, 2, 0.05, 1e-3, seed=4)
+    write_matrix(x, tmp_path / "x.csv")
+    t = read_matrix(tmp_path / "x.csv", device="cuda")
+    assert t.is_cuda and t.cpu().numpy().tobytes() == read_matrix(tmp_path / "x.csv").tobytes()
+    np.testing.assert_array_equal(
+        read_matrix(tmp_path / "x.csv", device="cuda", col0=5, cols=7).cpu().numpy(), x[:, 5:12])
+    spec = api.ProblemSpec(x=t, lambda_l=1.0, lambda_s=0.1)
+    rep = api.solve_split_spcp(spec, 3)
+    nnz = write_decomposition(rep, tmp_path / "l.csv", tmp_path / "s.bin")
+    np.testing.assert_array_equal(read_matrix(tmp_path / "l.csv"), rep.l)
+    assert read_matrix(tmp_path / "s.bin").tobytes() == rep.s.tobytes()
+    assert nnz == int(np.count_nonzero(rep.s))
