@@ -40,7 +40,8 @@ _LAZY = {
     "CertificateReport": "certificate", "certificate": "certificate",
     "factor_svd": "certificate",
     "SplitSPCP": "estimators",
-    "gen_low_rank_plus_sparse_device": "synth",
+    "gen_low_rank_plus_sparse_device": "synth", "gen_video_device": "synth",
+    "gen_low_rank_plus_sparse": "synth", "gen_mask": "synth",
     "solve_split_spcp_sharded": "dist",
 }
 

@@ -22,7 +22,7 @@ import math
 
 import numpy as np
 
-__all__ = ["gen_low_rank_plus_sparse", "gen_mask", "gen_low_rank_plus_sparse_device",
+__all__ = ["gen_low_rank_plus_sparse", "gen_mask", "gen_low_rank_plus_sparse_device", "gen_video_device",
            "factor_draw"]
 
 
@@ -113,3 +113,71 @@ def gen_low_rank_plus_sparse_device(m, n, rank, sparse_frac, noise_rel, seed=0, 
         out[r0:r1] = blk.to(tdt)
         del blk
     return out
+
+
+def gen_video_device(height=384, width=288, frames=2000, illum_rank=2, fg_size=(48, 32),
+                     n_objects=3, noise=1e-3, seed=0, dtype="float32", device=None):
+    """Synthetic surveillance video for the background-subtraction shape
+    (BASELINE config C3), built in HBM.
+
+    X has one column per frame (pixels in row-major order, height*width rows).
+    Its parts:
+      * background: a static image times 1 + a slow illumination drift of
+        rank `illum_rank`; L_ref has rank 1 + illum_rank;
+      * foreground: `n_objects` rectangles of `fg_size` moving at constant
+        velocity (bouncing off the frame edges), with intensities that differ
+        from the background — the sparse S_ref;
+      * Gaussian noise of standard deviation `noise`.
+
+    Returns (X, L_ref, fg_mask) as CUDA tensors (m x frames, fp32 / bool).
+    The reference has no video generator; this one follows the paper's
+    escalator / hall experiments in structure, not in pixels."""
+    import torch
+
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    tdt = torch.float32 if dtype == "float32" else torch.float64
+    g = torch.Generator(device=dev)
+    g.manual_seed(int(seed))
+    h, w, T = int(height), int(width), int(frames)
+    yy = torch.linspace(0, 1, h, device=dev, dtype=torch.float64)[:, None]
+    xx = torch.linspace(0, 1, w, device=dev, dtype=torch.float64)[None, :]
+    # smooth static scene: a few random low-frequency waves
+    bg = torch.zeros((h, w), device=dev, dtype=torch.float64)
+    for _ in range(6):
+        a, fy, fx, ph = torch.rand(4, generator=g, device=dev, dtype=torch.float64)
+        bg += (0.2 + 0.3 * a) * torch.cos(2 * math.pi * (1 + 3 * fy) * yy +
+                                          2 * math.pi * (1 + 3 * fx) * xx + 6.28 * ph)
+    bg = 0.5 + 0.25 * bg / bg.abs().max()
+    # illumination: spatial gain maps times slow temporal profiles
+    t = torch.linspace(0, 1, T, device=dev, dtype=torch.float64)
+    spatial = [bg.reshape(-1)]
+    temporal = [torch.ones(T, device=dev, dtype=torch.float64)]
+    for r in range(int(illum_rank)):
+        gy, gx = torch.rand(2, generator=g, device=dev, dtype=torch.float64)
+        spatial.append((0.1 * torch.cos(math.pi * (r + 1) * (gy * yy + gx * xx))).reshape(-1))
+        temporal.append(torch.sin(2 * math.pi * (r + 1) * t + float(gy) * 3.0))
+    A = torch.stack(spatial, 1)  # m x (1 + illum_rank)
+    B = torch.stack(temporal, 1)  # T x (1 + illum_rank)
+    L = A @ B.T
+    X = L.clone()
+    fg = torch.zeros((h, w, T), device=dev, dtype=torch.bool)
+    Xv = X.view(h, w, T)
+    oh, ow = fg_size
+    iy = torch.arange(h, device=dev)[:, None, None]
+    ix = torch.arange(w, device=dev)[None, :, None]
+    frame = torch.arange(T, device=dev, dtype=torch.float64)
+    for _ in range(int(n_objects)):
+        p0y, p0x, vy, vx, val = torch.rand(5, generator=g, device=dev, dtype=torch.float64)
+        ys = p0y * (h - oh) + (vy - 0.5) * 4.0 * frame
+        xs = p0x * (w - ow) + (vx - 0.5) * 4.0 * frame
+        # bounce: reflect the trajectory into [0, h - oh] x [0, w - ow]
+        ys = (h - oh) - ((ys % (2 * (h - oh))) - (h - oh)).abs()
+        xs = (w - ow) - ((xs % (2 * (w - ow))) - (w - ow)).abs()
+        y0, x0 = ys.long()[None, None, :], xs.long()[None, None, :]
+        box = (iy >= y0) & (iy < y0 + oh) & (ix >= x0) & (ix < x0 + ow)
+        Xv.masked_fill_(box, 0.15 + 0.7 * float(val))  # later objects occlude earlier ones
+        fg |= box
+        del box
+    if noise > 0:
+        X += noise * torch.randn(X.shape, generator=g, device=dev, dtype=torch.float64)
+    return X.to(tdt), L.to(tdt), fg.reshape(h * w, T)

@@ -267,3 +267,26 @@ def test_csv_device_read_and_decomposition_csv_outputs(torch, tmp_path):
     np.testing.assert_array_equal(read_matrix(tmp_path / "l.csv"), rep.l)
     assert read_matrix(tmp_path / "s.bin").tobytes() == rep.s.tobytes()
     assert nnz == int(np.count_nonzero(rep.s))
+
+
+def test_video_background_subtraction(torch):
+    """The background-subtraction use (BASELINE C3 shape, small): the device
+    video generator's static + illumination background is recovered as L and
+    the moving objects as the support of S; the result matches the numpy
+    oracle run on the same frames."""
+    import paper_1702_02241_b200 as api
+    from oracle import spcp_oracle as orc
+
+    x, l_ref, fg = api.gen_video_device(48, 36, 200, fg_size=(8, 6), n_objects=2, seed=0,
+                                        dtype="float64")
+    assert torch.linalg.matrix_rank(l_ref).item() == 3
+    spec = api.ProblemSpec(x=x, lambda_l=1.0, lambda_s=0.05)
+    rep = api.solve_split_spcp(spec, 3, api.SolverConfig(grad_tol=1e-6))
+    xh, lh, fgh = x.cpu().numpy(), l_ref.cpu().numpy(), fg.cpu().numpy()
+    moved = np.abs(xh - lh) > 0.1  # object pixels that differ from the background
+    s_on = rep.s != 0
+    assert s_on[moved].mean() > 0.99
+    assert (s_on & ~fgh).mean() < 1e-3
+    assert rel(rep.l, lh) < 0.02
+    ref = orc.solve_split_spcp(xh, 1.0, 0.05, 3, grad_tol=1e-6, max_iter=500)
+    assert rel(rep.l, ref["l"]) < 1e-4 and rel(rep.s, ref["s"]) < 1e-4
