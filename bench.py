@@ -15,11 +15,12 @@ N > 1 (torchrun, one rank per GPU): weak scaling, each rank owns a
 NCCL-all-reduced every evaluation; value = whole-job C2-block
 evaluations per second.
 
-The reference arm times the CPU oracle (oracle/spcp_oracle.py, a numpy
-restatement of the reference's split_objective — the reference is a Python
-package, so there is no compiled oracle/_ref) on a bounded column block of
-the same workload and scales to the full matrix (the objective is separable
-over column blocks).
+The reference arm times the reference's own split_objective: the unmodified
+`spcp` package that `__graft_entry__.build()` pip-installs into baseline/_ref
+(git-ignored, travels to the GPU box), or the CPU oracle port
+(oracle/spcp_oracle.py) when that install is absent; `cpu_baseline.kind` says
+which.  It runs on a bounded column block of the same workload and scales to
+the full matrix (the objective is separable over column blocks).
 """
 
 import argparse
@@ -141,23 +142,61 @@ def alg_bytes(m, n, k, masked=False):
     return 4 * m * n + (((m * n + 7) // 8) if masked else 0) + 2 * 4 * (m + n) * k
 
 
-def cpu_sample(block_cols=CPU_BLOCK_COLS, evals=2, warmup=0):
-    """Oracle split_objective on a 20000 x block_cols column block of the C2 law."""
-    from oracle import spcp_oracle as orc
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
-    x, _, _ = orc.gen_low_rank_plus_sparse(M, block_cols, RANK, 0.05, 1e-3, seed=0)
-    x = x.astype(np.float32).astype(np.float64)
+
+def reference_pkg():
+    """The unmodified reference package (`spcp`, pure Python) installed into
+    baseline/_ref by `__graft_entry__.build()` (pip --target), or None."""
+    if not os.path.isdir(os.path.join(REF_DIR, "spcp")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import spcp
+    except Exception:
+        return None
+    if not os.path.abspath(spcp.__file__).startswith(REF_DIR):
+        return None
+    return spcp
+
+
+def cpu_sample(block_cols=CPU_BLOCK_COLS, evals=2, warmup=0):
+    """split_objective on a 20000 x block_cols column block of the C2 law: the
+    reference's own (baseline/_ref, `kind` "reference") when installed, else
+    the oracle port ("port").  Returns (times, kind, what)."""
     rng = np.random.default_rng(1)
     u = rng.standard_normal((M, K)) * np.sqrt(2.0)
     v = rng.standard_normal((block_cols, K)) * np.sqrt(2.0)
+    ref = reference_pkg()
+    if ref is not None:
+        x, _, _ = ref.gen_low_rank_plus_sparse(M, block_cols, RANK, 0.05, 1e-3, seed=0)
+        x = x.astype(np.float32).astype(np.float64)
+        spec = ref.ProblemSpec(x=x, lambda_l=LAM_L, lambda_s=LAM_S)
+        fp = ref.FactorPair(u, v)
+
+        def call():
+            ref.split_objective(fp, spec)
+
+        kind, what = "reference", "reference spcp.split_objective (baseline/_ref, numpy/OpenBLAS)"
+    else:
+        from oracle import spcp_oracle as orc
+
+        x, _, _ = orc.gen_low_rank_plus_sparse(M, block_cols, RANK, 0.05, 1e-3, seed=0)
+        x = x.astype(np.float32).astype(np.float64)
+
+        def call():
+            orc.split_objective(u, v, x, LAM_L, LAM_S)
+
+        kind, what = "port", "oracle split_objective (numpy/OpenBLAS port of the reference)"
     for _ in range(warmup):
-        orc.split_objective(u, v, x, LAM_L, LAM_S)
+        call()
     times = []
     for _ in range(evals):
         t0 = time.perf_counter()
-        orc.split_objective(u, v, x, LAM_L, LAM_S)
+        call()
         times.append(time.perf_counter() - t0)
-    return times
+    return times, kind, what
 
 
 def run_reference(args, rank, world):
@@ -165,7 +204,7 @@ def run_reference(args, rank, world):
         return
     # bounded per-step sample: the whole --steps K run stays within a few minutes
     cols = CPU_BLOCK_COLS if args.steps <= 50 else CPU_BLOCK_COLS // 4
-    times = cpu_sample(block_cols=cols, evals=args.steps, warmup=args.warmup)
+    times, kind, what = cpu_sample(block_cols=cols, evals=args.steps, warmup=args.warmup)
     per_block = float(np.mean(times))
     full = per_block * (N_COLS / cols)
     val = 1.0 / full
@@ -177,8 +216,8 @@ def run_reference(args, rank, world):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "C2 synthetic 20000x20000 rank 20 k=20, lambda_L=40 lambda_S=0.1",
                    "sample": f"{M}x{cols} column block x {N_COLS // cols}"},
-        "cpu_baseline": {"value": val, "unit": "evals/s", "cores": cores, "kind": "port",
-                         "sample": f"oracle split_objective on a {M}x{cols} column "
+        "cpu_baseline": {"value": val, "unit": "evals/s", "cores": cores, "kind": kind,
+                         "sample": f"{what} on a {M}x{cols} column "
                                    f"block per step, scaled x{N_COLS // cols} (separable)"},
         "e2e": {"value": val, "unit": "evals/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -296,13 +335,12 @@ def run_b200(args, rank, world):
         peak, peak_src = peaks()
         cpu = None
         if world == 1 and not args.skip_cpu:
-            times = cpu_sample(evals=2)
+            times, kind, what = cpu_sample(evals=2)
             full = float(np.mean(times)) * (N_COLS / CPU_BLOCK_COLS)
             cpu = {"value": 1.0 / full, "unit": "evals/s", "cores": os.cpu_count(),
-                   "kind": "port",
-                   "sample": f"oracle split_objective (numpy/OpenBLAS, fp64) on a "
-                             f"{M}x{CPU_BLOCK_COLS} column block of the C2 law, 2 evals, "
-                             f"scaled x{N_COLS // CPU_BLOCK_COLS} (separable)"}
+                   "kind": kind,
+                   "sample": f"{what}, fp64, on a {M}x{CPU_BLOCK_COLS} column block of the "
+                             f"C2 law, 2 evals, scaled x{N_COLS // CPU_BLOCK_COLS} (separable)"}
         line = {
             "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step,
