@@ -290,3 +290,50 @@ def test_video_background_subtraction(torch):
     assert rel(rep.l, lh) < 0.02
     ref = orc.solve_split_spcp(xh, 1.0, 0.05, 3, grad_tol=1e-6, max_iter=500)
     assert rel(rep.l, ref["l"]) < 1e-4 and rel(rep.s, ref["s"]) < 1e-4
+
+
+def test_reference_solver_drives_the_c_abi_plugin():
+    """The drop-in boundary seen from the reference side:
+    the UNMODIFIED reference L-BFGS (`spcp.solver.lbfgs_minimize` from
+    baseline/_ref, installed by build()) drives `spcp_split_objective_host`
+    (fp64 mode) as its plug-in `fun(z) -> (f, grad)`, and reaches the same
+    iterates, termination and objective as with its own numpy objective."""
+    import importlib
+    import os
+    import sys
+
+    ref_dir = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                           "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "spcp")):
+        pytest.skip("reference package not installed in baseline/_ref (run build())")
+    sys.path.insert(0, ref_dir)
+    try:
+        spcp = importlib.import_module("spcp")
+        ref_solver = importlib.import_module("spcp.solver")
+    finally:
+        sys.path.remove(ref_dir)
+    from paper_1702_02241_b200._lib import SPCP_F64
+    from paper_1702_02241_b200.device import DeviceProblem
+
+    x, _, _ = spcp.gen_low_rank_plus_sparse(300, 200, 4, 0.05, 1e-3, seed=11)
+    spec = spcp.ProblemSpec(x=x, lambda_l=2.0, lambda_s=0.1)
+    m, n, k = 300, 200, 5
+    start = spcp.init_factors(spec, k, strategy="rsvd", seed=0)
+    cfg = spcp.SolverConfig(grad_tol=1e-6, max_iter=300)
+    dp = DeviceProblem(x, 2.0, 0.1, store=("f64",))
+
+    def gpu_fun(z):
+        u = z[: m * k].reshape(m, k)
+        v = z[m * k:].reshape(n, k)
+        f, gu, gv = dp.split_objective_host(u, v, SPCP_F64)
+        return f, np.concatenate([gu.ravel(), gv.ravel()])
+
+    own = ref_solver.lbfgs_minimize(ref_solver._flat_split_objective(spec, m, n, k), start, cfg)
+    ours = ref_solver.lbfgs_minimize(gpu_fun, start, cfg)
+    assert own.termination == "converged" and ours.termination == "converged"
+    assert ours.objective == pytest.approx(own.objective, rel=1e-10)
+    # same trajectory (the stopping iteration may differ by one at the threshold)
+    assert abs(len(ours.iterations) - len(own.iterations)) <= 1
+    for a, b in zip(ours.iterations, own.iterations):
+        assert a.objective == pytest.approx(b.objective, rel=1e-9)
+    assert rel(ours.factors.compose(), own.factors.compose()) < 1e-5
