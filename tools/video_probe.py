@@ -29,6 +29,7 @@ def main():
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     rep = api.solve_split_spcp(spec, args.k, api.SolverConfig())
+    torch.cuda.synchronize()
     t1 = time.perf_counter()
     cert = api.certificate(rep.factors, spec, f_bound_hint=rep.best_objective)
     torch.cuda.synchronize()
