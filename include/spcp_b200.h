@@ -190,6 +190,11 @@ int spcp_vec_lincomb(spcp_problem* p, int64_t len, int count, const double* coef
  * vector is read once (one pass for all dots of an L-BFGS iteration). */
 int spcp_vec_gram(spcp_problem* p, int64_t len, int na, const double* const* a, int nb,
                   const double* const* b, double* out_host);
+/* vec_gram_dev: the same dots into a device buffer (na * nb float64), stream
+ * ordered, no synchronisation: the column-sharded path all-reduces them on the
+ * device before one copy to the host (dist.py). */
+int spcp_vec_gram_dev(spcp_problem* p, int64_t len, int na, const double* const* a, int nb,
+                      const double* const* b, double* out_dev);
 
 /* ---- tall-skinny factor algebra (linalg.py:43-59, certificate.py:50-67) ----
  * gram: out_host (p x q, float64) = A^T B, A: rows x p, B: rows x q (device).

@@ -56,6 +56,7 @@ EXPORTS = {
     "spcp_vec_multidot": [_vp, _i64, _i32, _pp, _pp, _dp],
     "spcp_vec_lincomb": [_vp, _i64, _i32, _dp, _pp, _vp],
     "spcp_vec_gram": [_vp, _i64, _i32, _pp, _i32, _pp, _dp],
+    "spcp_vec_gram_dev": [_vp, _i64, _i32, _pp, _i32, _pp, _vp],
     "spcp_gram": [_vp, _i64, _i64, _vp, _i64, _vp, _dp],
     "spcp_matmul_small": [_vp, _i64, _i64, _vp, _i64, _dp, _vp],
     "spcp_prof_enable": [_vp, _i32],

@@ -11,15 +11,20 @@ distance from 0 to the subdifferential of lambda|L|_* + phi(L) is
   * a^T = D^T U1 and b = D V1 come from ONE fused streaming pass over X
     (`spcp_apply` with both product operands), c = a V1 is a Gram;
   * t4 needs the singular values of P above 1.  The reference takes a dense
-    SVD of the m x n P.  Here P is never formed for large problems: a block
-    subspace iteration applies P and P^T through streaming passes (D W and
-    D^T Y computed from X on the fly, then projected) and the Ritz values
+    SVD of the m x n P (certificate.py:70-74,119).  Here P is never formed: a
+    block subspace iteration applies P and P^T through streaming passes (D W
+    and D^T Y computed from X on the fly, then projected) and the Ritz values
     give sigma_i(P); the block grows until its smallest Ritz value is below 1
-    so every sigma > 1 is captured.  Small problems (dense_limit) take the
-    reference's dense route on the device.
+    so every sigma > 1 is captured.  Ritz values are lower bounds: t4 comes
+    from converged values, or is proved to be exactly 0 by a probabilistic
+    bound on sigma_max(P) (`_power_bound_iters`), and `info` says which.
+  * Column-sharded problems run the same code with `CertOps`
+    reductions: Grams of row-sharded n-side blocks and the m x b products
+    D W are summed across ranks (dist.certificate_sharded).
 """
 
 import math
+import warnings
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -27,9 +32,12 @@ import numpy as np
 from .errors import NumericalError
 from .linalg import SvdTriplet, device_thin_qr, svd_small, thin_qr
 
-__all__ = ["CertificateReport", "factor_svd", "certificate", "DENSE_LIMIT"]
+__all__ = ["CertificateReport", "factor_svd", "certificate", "CertOps", "certificate_core",
+           "FP32_PRODUCTS_MIN_ELEMS"]
 
-DENSE_LIMIT = 4096 * 4096  # entries of P below which t4 uses the dense SVD
+# above this many entries the subspace iteration's D products stream the fp32
+# copy of X (they are compared against 1 only); below it they run in fp64
+FP32_PRODUCTS_MIN_ELEMS = 1 << 22
 
 
 @dataclass(frozen=True)
@@ -60,13 +68,38 @@ def factor_svd(fp, rank_tol=1e-10):
     return SvdTriplet((qu @ core.u)[:, :r], sig[:r].copy(), (qv @ core.v)[:, :r])
 
 
-def _device_factor_svd(dp, z, m, n, k, rank_tol, gram_reduce=None, v_rows=None):
-    """factor_svd on device factors; returns (u1 dev m x r, sigma, v1 dev n x r,
-    all singular values)."""
-    uu = z[: m * k].reshape(m, k)
-    vv = z[m * k:].reshape(v_rows if v_rows is not None else n, k)
-    qu, ru = device_thin_qr(dp, uu)
-    qv, rv = device_thin_qr(dp, vv, gram_reduce)
+class CertOps:
+    """Cross-rank sums for a column-sharded problem (identities on one GPU).
+
+    host(a): sum a small host array (Grams of row-sharded n-side blocks).
+    dev(t):  sum a device tensor in place (the m x b products D_p W_p)."""
+
+    def __init__(self, host=None, dev=None, n_total=None, col0=0):
+        self._host = host
+        self._dev = dev
+        self.n_total = n_total
+        self.col0 = int(col0)
+        self.sharded = host is not None
+
+    def host(self, a):
+        return a if self._host is None else self._host(a)
+
+    def dev(self, t):
+        if self._dev is not None:
+            self._dev(t)
+        return t
+
+    def gram_rows(self, dp, a, b):
+        """a^T b for n-side (row-sharded) device matrices."""
+        return self.host(dp.gram(a, b))
+
+
+def _device_factor_svd(dp, u, v, rank_tol, ops):
+    """factor_svd (certificate.py:50-67) on device factors u (m x k,
+    replicated) and v (n_p x k, this rank's rows); returns (u1, sigma, v1,
+    all singular values) with u1, v1 device matrices."""
+    qu, ru = device_thin_qr(dp, u)
+    qv, rv = device_thin_qr(dp, v, ops.host if ops.sharded else None)
     core = svd_small(ru @ rv.T)
     sig = core.sigma
     r = 0 if (sig.size == 0 or sig[0] <= 0.0) else int(np.sum(sig > rank_tol * sig[0]))
@@ -77,127 +110,155 @@ def _device_factor_svd(dp, z, m, n, k, rank_tol, gram_reduce=None, v_rows=None):
     return u1, sig[:r].copy(), v1, sig
 
 
-def _sq(dp, a):
-    return float(np.trace(dp.gram(a, a)))
-
-
-def _dense_sigmas(dp, z, k, lam, u1, v1):
-    """sigma(P) by the reference's dense route, computed on the device."""
-    import torch
-
-    g = dp.grad_dense(k, z)
-    d = g.mul_(-1.0 / lam)
-    if u1 is not None:
-        d = d - u1 @ (u1.T @ d)
-        d = d - (d @ v1) @ v1.T
-    return torch.linalg.svdvals(d).cpu().numpy()
-
-
 class _ProjectedOperator:
     """x -> P x and y -> P^T y with P = (I - U1U1^T) D (I - V1V1^T), D = -G/lam,
     every D product a streaming pass over X (spcp_apply)."""
 
-    def __init__(self, dp, z, k, lam, u1, v1):
+    def __init__(self, dp, z, k, lam, u1, v1, ops, precision):
         self.dp, self.z, self.k, self.lam, self.u1, self.v1 = dp, z, k, lam, u1, v1
+        self.ops = ops
+        self.precision = precision
 
-    def _proj(self, basis, w):
-        if basis is None:
+    def proj_u(self, w):  # replicated m-side
+        if self.u1 is None:
             return w
-        c = self.dp.gram(basis, w)
-        return w - self.dp.matmul_small(basis, c)
+        c = self.dp.gram(self.u1, w)
+        return w - self.dp.matmul_small(self.u1, c)
 
-    # The subspace iteration only compares sigma(P) against 1, so its D
-    # products stream X in fp32 (spcp_apply_f32; fp64 when no fp32 copy of X is
-    # stored).  The cross terms t1..t3 keep the fp64 products.
-    def right(self, w):  # P w, w: n x b
-        w = self._proj(self.v1, w)
-        y, _ = self.dp.apply(self.k, self.z, w_right=w.contiguous(), precision="fp32")
-        return self._proj(self.u1, y.mul_(-1.0 / self.lam))
+    def proj_v(self, w):  # row-sharded n-side
+        if self.v1 is None:
+            return w
+        c = self.ops.gram_rows(self.dp, self.v1, w)
+        return w - self.dp.matmul_small(self.v1, c)
 
-    def left(self, y):  # P^T y, y: m x b
-        y = self._proj(self.u1, y)
-        _, w = self.dp.apply(self.k, self.z, w_left=y.contiguous(), precision="fp32")
-        return self._proj(self.v1, w.mul_(-1.0 / self.lam))
+    def right(self, w):  # P w, w: n_p x b
+        w = self.proj_v(w)
+        y, _ = self.dp.apply(self.k, self.z, w_right=w.contiguous(), precision=self.precision)
+        self.ops.dev(y)  # sum_p D_p W_p
+        return self.proj_u(y.mul_(-1.0 / self.lam))
+
+    def left(self, y):  # P^T y, y: m x b (replicated)
+        y = self.proj_u(y)
+        _, w = self.dp.apply(self.k, self.z, w_left=y.contiguous(), precision=self.precision)
+        return self.proj_v(w.mul_(-1.0 / self.lam))
 
 
 _SUBSPACE_TOL = 1e-9
+_FAIL_PROB = 1e-6
+# (1 - eps, certified factor): after the bound's iteration count, with
+# probability >= 1 - fail, theta^2 >= (1 - eps) sigma_max^2, i.e.
+# sigma_max <= theta / sqrt(1 - eps)
+_TIERS = ((0.25, 2.0), (0.5, math.sqrt(2.0)))
 
 
-def _q_bound(n, eps=0.5, fail=1e-6):
-    """Iterations after which 1.648 sqrt(n) e^(-eps (2q - 1)) <= fail."""
-    return int(math.ceil((math.log(1.648 * math.sqrt(max(n, 1)) / fail) / eps + 1.0) / 2.0))
+def _power_bound_iters(dim, one_minus_eps, fail):
+    """Iterations q after which a sqrt(theta) Ritz value of the block subspace
+    iteration on P^T P certifies sigma_max(P) <= theta / sqrt(1 - eps) except
+    with probability <= fail.
+
+    Kuczynski & Wozniakowski (1992), power method from a random start on a
+    dim x dim PSD matrix: P[xi_k < (1 - eps) lambda_1] <= 0.824 sqrt(dim)
+    (1 - eps)^(k - 1/2), xi_k the Rayleigh quotient after k steps.  The block
+    iteration's span after q passes contains the power iterate with k = q - 1
+    steps of its first start vector, and its top Ritz value theta satisfies
+    theta^2 >= xi_{q-1} (Cauchy-Schwarz), so the power-method bound applies
+    with k = q - 1.  The iteration tests the bound at every step: a union bound
+    over steps (geometric in q) and over the two tiers gives the factor
+    2 / eps on top of `fail`."""
+    eps = 1.0 - one_minus_eps
+    budget = fail * eps / 2.0
+    k = math.log(0.824 * math.sqrt(max(dim, 1)) / budget) / -math.log(one_minus_eps) + 0.5
+    return int(math.ceil(k)) + 1
 
 
-def _subspace_sigmas(op, n, m, r, block=16, max_iter=60, tol=None, seed=0):
+def _subspace_sigmas(op, n_total, m, r, block=16, max_iter=400, tol=None, seed=0):
     """Top singular values of P by randomized block subspace iteration with
-    Rayleigh-Ritz; the block doubles until its smallest Ritz value < 1."""
+    Rayleigh-Ritz; the block doubles until its smallest Ritz value < 1.
+    Returns (sigmas, info)."""
     import torch
 
-    dp = op.dp
+    dp, ops = op.dp, op.ops
     tol = _SUBSPACE_TOL if tol is None else tol
-    cap = max(1, min(m, n) - r)
+    cap = max(1, min(m, n_total) - r)
     b = min(block, cap)
+    n_loc = dp.n
     iters_total = 0
+    bounds = [(ome, fac, _power_bound_iters(n_total, ome, _FAIL_PROB)) for ome, fac in _TIERS]
     while True:
-        w = torch.from_numpy(np.random.default_rng(seed).standard_normal((n, b))).to(dp.device)
-        q, _ = device_thin_qr(dp, op._proj(op.v1, w))
+        # start block drawn over all n_total rows (the same on every rank and
+        # the same as a single-GPU run), each rank keeps its own rows
+        w_all = np.random.default_rng(seed).standard_normal((n_total, b))
+        w = torch.from_numpy(np.ascontiguousarray(w_all[ops.col0:ops.col0 + n_loc])).to(dp.device)
+        q, _ = device_thin_qr(dp, op.proj_v(w), ops.host if ops.sharded else None)
         prev = None
-        sig = None
+        sig = np.zeros(0)
+        converged = False
         for it in range(max_iter):
+            if q.shape[1] == 0:  # P vanishes on the start block: sigma(P) = 0
+                return np.zeros(0), {"t4_method": "subspace", "block": b,
+                                     "iters": iters_total, "sigma_p_max": 0.0,
+                                     "converged": True}
             y = op.right(q)
             qy, _ = device_thin_qr(dp, y)
+            if qy.shape[1] == 0:
+                return np.zeros(0), {"t4_method": "subspace", "block": b,
+                                     "iters": iters_total + 1, "sigma_p_max": 0.0,
+                                     "converged": True}
             wz = op.left(qy)  # (Qy^T P)^T: its singular values are the Ritz values
-            ev = np.linalg.eigvalsh(dp.gram(wz, wz))
+            ev = np.linalg.eigvalsh(ops.gram_rows(dp, wz, wz))
             sig = np.sqrt(np.clip(ev[::-1], 0.0, None))
             iters_total += 1
             t4 = float(np.sum(np.maximum(sig - 1.0, 0.0) ** 2))
             if prev is not None and abs(sig[0] - prev[0]) <= tol * max(1.0, sig[0]) and \
                     abs(t4 - prev[1]) <= tol * max(1.0, t4):
+                converged = True
                 break
-            # t4 only needs sigma(P) against 1.  After q steps from a Gaussian start
-            # the top Ritz value theta of the subspace (power) iteration on P^T P
-            # satisfies P[theta^2 < (1 - eps) sigma_max^2] <= 1.648 sqrt(n)
-            # e^(-eps (2q - 1)) (Kuczynski & Wozniakowski 1992).  With eps = 1/2 and
-            # q >= _Q_BOUND(n) that is < 1e-6, so sqrt(2) theta < 1 proves every
-            # sigma(P) < 1 and t4 = 0 exactly (the reference's dense SVD value).
-            if it + 1 >= _q_bound(n) and math.sqrt(2.0) * sig[0] < 1.0:
-                return sig, {"t4_method": "subspace", "block": b, "iters": iters_total,
-                             "sigma_p_max": float(sig[0]),
-                             "t4_bound": "sigma_max(P) < sqrt(2) theta_max < 1 "
-                                         "(failure prob < 1e-6)"}
+            # t4 only needs sigma(P) against 1: a certified sigma_max(P) < 1
+            # makes t4 = 0 exactly (the reference's dense value)
+            for ome, fac, q_need in bounds:
+                if it + 1 >= q_need and fac * sig[0] < 1.0:
+                    return sig, {"t4_method": "subspace", "block": b, "iters": iters_total,
+                                 "sigma_p_max": float(sig[0]), "converged": True,
+                                 "t4_bound": f"sigma_max(P) <= {fac:.4g} theta_max < 1 after "
+                                             f"{it + 1} >= {q_need} passes (power-method "
+                                             f"bound, failure prob < {_FAIL_PROB:g} over "
+                                             f"the random start)"}
             prev = (sig[0], t4)
-            q, _ = device_thin_qr(dp, wz)
-        if sig[-1] < 1.0 or b >= cap:
-            return sig, {"t4_method": "subspace", "block": b, "iters": iters_total,
-                         "sigma_p_max": float(sig[0])}
+            q, _ = device_thin_qr(dp, wz, ops.host if ops.sharded else None)
+        info = {"t4_method": "subspace", "block": b, "iters": iters_total,
+                "sigma_p_max": float(sig[0]) if sig.size else 0.0, "converged": converged}
+        if not converged:
+            warnings.warn(f"certificate: subspace iteration for sigma(P) did not converge in "
+                          f"{max_iter} passes; t4 is a lower bound", RuntimeWarning)
+            return sig, info
+        if sig.size == 0 or sig[-1] < 1.0 or b >= cap:
+            return sig, info
         b = min(2 * b, cap)
 
 
-def certificate(l_factors, spec, f_bound_hint=None, rank_tol=1e-10, dense_limit=DENSE_LIMIT):
-    """Certify L = U V^T for the convex objective (certificate.py:77-141)."""
-    import torch
-
-    lam = spec.lambda_l
-    m, n = spec.shape
-    k = l_factors.k
-    dp = spec.device("fp64")
-    z = torch.from_numpy(np.ascontiguousarray(l_factors.flatten())).to(dp.device)
-    u1, sig, v1, all_sig = _device_factor_svd(dp, z, m, n, k, rank_tol)
+def certificate_core(dp, z, m, n_total, k, lam, rank_tol, f_zero, f_bound_hint, ops):
+    """The certificate (certificate.py:77-141) of the device iterate z = [U | V_p]
+    against the device problem dp (a column shard when `ops` is sharded)."""
+    u = z[: m * k].reshape(m, k)
+    v = z[m * k:].reshape(dp.n, k)
+    u1, sig, v1, all_sig = _device_factor_svd(dp, u, v, rank_tol, ops)
     r = sig.shape[0]
     l_norm = float(np.sqrt(np.sum(all_sig * all_sig)))  # |U V^T|_F = |R_U R_V^T|_F
-    info = {}
     if r > 0:
         gv1, gtu1 = dp.apply(k, z, w_right=v1, w_left=u1)
+        ops.dev(gv1)
         b = gv1.mul_(-1.0 / lam)  # D V1            (m x r)
-        at = gtu1.mul_(-1.0 / lam)  # (U1^T D)^T     (n x r)
-        c = dp.gram(at, v1)  # U1^T D V1 (r x r)
+        at = gtu1.mul_(-1.0 / lam)  # (U1^T D)^T     (n_p x r)
+        c = ops.gram_rows(dp, at, v1)  # U1^T D V1 (r x r)
         csq = float(np.sum(c * c))
         t1 = float(np.sum((np.eye(r) - c) ** 2))
-        t2 = _sq(dp, at) - csq
-        t3 = _sq(dp, b) - csq
+        t2 = float(np.trace(ops.gram_rows(dp, at, at))) - csq
+        t3 = float(np.trace(dp.gram(b, b))) - csq
         if t2 < -1e-9 or t3 < -1e-9:  # certificate.py:108-115
-            t2 = _sq(dp, at - dp.matmul_small(v1, c.T))
-            t3 = _sq(dp, b - dp.matmul_small(u1, c))
+            a2 = at - dp.matmul_small(v1, c.T)
+            b2 = b - dp.matmul_small(u1, c)
+            t2 = float(np.trace(ops.gram_rows(dp, a2, a2)))
+            t3 = float(np.trace(dp.gram(b2, b2)))
             if t2 < -1e-9 or t3 < -1e-9:
                 raise NumericalError(
                     f"certificate cross terms negative after recompute: t2={t2}, t3={t3}")
@@ -205,20 +266,29 @@ def certificate(l_factors, spec, f_bound_hint=None, rank_tol=1e-10, dense_limit=
     else:
         t1 = t2 = t3 = 0.0
         u1 = v1 = None
-    if m * n <= dense_limit:
-        sp = _dense_sigmas(dp, z, k, lam, u1, v1)
-        info = {"t4_method": "dense", "sigma_p_max": float(sp[0]) if sp.size else 0.0}
-    else:
-        op = _ProjectedOperator(dp, z, k, lam, u1, v1)
-        sp, info = _subspace_sigmas(op, n, m, r)
+    precision = "fp32" if (m * n_total > FP32_PRODUCTS_MIN_ELEMS and "f32" in dp.store) \
+        else "fp64"
+    op = _ProjectedOperator(dp, z, k, lam, u1, v1, ops, precision)
+    sp, info = _subspace_sigmas(op, n_total, m, r)
+    info["products"] = precision
     over = np.maximum(sp - 1.0, 0.0)
     t4 = float(np.sum(over * over))
     info["n_sigma_over_1"] = int(np.sum(sp > 1.0))
     lsq = lam * lam
     terms = (lsq * t1, lsq * t2, lsq * t3, lsq * t4)
     e_norm = math.sqrt(sum(terms))
-    f_zero = dp.f_zero
     f_bound = f_zero if f_bound_hint is None else min(float(f_bound_hint), f_zero)
     gap = e_norm * (l_norm + f_bound / lam)
     return CertificateReport(e_norm=e_norm, terms=terms, f_bound=f_bound, gap_bound=gap, r=r,
                              l_norm=l_norm, info=info)
+
+
+def certificate(l_factors, spec, f_bound_hint=None, rank_tol=1e-10):
+    """Certify L = U V^T for the convex objective (certificate.py:77-141)."""
+    import torch
+
+    m, n = spec.shape
+    dp = spec.device("fp64")
+    z = torch.from_numpy(np.ascontiguousarray(l_factors.flatten())).to(dp.device)
+    return certificate_core(dp, z, m, n, l_factors.k, spec.lambda_l, rank_tol, dp.f_zero,
+                            f_bound_hint, CertOps(n_total=n))

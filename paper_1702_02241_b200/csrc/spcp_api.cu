@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -28,14 +29,23 @@ namespace spcp {
 // Launch with programmatic stream serialization (PDL): the kernel may start
 // launching while its predecessor drains; it calls griddepcontrol.wait before
 // touching the predecessor's results.  SPCP_PDL=0 turns it off.
-static bool pdl_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("SPCP_PDL");
-    on = (e && std::string(e) == "0") ? 0 : 1;
-  }
-  return on == 1;
+// Environment switches are read once per process (thread-safe static
+// initialisation), never per launch.
+static std::string env_str(const char* name) {
+  const char* e = getenv(name);
+  return e ? std::string(e) : std::string();
 }
+static bool pdl_enabled() {
+  static const bool on = env_str("SPCP_PDL") != "0";
+  return on;
+}
+
+// Per-device caches of one-time launch setup (kernel attributes, occupancy):
+// cudaFuncSetAttribute applies to the current device only, so a process that
+// drives several GPUs must set it once per device.  Zero = not yet set.
+constexpr int kMaxDevices = 64;
+using DevFlags = std::atomic<int>[kMaxDevices];
+static int dev_slot(int device) { return device >= 0 && device < kMaxDevices ? device : 0; }
 template <typename... KArgs, typename... Args>
 static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                               cudaStream_t stream, Args&&... args) {
@@ -61,12 +71,8 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 bool debug_sync() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SPCP_DEBUG_SYNC");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
+  static const bool v = env_str("SPCP_DEBUG_SYNC") == "1";
+  return v;
 }
 
 int cuda_fail(cudaError_t e, const char* where) {
@@ -176,12 +182,14 @@ static int launch_stream(spcp_problem* p, StreamParams sp, LaunchShape& shape, b
   using G = StreamGeom<T>;
   auto kern = stream_kernel<T, TX, KR, PW, MODE, MASK>;
   constexpr size_t smem = stream_smem_bytes<T, TX, KR, PW, MODE, MASK>();
-  static int occ = -1;  // per instantiation
-  if (occ < 0) {
+  static DevFlags occ_dev = {};  // per instantiation and device
+  int occ = occ_dev[dev_slot(p->device)].load(std::memory_order_relaxed);
+  if (occ == 0) {
     SPCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int o = 0;
     SPCP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, G::NT, smem));
     occ = std::max(o, 1);
+    occ_dev[dev_slot(p->device)].store(occ, std::memory_order_relaxed);
   }
   const int64_t nrb = p->m_pad / G::BM;
   const int64_t ntiles = p->n_pad / G::BN;
@@ -354,8 +362,8 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 static bool tc_env_enabled() {
-  const char* e = getenv("SPCP_FP32_KERNEL");
-  return !(e && std::string(e) == "simt");
+  static const bool on = env_str("SPCP_FP32_KERNEL") != "simt";
+  return on;
 }
 
 // Static schedule: tiles (sb, tc) in 2-D super-block order, exactly balanced
@@ -363,15 +371,16 @@ static bool tc_env_enabled() {
 // the reduce kernel folds in a fixed order.
 static int tc_build(spcp_problem* p) {
   if (p->tc_ready) return SPCP_OK;
-  static EncodeTiledFn enc = nullptr;
-  if (!enc) {
+  static const EncodeTiledFn enc = []() -> EncodeTiledFn {
     cudaDriverEntryPointQueryResult q;
     void* fn = nullptr;
-    SPCP_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
-    if (!fn || q != cudaDriverEntryPointSuccess)
-      return fail(SPCP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-    enc = reinterpret_cast<EncodeTiledFn>(fn);
-  }
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    return reinterpret_cast<EncodeTiledFn>(fn);
+  }();
+  if (!enc) return fail(SPCP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   {
     cuuint64_t dims[2] = {cuuint64_t(p->ldx), cuuint64_t(p->m_pad)};
     cuuint64_t strides[1] = {cuuint64_t(p->ldx) * 4};
@@ -379,8 +388,9 @@ static int tc_build(spcp_problem* p) {
     cuuint32_t es[2] = {1, 1};
     // SPCP_X_L2PROMO = none | 64 | 128 | 256 (default): L2 promotion of the X stream
     CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-    if (const char* e = getenv("SPCP_X_L2PROMO")) {
-      const std::string v(e);
+    static const std::string promo_env = env_str("SPCP_X_L2PROMO");
+    if (!promo_env.empty()) {
+      const std::string& v = promo_env;
       promo = v == "none" ? CU_TENSOR_MAP_L2_PROMOTION_NONE
               : v == "64" ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
               : v == "128" ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
@@ -501,10 +511,10 @@ template <int KP16, bool MASK, int SEG = 0>
 static int tc_launch(spcp_problem* p, int64_t k) {
   using C = TcCfg<KP16, MASK, SEG>;
   auto kern = tc_eval_kernel<KP16, MASK, SEG>;
-  static bool attr = false;
-  if (!attr) {
+  static DevFlags attr = {};  // per instantiation and device
+  if (!attr[dev_slot(p->device)].load(std::memory_order_relaxed)) {
     SPCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    attr = true;
+    attr[dev_slot(p->device)].store(1, std::memory_order_relaxed);
   }
   TcParams tp{};
   tp.units = p->tc_units.as<TcUnit>();
@@ -516,34 +526,17 @@ static int tc_launch(spcp_problem* p, int64_t k) {
   tp.pright = p->pright.as<float>();
   tp.pphi = p->pphi.as<double>();
   tp.kstore = int(round_up(k, 4));
-  {
-    const char* e = getenv("SPCP_TC_DEBUG");
-    tp.debug = e ? atoi(e) : 0;
-  }
+#ifdef SPCP_TC_TIMESTAMPS
   static long long* dbg = nullptr;
-  if (tp.debug & 4) {
-    if (!dbg) SPCP_CUDA(cudaMalloc(&dbg, 64 * 32 * sizeof(long long)));
-    SPCP_CUDA(cudaMemsetAsync(dbg, 0, 64 * 32 * sizeof(long long), p->stream));
-    tp.dbg_ts = dbg;
-  }
+  if (!dbg) SPCP_CUDA(cudaMalloc(&dbg, 64 * 32 * sizeof(long long)));
+  SPCP_CUDA(cudaMemsetAsync(dbg, 0, 64 * 32 * sizeof(long long), p->stream));
+  tp.dbg_ts = dbg;
+#endif
   if (p->prof && prof_begin(p)) return SPCP_ERR_CUDA;
   SPCP_CUDA(launch_pdl(kern, dim3(p->tc_grid), dim3(C::NTHREADS), C::SMEM, p->stream, p->tc_xmap,
                        p->tc_mmap, tp));
   SPCP_CHECK_LAUNCH("tc_eval_kernel");
   if (p->prof && prof_end(p)) return SPCP_ERR_CUDA;
-  if (tp.debug & 4) {
-    long long h[64 * 32];
-    SPCP_CUDA(cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, p->stream));
-    SPCP_CUDA(cudaStreamSynchronize(p->stream));
-    FILE* f = fopen("gpurun_out/tc_ts.txt", "w");
-    if (f) {
-      for (int t = 0; t < 64; ++t) {
-        for (int c = 0; c < 26; ++c) fprintf(f, "%lld ", h[t * 32 + c] ? h[t * 32 + c] - h[0] : -1);
-        fprintf(f, "\n");
-      }
-      fclose(f);
-    }
-  }
   p->launches++;
   return SPCP_OK;
 }
@@ -583,8 +576,8 @@ static int tc_images_kc(spcp_problem* p, int64_t k, const double* z, const doubl
 
 // K-concatenated layout (k <= 20): SEG = round_up(k, 4)
 static bool tc_use_kc(int64_t k) {
-  const char* e = getenv("SPCP_TC_LAYOUT");
-  return k <= 20 && !(e && std::string(e) == "split");
+  static const bool split = env_str("SPCP_TC_LAYOUT") == "split";
+  return k <= 20 && !split;
 }
 
 template <bool MASK>
@@ -904,17 +897,13 @@ static int run_reduce(spcp_problem* p, int64_t k, int kp, int part_dtype, const 
     const bool skewed = std::max(lp_u, lp_v) >= 8 * std::min(lp_u, lp_v);  // C3: 1 vs 32
 #endif
     // balanced: SPCP_REDUCE_LPI = 2 (default) or 4 lanes per item
-    static int lpi_env = -1;
-    if (lpi_env < 0) {
-      const char* e = getenv("SPCP_REDUCE_LPI");
-      lpi_env = (e && std::string(e) == "4") ? 4 : 2;
-    }
+    static const int lpi_env = env_str("SPCP_REDUCE_LPI") == "4" ? 4 : 2;
     const int lanes_used = skewed ? lp : lpi_env;
     const int kind = skewed ? 2 : (lpi_env == 4 ? 1 : 0);
     // one wave of resident blocks (grid-stride over the items): a partial
     // second wave left ~1/3 of the SM time idle (ncu, C2)
-    static int resident[3] = {0, 0, 0};
-    int& res = resident[kind];
+    static std::atomic<int> resident[kMaxDevices][3] = {};
+    int res = resident[dev_slot(p->device)][kind].load(std::memory_order_relaxed);
     if (!res) {
       int per_sm = 0;
       cudaError_t e = kind == 2 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(
@@ -925,6 +914,7 @@ static int run_reduce(spcp_problem* p, int64_t k, int kp, int part_dtype, const 
                                       &per_sm, tc_reduce_lpi_kernel<2>, 256, 0);
       if (e != cudaSuccess || per_sm < 1) per_sm = 4;
       res = per_sm * kSMs;
+      resident[dev_slot(p->device)][kind].store(res, std::memory_order_relaxed);
     }
     const int nb = int(std::min<int64_t>((items * lanes_used + 255) / 256, res));
     if ((rc = p->blk.ensure(size_t(nb) * 6 * sizeof(double)))) return rc;
@@ -1202,7 +1192,6 @@ int spcp_problem_create(spcp_problem** out, int device, int64_t m, int64_t n, co
 
 int spcp_problem_destroy(spcp_problem* p) {
   if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
-  if (!p) return SPCP_OK;
   cudaSetDevice(p->device);
   if (p->stream) cudaStreamSynchronize(p->stream);
   for (DevBuf* b : {&p->x32, &p->x64, &p->mbits, &p->uc, &p->vc, &p->wr, &p->wl, &p->pleft,
@@ -1486,9 +1475,8 @@ int spcp_vec_lincomb(spcp_problem* p, int64_t len, int count, const double* coef
   return SPCP_OK;
 }
 
-int spcp_vec_gram(spcp_problem* p, int64_t len, int na, const double* const* a, int nb,
-                  const double* const* b, double* out_host) {
-  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
+static int vec_gram_impl(spcp_problem* p, int64_t len, int na, const double* const* a, int nb,
+                         const double* const* b, double* out_host, double* out_dev) {
   int rc;
   SPCP_CUDA(cudaSetDevice(p->device));
   if (nb < 1 || nb > 4 || na < 1) return fail(SPCP_ERR_VALUE, "vec_gram: need 1<=nb<=4, na>=1");
@@ -1508,15 +1496,31 @@ int spcp_vec_gram(spcp_problem* p, int64_t len, int na, const double* const* a, 
       default: vec_gram_kernel<4><<<nblk, 256, 0, p->stream>>>(gp, cnt, len, part); break;
     }
     SPCP_CHECK_LAUNCH("vec_gram");
-    vec_gram_fold_kernel<<<1, 256, 0, p->stream>>>(part, nblk, cnt, nb, p->out_dev.as<double>());
+    double* dst = out_dev ? out_dev + size_t(a0) * nb : p->out_dev.as<double>();
+    vec_gram_fold_kernel<<<1, 256, 0, p->stream>>>(part, nblk, cnt, nb, dst);
     SPCP_CHECK_LAUNCH("vec_gram_fold");
     p->launches += 2;
-    SPCP_CUDA(cudaMemcpyAsync(p->host_out, p->out_dev.ptr, size_t(cnt) * nb * sizeof(double),
-                              cudaMemcpyDeviceToHost, p->stream));
-    SPCP_CUDA(cudaStreamSynchronize(p->stream));
-    std::memcpy(out_host + size_t(a0) * nb, p->host_out, size_t(cnt) * nb * sizeof(double));
+    if (out_host) {
+      SPCP_CUDA(cudaMemcpyAsync(p->host_out, p->out_dev.ptr, size_t(cnt) * nb * sizeof(double),
+                                cudaMemcpyDeviceToHost, p->stream));
+      SPCP_CUDA(cudaStreamSynchronize(p->stream));
+      std::memcpy(out_host + size_t(a0) * nb, p->host_out, size_t(cnt) * nb * sizeof(double));
+    }
   }
   return SPCP_OK;
+}
+
+int spcp_vec_gram(spcp_problem* p, int64_t len, int na, const double* const* a, int nb,
+                  const double* const* b, double* out_host) {
+  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
+  return vec_gram_impl(p, len, na, a, nb, b, out_host, nullptr);
+}
+
+int spcp_vec_gram_dev(spcp_problem* p, int64_t len, int na, const double* const* a, int nb,
+                      const double* const* b, double* out_dev) {
+  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
+  if (!out_dev) return fail(SPCP_ERR_VALUE, "vec_gram_dev: null output");
+  return vec_gram_impl(p, len, na, a, nb, b, nullptr, out_dev);
 }
 
 int spcp_gram(spcp_problem* p, int64_t rows, int64_t pa, const double* a, int64_t qb,

@@ -41,6 +41,14 @@
 
 #include <utility>
 
+// Bisection switches for tools/bisect_*.sh, compile-time only (the product
+// library is built with 0): 1 skip G^T U stores, 2 skip G.V stores, 8 skip all
+// MMAs (pipeline skeleton), 16 / 32 / 64 skip the G^T U / G.V / residual MMAs,
+// 128 epilogue ignores MMA completion, 256 drop G^T U stores, 512 store only.
+#ifndef SPCP_TC_DEBUG_BITS
+#define SPCP_TC_DEBUG_BITS 0
+#endif
+
 #ifndef SPCP_TC_XPF
 #define SPCP_TC_XPF 0  // X tiles prefetched into L2 ahead of the stage ring (measured: no gain)
 #endif
@@ -77,11 +85,9 @@ struct TcParams {
   float* pright;  // [gt_slots][64][kstore]
   double* pphi;   // [grid]
   int kstore;  // partial row stride (floats): k rounded up to 4
-  int debug;  // bisection switches (SPCP_TC_DEBUG): 1 skip GT stores, 2 skip GV stores,
-              // 8 skip all MMAs (pipeline skeleton only), 16 / 32 / 64 skip the
-              // G^T U / G.V / residual MMAs, 128 epilogue ignores MMA completion
-              // (timing only: decouples the epilogue from the reduction MMAs)
-  long long* dbg_ts;  // [64][16] per-tile timestamps of CTA 0 (SPCP_TC_TIMESTAMPS builds)
+#ifdef SPCP_TC_TIMESTAMPS
+  long long* dbg_ts;  // [64][32] per-tile timestamps of CTA 0 (tools/ts_run.sh builds only)
+#endif
 };
 
 template <int KP16, bool MASK, int SEG = 0>
@@ -261,7 +267,7 @@ __device__ __noinline__ void tc_residual_issuer(unsigned char* sm, TcBarriers* b
   using namespace tc;
   constexpr uint32_t ID_RES = idesc_f16(128, 64, false, false);
   constexpr int KS = KP16 / 16;
-  const bool do_mma = !(p.debug & 8);
+  const bool do_mma = !(SPCP_TC_DEBUG_BITS & 8);
   const uint32_t u0 = smem_u32(sm + C::OFF_U), v0 = smem_u32(sm + C::OFF_V);
   TcUnit un_next = T > 0 ? units[0] : TcUnit{};
   const uint64_t dU_k = umma_desc(u0, 16, 8 * C::RB, C::SWK);  // residual A (K-major)
@@ -280,7 +286,7 @@ __device__ __noinline__ void tc_residual_issuer(unsigned char* sm, TcBarriers* b
         // previous run's residual MMAs, which read the single TMEM copy
         tc_fence_after();
         const uint64_t du = dU_k + uint64_t(ubuf * (C::U_BYTES >> 4));
-        if (do_mma && !(p.debug & 64)) {
+        if (do_mma && !(SPCP_TC_DEBUG_BITS & 64)) {
           static_for<C::NKS>([&](auto I) {
             tmem_cp_128x256b_w(tm + C::T_U + 8 * I, du + uint64_t(2 * I));
           });
@@ -296,7 +302,7 @@ __device__ __noinline__ void tc_residual_issuer(unsigned char* sm, TcBarriers* b
     tc_fence_after();
     const uint64_t da = dU_k + uint64_t(ubuf * (C::U_BYTES >> 4));
     const uint64_t db = dV_k + uint64_t(st * (C::V_BYTES >> 4));
-    if (do_mma && !(p.debug & 64)) {
+    if (do_mma && !(SPCP_TC_DEBUG_BITS & 64)) {
       // uh.vh + uh.vm + um.vh: product q uses U split (q == 2), V split (q == 1)
       const uint32_t dt = tm + C::T_S + b * 64;
       if constexpr (C::KC) {
@@ -335,7 +341,7 @@ __device__ __noinline__ void tc_reduction_issuer(unsigned char* sm, TcBarriers* 
   // gl part, kept as separate partial rows and summed by the reduce kernel
   constexpr uint32_t ID_GV = idesc_f16(128, C::GVW, false, true);
   constexpr uint32_t ID_GT = idesc_f16(C::KC ? 128 : 64, C::GTW, true, true);
-  const bool do_mma = !(p.debug & 8);
+  const bool do_mma = !(SPCP_TC_DEBUG_BITS & 8);
   const uint32_t u0 = smem_u32(sm + C::OFF_U), v0 = smem_u32(sm + C::OFF_V);
   const uint32_t g0 = smem_u32(sm + C::OFF_G);
   TcUnit un_next = T > 0 ? units[0] : TcUnit{};
@@ -355,17 +361,17 @@ __device__ __noinline__ void tc_reduction_issuer(unsigned char* sm, TcBarriers* 
     TC_TS(t, ROLE == 2 ? 26 : 14);
     mbar_wait(&bar->g_full[b], (t >> 1) & 1);
     TC_TS(t, ROLE == 2 ? 27 : 2);
-    if (ROLE != 2 && !(p.debug & 128)) mbar_wait(&bar->gt_empty[gtb], ((t / C::NGT) & 1) ^ 1);
-    if (ROLE != 1 && first && !(p.debug & 128)) mbar_wait(&bar->gv_empty[gvb], ((run >> 1) & 1) ^ 1);
+    if (ROLE != 2 && !(SPCP_TC_DEBUG_BITS & 128)) mbar_wait(&bar->gt_empty[gtb], ((t / C::NGT) & 1) ^ 1);
+    if (ROLE != 1 && first && !(SPCP_TC_DEBUG_BITS & 128)) mbar_wait(&bar->gv_empty[gvb], ((run >> 1) & 1) ^ 1);
     TC_TS(t, ROLE == 2 ? 28 : 3);
     tc_fence_after();
     const uint64_t dUn = dUn0 + uint64_t(ubuf * (C::U_BYTES >> 4));
     const uint64_t goff = uint64_t((C::GB == 1 ? 0 : b) * (C::G_BYTES >> 4));
     const uint32_t gt = tm + C::T_GT + gtb * C::GTW;
-    if (C::KC && ROLE != 2 && do_mma && !(p.debug & 16)) {
+    if (C::KC && ROLE != 2 && do_mma && !(SPCP_TC_DEBUG_BITS & 16)) {
       // stacked [gh; gl]^T U: 8 K-steps of 16 tile rows (A += 2048 B, B += 16 RB)
       mma_ss_batch<8, 128, C::RB>(gt, dGm + goff, dUn, ID_GT, 0u);
-    } else if (ROLE != 2 && do_mma && !(p.debug & 16)) {
+    } else if (ROLE != 2 && do_mma && !(SPCP_TC_DEBUG_BITS & 16)) {
       static_for<8>([&](auto I) {
         constexpr int ks = I;
         constexpr int uo = (ks * 16 * C::RB) >> 4, go = (2048 * ks) >> 4;
@@ -388,9 +394,9 @@ __device__ __noinline__ void tc_reduction_issuer(unsigned char* sm, TcBarriers* 
     TC_TS(t, ROLE == 2 ? 29 : 25);
     const uint64_t dVn = dVn0 + uint64_t(st * (C::V_BYTES >> 4));
     const uint32_t gv = tm + C::T_GV + gvb * C::GVW;
-    if (C::KC && ROLE != 1 && do_mma && !(p.debug & 32)) {
+    if (C::KC && ROLE != 1 && do_mma && !(SPCP_TC_DEBUG_BITS & 32)) {
       mma_gv_ts_batch<C::RB>(gv, tm + C::T_S + (t % C::NSB) * 64, dVn, ID_GV, first ? 0u : 1u);
-    } else if (ROLE != 1 && do_mma && !(p.debug & 32)) {
+    } else if (ROLE != 1 && do_mma && !(SPCP_TC_DEBUG_BITS & 32)) {
       static_for<4>([&](auto I) {
         constexpr int ks = I;
         constexpr int vo = (ks * 16 * C::RB) >> 4;
@@ -422,7 +428,7 @@ __device__ __noinline__ void tc_reduction_issuer(unsigned char* sm, TcBarriers* 
     TC_TS(t, ROLE == 2 ? 30 : 15);
   }
   // decoupled-timing mode: nobody else waited for the last reductions
-  if ((p.debug & 128) && T > 0) mbar_wait(&bar->gs_empty[(T - 1) & 1], ((T - 1) >> 1) & 1);
+  if ((SPCP_TC_DEBUG_BITS & 128) && T > 0) mbar_wait(&bar->gs_empty[(T - 1) & 1], ((T - 1) >> 1) & 1);
 }
 
 template <int KP16, bool MASK, int SEG = 0>
@@ -603,10 +609,10 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK, SEG>::NTHREADS, 1)
     // G^T U of tile t2 (this group's previous tile) -> CTA-private slot
     auto drain_gt = [&](int t2, const TcUnit& u2) {
       const int b = t2 % C::NGT;
-      if (!(p.debug & 128)) mbar_wait(&bar->gt_full[b], (t2 / C::NGT) & 1);
+      if (!(SPCP_TC_DEBUG_BITS & 128)) mbar_wait(&bar->gt_full[b], (t2 / C::NGT) & 1);
       tc_fence_after();
       if constexpr (C::KC) {
-        if (!(p.debug & 1)) {
+        if (!(SPCP_TC_DEBUG_BITS & 1)) {
           // M = 128 stacked accumulator: lane = slot row (0..63 gh part, 64..127 gl
           // part); output column c = D[c] (uh) + D[2 SEG + c] (um)
           // slot layout [kst / 4][128 rows][4]: a warp's float4 stores cover 512
@@ -627,9 +633,9 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK, SEG>::NTHREADS, 1)
                                            __uint_as_float(v[2]) + __uint_as_float(w[2]),
                                            __uint_as_float(v[3]) + __uint_as_float(w[3]));
               float* d4 = dst + cc * 128;  // chunk cc / 4 of 128 rows x 4
-              if (p.debug & 256) {
+              if (SPCP_TC_DEBUG_BITS & 256) {
                 if (o.x == 1.2345f) d4[0] = o.y;  // keep the loads, drop the stores
-              } else if (first || (p.debug & 512)) {
+              } else if (first || (SPCP_TC_DEBUG_BITS & 512)) {
                 *reinterpret_cast<float4*>(d4) = o;
               } else {
                 red_add_v4(d4, __float_as_uint(o.x), __float_as_uint(o.y),
@@ -638,7 +644,7 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK, SEG>::NTHREADS, 1)
             }
           });
         }
-      } else if (!(p.debug & 1)) {
+      } else if (!(SPCP_TC_DEBUG_BITS & 1)) {
         // chunked slot [kst / 4][64 rows][4] (coalesced float4 stores)
         float* dst = p.pright + size_t(u2.gt_slot) * 64 * kst + (16 * q + lane) * 4;
         const bool first = (u2.flags & TCU_FIRST_TOUCH) != 0;
@@ -680,10 +686,10 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK, SEG>::NTHREADS, 1)
     auto drain_gv = [&](const TcUnit& u2) {
       const int run = u2.gv_slot - run0;
       const int gvb = run & 1;
-      if (!(p.debug & 128)) mbar_wait(&bar->gv_full[gvb], (run >> 1) & 1);
+      if (!(SPCP_TC_DEBUG_BITS & 128)) mbar_wait(&bar->gv_full[gvb], (run >> 1) & 1);
       tc_fence_after();
       if constexpr (C::KC) {
-        if (!(p.debug & 2)) {
+        if (!(SPCP_TC_DEBUG_BITS & 2)) {
           // output column c = D[c] (vh) + D[SEG + c] (vm)
           float* dst = p.pleft + size_t(u2.gv_slot) * 128 * kst + row * 4;  // [kst/4][128][4]
           const uint32_t col = tm + lane_addr + C::T_GV + gvb * C::GVW;
@@ -703,7 +709,7 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK, SEG>::NTHREADS, 1)
             }
           });
         }
-      } else if (!(p.debug & 2)) {
+      } else if (!(SPCP_TC_DEBUG_BITS & 2)) {
         float* dst = p.pleft + size_t(u2.gv_slot) * 128 * kst + row * 4;  // [kst/4][128][4]
         constexpr int CH = GTC < 16 ? GTC : 16;
 #pragma unroll
@@ -823,7 +829,7 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK, SEG>::NTHREADS, 1)
         // (the other parity's barrier, phase (t-1)/2; in-order MMA completion
         // covers tile t-2).  Per-parity barriers never lag two phases behind.
         if (t >= 1) mbar_wait(&bar->gs_empty[(t - 1) & 1], ((t - 1) >> 1) & 1);
-      } else if (!(p.debug & 128)) {
+      } else if (!(SPCP_TC_DEBUG_BITS & 128)) {
         mbar_wait(&bar->gs_empty[b], ((t >> 1) & 1) ^ 1);
       }
       if (ts_w) TC_TS(t, 9);

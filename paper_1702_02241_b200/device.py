@@ -252,6 +252,16 @@ class DeviceProblem:
                                 _ptr_array(b_list), out))
         return np.frombuffer(out, dtype=np.float64).reshape(na, nb).copy()
 
+    def vec_gram_dev(self, a_list, b_list, out=None):
+        """The same dots into a device float64 tensor (na x nb), no host sync."""
+        torch = torch_mod()
+        na, nb = len(a_list), len(b_list)
+        if out is None:
+            out = torch.empty((na, nb), dtype=torch.float64, device=self.device)
+        check(lib.spcp_vec_gram_dev(self.h, a_list[0].numel(), na, _ptr_array(a_list), nb,
+                                    _ptr_array(b_list), dptr(out)))
+        return out
+
     def lincomb(self, coefs, vecs, out):
         cnt = len(vecs)
         c = (ctypes.c_double * cnt)(*[float(x) for x in coefs])

@@ -4,16 +4,28 @@ Rank p owns columns J_p = [col0, col0 + n_p) of X (and of the mask), the
 matching rows V_p of V, and a replica of U.  Per evaluation:
 
   local fused kernel -> phi_p, G_p V_p (m x k), grad_V shard, V-part dots
-  ONE all-reduce of G_p V_p (fp32 in fp32 mode) + one of 4 fp64 scalars
-  -> grad_U = sum_p G_p V_p + lambda U on every rank (identical bits).
+  one all-reduce step: G_p V_p (fp32 in fp32 mode) and the 4 fp64 scalars
+  travel in ONE fused NCCL launch (a coalesced group of the two buffers; the
+  dtypes differ, so they cannot share one buffer without losing the scalars'
+  fp64 sums) -> grad_U = sum_p G_p V_p + lambda U on every rank (identical bits).
 
 L-BFGS vectors keep the [U | V_p] layout: U-part inner products are computed
-redundantly (identical on all ranks), V-part ones are summed across ranks in
-the same all-reduce call per iteration (`vec_gram`), so the replicated U and
-the history stay bit-identical on every rank.  NCCL over NVLink/NVSwitch is
-the transport on GPUs (torch.distributed, backend "nccl"); the host logic is
-exercised with backend "gloo" on CPU by the tests (tests/test_dist_gloo.py).
+redundantly (identical on all ranks), V-part ones are summed across ranks on
+the device (`vec_gram_dev` + all-reduce, one copy to the host per iteration),
+so the replicated U and the history stay bit-identical on every rank.  NCCL
+over NVLink/NVSwitch is the transport on GPUs (torch.distributed, backend
+"nccl"; `pin_nccl()` fixes the algorithm and protocol so repeated runs sum in
+the same order); the host logic is exercised with backend "gloo" on CPU by the
+tests (tests/test_dist_gloo.py).
+
+The certificate over column shards (`certificate_sharded`, certificate.py:77-141)
+is the single-GPU code with CertOps reductions: the m x b products D_p W_p of
+the subspace iteration and D_p V1_p are all-reduced, Grams of row-sharded
+n-side blocks (V, V1, D^T U1, the subspace block) are summed as host k x k /
+b x b matrices.
 """
+
+import os
 
 import math
 
@@ -22,7 +34,15 @@ import numpy as np
 from .lbfgs import DeviceLbfgs
 from .report import IterateState, SolveReport, WorkTimer
 
-__all__ = ["ShardedSpace", "solve_split_spcp_sharded", "allreduce_host", "shard_bounds"]
+__all__ = ["ShardedSpace", "solve_split_spcp_sharded", "certificate_sharded", "allreduce_host",
+           "shard_bounds", "pin_nccl", "allreduce_fused"]
+
+
+def pin_nccl():
+    """Fix NCCL's algorithm and protocol (before the communicator is created)
+    so the all-reduce order, hence the bits, repeat run to run."""
+    os.environ.setdefault("NCCL_ALGO", "Ring")
+    os.environ.setdefault("NCCL_PROTO", "Simple")
 
 
 def shard_bounds(n_total, world, rank):
@@ -47,6 +67,21 @@ def allreduce_host(arr, device, group=None):
     return t.cpu().numpy()
 
 
+def allreduce_fused(tensors, group=None):
+    """Sum several device buffers across ranks in one collective launch: an
+    NCCL group (torch's coalescing manager) when the backend is NCCL, plain
+    calls otherwise (gloo on CPU tests)."""
+    dist = _dist()
+    if dist.get_backend(group) == "nccl" and hasattr(dist, "_coalescing_manager"):
+        with dist._coalescing_manager(group=group, device=tensors[0].device, async_ops=True) as cm:
+            for t in tensors:
+                dist.all_reduce(t, group=group)
+        cm.wait()
+        return
+    for t in tensors:
+        dist.all_reduce(t, group=group)
+
+
 class ShardedSpace:
     """DeviceLbfgs vector space over [U (replicated) | V_p (shard)] vectors.
 
@@ -67,6 +102,7 @@ class ShardedSpace:
         self.gu64 = torch.empty(self.mk, dtype=torch.float64, device=dp.device)
         self.scal = torch.empty(4, dtype=torch.float64, device=dp.device)
         self.comm_bytes = 0
+        self.comm_calls = 0
 
     def empty(self):
         return self.dp.empty(self.length)
@@ -78,9 +114,9 @@ class ShardedSpace:
         code = SPCP_F32 if precision == "fp32" else SPCP_F64
         gu = self.gu32 if (precision == "fp32" and self.k <= 64) else self.gu64
         self.dp.eval_partial(self.k, code, z, d, alpha, gu, self.scal, g_out)
-        dist.all_reduce(gu, group=self.group)
-        dist.all_reduce(self.scal, group=self.group)
+        allreduce_fused([gu, self.scal], self.group)
         self.comm_bytes += gu.numel() * gu.element_size() + 32
+        self.comm_calls += 1
         out = self.dp.eval_finish(self.k, code, z, d, alpha, gu, self.scal, g_out)
         return out[0], out[3], out[4]
 
@@ -89,9 +125,17 @@ class ShardedSpace:
         ub = [b[: self.mk] for b in b_list]
         va = [a[self.mk:] for a in a_list]
         vb = [b[self.mk:] for b in b_list]
-        u_part = self.dp.vec_gram(ua, ub)
-        v_part = self.dp.vec_gram(va, vb) if self.n > 0 else np.zeros_like(u_part)
-        return u_part + allreduce_host(v_part, self.comm_device, self.group)
+        dev = getattr(self.dp, "vec_gram_dev", None)
+        if dev is None:  # host-side test doubles
+            u_part = self.dp.vec_gram(ua, ub)
+            v_part = self.dp.vec_gram(va, vb) if self.n > 0 else np.zeros_like(u_part)
+            return u_part + allreduce_host(v_part, self.comm_device, self.group)
+        import torch
+
+        u_part = dev(ua, ub)
+        v_part = dev(va, vb) if self.n > 0 else torch.zeros_like(u_part)
+        _dist().all_reduce(v_part, group=self.group)
+        return (u_part + v_part).cpu().numpy()
 
     def lincomb(self, coefs, vecs, out):
         return self.dp.lincomb(coefs, vecs, out)
@@ -155,11 +199,16 @@ def solve_split_spcp_sharded(x_local, lambda_l, lambda_s, k, n_total, col0, cfg=
     n = int(x_local.shape[1])
     precision = _effective_precision(cfg.precision, (m, n_total))
     store = ("f32",) if precision in ("fp32", "mixed") else ("f64",)
-    if not isinstance(x_local, torch.Tensor):
+    if isinstance(x_local, torch.Tensor):
+        exact = x_local.dtype == torch.float32 or bool(
+            (x_local.float().double() == x_local).all())
+    else:
         xa = np.asarray(x_local)
-        if precision != "fp32" and not np.array_equal(xa.astype(np.float32).astype(xa.dtype),
-                                                      xa):
-            store = ("f32", "f64") if precision == "mixed" else ("f64",)
+        exact = bool(np.array_equal(xa.astype(np.float32).astype(xa.dtype), xa))
+    if precision != "fp32" and not exact:
+        # the fp64 phase must stream the unrounded X (ProblemSpec.device does
+        # the same check): keep an fp64 copy next to the fp32 one
+        store = ("f32", "f64") if precision == "mixed" else ("f64",)
     dp = DeviceProblem(x_local, lambda_l, lambda_s, mask_local, store=store, n_total=n_total,
                        col0=col0)
     comm_device = dp.device
@@ -187,8 +236,34 @@ def solve_split_spcp_sharded(x_local, lambda_l, lambda_s, k, n_total, col0, cfg=
     from .solver import FactorPair
 
     factors = FactorPair(zh[: m * k].reshape(m, k), zh[m * k:].reshape(n, k))
-    return SolveReport(solver="split", termination=res.termination, iterations=res.records,
-                       l=None, s=None, objective=res.objective, factors=factors,
-                       extra={"k_final": k, "columns_grown": 0, "n_evals": res.n_evals,
-                              "precision": precision, "allreduce_bytes": space.comm_bytes,
-                              "col0": col0, "n_local": n, "problem": dp})
+    rep = SolveReport(solver="split", termination=res.termination, iterations=res.records,
+                      l=None, s=None, objective=res.objective, factors=factors,
+                      extra={"k_final": k, "columns_grown": 0, "n_evals": res.n_evals,
+                             "precision": precision, "allreduce_bytes": space.comm_bytes,
+                             "allreduce_calls": space.comm_calls, "col0": col0, "n_local": n,
+                             "n_total": n_total, "problem": dp})
+    rep.device_state = (dp, k, z)
+    return rep
+
+
+def certificate_sharded(report, lambda_l=None, f_bound_hint=None, rank_tol=1e-10, group=None):
+    """certificate (certificate.py:77-141) of a column-sharded solve: every
+    rank passes its own SolveReport from solve_split_spcp_sharded; all ranks
+    return the same CertificateReport."""
+    from .certificate import CertOps, certificate_core
+
+    dp, k, z = report.device_state
+    ex = report.extra
+    lam = float(lambda_l if lambda_l is not None else dp.lambda_l)
+    dist = _dist()
+
+    def red_host(a):
+        return allreduce_host(a, dp.device, group)
+
+    def red_dev(t):
+        dist.all_reduce(t, group=group)
+
+    ops = CertOps(host=red_host, dev=red_dev, n_total=ex["n_total"], col0=ex["col0"])
+    f_zero = float(red_host(np.array([dp.f_zero]))[0])
+    hint = report.best_objective if f_bound_hint is None else f_bound_hint
+    return certificate_core(dp, z, dp.m, ex["n_total"], k, lam, rank_tol, f_zero, hint, ops)

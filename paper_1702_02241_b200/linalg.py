@@ -123,13 +123,21 @@ def _chol_upper(g):
 
 
 def device_thin_qr(dp, a, gram_reduce=None):
-    """Q, R (R host, diag >= 0) of a tall float64 device matrix a (rows x w).
+    """Q, R (R host) of a tall float64 device matrix a (rows x w), A = Q R.
 
     CholeskyQR2: R1 = chol(a^T a), Q1 = a R1^-1, R2 = chol(Q1^T Q1),
-    Q = Q1 R2^-1, R = R2 R1 (unique for full column rank, so Q matches the
-    reference's Householder QR with the diag(R) >= 0 convention).
-    `gram_reduce` sums Grams across column-sharded ranks (row-sharded a).
-    Rank-deficient input falls back to Householder QR on the device.
+    Q = Q1 R2^-1, R = R2 R1 (unique for full column rank with diag(R) > 0, so
+    Q matches the reference's Householder QR with the diag(R) >= 0 convention,
+    linalg.py:43-59).  `gram_reduce` sums Grams across column-sharded ranks
+    (row-sharded a).
+
+    Numerically rank-deficient input (the certificate's factor QRs of a
+    rank-deficient product, a subspace block P W with rank(P) < w) takes an
+    eigenbasis route on the same device Grams: Q = A W_r diag(l_r)^-1/2 over
+    the r eigenpairs above the noise floor, re-orthonormalised by one
+    CholeskyQR pass, R = Q^T A (r x w, not triangular).  Q then has r <= w
+    columns; every caller only needs A = Q R with orthonormal Q (the factor
+    SVD uses R_U R_V^T, the subspace iteration only span(Q)).
     """
     red = gram_reduce or (lambda x: x)
     g1 = red(dp.gram(a, a))
@@ -141,13 +149,19 @@ def device_thin_qr(dp, a, gram_reduce=None):
         if r2 is not None:
             q = dp.matmul_small(q1, np.linalg.inv(r2))
             return q, r2 @ r1
-    if gram_reduce is not None:
-        raise NumericalError("rank-deficient sharded block: CholeskyQR2 failed")
-    import torch
-
-    q, r = torch.linalg.qr(a, mode="reduced")
-    sgn = torch.where(torch.diagonal(r) < 0.0, -1.0, 1.0).to(a.dtype)
-    return (q * sgn).contiguous(), (r * sgn[:, None]).cpu().numpy()
+    lam, wv = np.linalg.eigh(0.5 * (g1 + g1.T))
+    lam, wv = lam[::-1], wv[:, ::-1]
+    top = float(lam[0]) if lam.size else 0.0
+    keep = lam > max(top, 0.0) * 1e-13 if top > 0.0 else np.zeros(lam.shape, bool)
+    w = a.shape[1]
+    if not keep.any():
+        return a[:, :0].contiguous(), np.zeros((0, w))
+    q1 = dp.matmul_small(a, wv[:, keep] / np.sqrt(lam[keep]))
+    r2 = _chol_upper(red(dp.gram(q1, q1)))
+    if r2 is None:
+        raise NumericalError("device_thin_qr: re-orthonormalisation of the eigenbasis failed")
+    q = dp.matmul_small(q1, np.linalg.inv(r2))
+    return q, red(dp.gram(q, a))
 
 
 def rand_svd_device(dp, k, oversample=10, power_iters=1, seed=0, omega=None):

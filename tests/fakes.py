@@ -101,3 +101,37 @@ class NumpyShardProblem:
             acc = acc + c * v
         out.copy_(acc)
         return out
+
+
+class NumpyCertProblem(NumpyShardProblem):
+    """The DeviceProblem surface the certificate uses (gram, matmul_small,
+    apply, f_zero) for one column shard, from the oracle's arithmetic on CPU
+    torch tensors: certificate_core / certificate_sharded run unchanged."""
+
+    def __init__(self, x_local, lam_l, lam_s, mask_local=None):
+        super().__init__(x_local, lam_l, lam_s)
+        self.mask = mask_local
+        self.lambda_l = lam_l
+        xo = x_local if mask_local is None else np.where(mask_local, x_local, 0.0)
+        self.f_zero = 0.5 * float(np.sum(xo * xo))
+        self.store = frozenset({"f64"})
+        self.apply_calls = 0
+
+    def gram(self, a, b):
+        return a.double().numpy().T @ b.double().numpy()
+
+    def matmul_small(self, a, mat):
+        import torch
+
+        return torch.from_numpy(a.double().numpy() @ np.asarray(mat, np.float64))
+
+    def apply(self, k, z, w_right=None, w_left=None, precision="fp64"):
+        import torch
+
+        zz = z.numpy()
+        u, v = self._split(zz, k)
+        _, g, _ = orc.phi_value_grad(u @ v.T, self.x, self.lam_s, self.mask)
+        self.apply_calls += 1
+        left = torch.from_numpy(g @ w_right.numpy()) if w_right is not None else None
+        right = torch.from_numpy(g.T @ w_left.numpy()) if w_left is not None else None
+        return left, right

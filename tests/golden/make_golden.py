@@ -271,11 +271,103 @@ def gen_io(spcp):
     np.savez_compressed(os.path.join(OUT, "io.npz"), **out)
 
 
+# Headline configurations (BASELINE.json configs[1..3]): the real
+# reference solves them once here (minutes to ~1 h of CPU each) and the
+# fixtures pin solve-level parity at the shapes the bench numbers are quoted
+# on: objective, termination, records, the final factors (L = U V^T is
+# compared in k-space, S* = shrink(X - L) is re-materialised from them on the
+# device), S statistics, and the certificate terms / verdict.  The top
+# singular values of the projected operator P (the reference's dense SVD in
+# _complement_term) are captured too, to pin the streaming t4 route.
+CONFIGS = {  # tag: (m, n, rank, gen_seed, mask (frac, seed) | None, lam_l, ks)
+    "c2": (20000, 20000, 20, 0, None, 40.0, (20,)),
+    "c3": (110592, 2000, 3, 0, None, 30.0, (3, 5)),
+    "c4s": (16000, 3200, 30, 0, (0.3, 1), 20.0, (30,)),
+}
+
+
+def _gen_config(spcp, tag):
+    import time
+
+    rcert = sys.modules["spcp.certificate"]
+
+    m, n, rank, gs, mk, lam_l, ks = CONFIGS[tag]
+    t0 = time.perf_counter()
+    x, _, _ = spcp.gen_low_rank_plus_sparse(m, n, rank, 0.05, 1e-3, seed=gs)
+    x = x.astype(np.float32).astype(np.float64)  # the device receives exactly X32
+    mask = spcp.gen_mask(m, n, mk[0], seed=mk[1]) if mk else None
+    spec = spcp.ProblemSpec(x=x, lambda_l=lam_l, lambda_s=0.1, mask=mask)
+    out = {"meta": np.array([m, n, rank, gs, lam_l, 0.1] + ([mk[0], mk[1]] if mk else [0, 0]),
+                            np.float64),
+           "x_sum": float(x.sum()), "x_sq": float((x * x).sum()),
+           "gen_s": time.perf_counter() - t0}
+    print(tag, "generated", out["gen_s"], flush=True)
+    cap = {}
+    orig = rcert.svd_small
+
+    def spy(a):
+        t = orig(a)
+        if a.shape == (m, n):
+            cap["sig"] = np.asarray(t.sigma[:64]).copy()
+        return t
+
+    rcert.svd_small = spy
+    try:
+        for k in ks:
+            fp0 = spcp.init_factors(spec, k, strategy="rsvd", seed=0)
+            f0, gu0, gv0 = spcp.split_objective(fp0, spec)
+            out.update({f"k{k}_init_f": f0, f"k{k}_init_u": fp0.u.astype(np.float32),
+                        f"k{k}_init_v": fp0.v.astype(np.float32),
+                        f"k{k}_init_gu_norm": float(np.linalg.norm(gu0)),
+                        f"k{k}_init_gv_norm": float(np.linalg.norm(gv0)),
+                        f"k{k}_init_gu_rows": gu0[:256].copy(),
+                        f"k{k}_init_gv_rows": gv0[:256].copy()})
+            t1 = time.perf_counter()
+            rep = spcp.solve_split_spcp(spec, k, spcp.SolverConfig())
+            t2 = time.perf_counter()
+            cert = rcert.certificate(rep.factors, spec, f_bound_hint=rep.best_objective)
+            t3 = time.perf_counter()
+            it, ob, gn = _records(rep.iterations)
+            s = rep.s
+            out.update({f"k{k}_u": rep.factors.u, f"k{k}_v": rep.factors.v,
+                        f"k{k}_obj": rep.objective, f"k{k}_term": rep.termination,
+                        f"k{k}_recobj": ob, f"k{k}_recgn": gn,
+                        f"k{k}_evals": rep.extra["n_evals"],
+                        f"k{k}_s_nnz": int(np.count_nonzero(s)),
+                        f"k{k}_s_fro": float(np.linalg.norm(s)),
+                        f"k{k}_l_fro": float(np.linalg.norm(rep.l)),
+                        f"k{k}_cert": np.array([cert.e_norm, *cert.terms, cert.f_bound,
+                                                cert.gap_bound, cert.r, cert.l_norm]),
+                        f"k{k}_sigma_p": cap.pop("sig", np.zeros(0)),
+                        f"k{k}_solve_s": t2 - t1, f"k{k}_cert_s": t3 - t2})
+            print(tag, k, rep.termination, len(it) - 1, rep.extra["n_evals"], rep.objective,
+                  "solve", t2 - t1, "cert", t3 - t2, "e_norm", cert.e_norm, flush=True)
+            del rep, s
+    finally:
+        rcert.svd_small = orig
+    out["ncpu"] = os.cpu_count()
+    np.savez_compressed(os.path.join(OUT, f"{tag}.npz"), **out)
+
+
+def gen_c2(spcp):
+    _gen_config(spcp, "c2")
+
+
+def gen_c3(spcp):
+    _gen_config(spcp, "c3")
+
+
+def gen_c4s(spcp):
+    _gen_config(spcp, "c4s")
+
+
 if __name__ == "__main__":
     ref = _ref()
     only = sys.argv[1:]
-    for fn in (gen_phi, gen_split, gen_lbfgs, gen_solve, gen_cert, gen_synth, gen_c1, gen_io):
-        if only and fn.__name__ not in only:
+    for fn in (gen_phi, gen_split, gen_lbfgs, gen_solve, gen_cert, gen_synth, gen_c1, gen_io,
+               gen_c3, gen_c4s, gen_c2):
+        heavy = fn in (gen_c3, gen_c4s, gen_c2)  # minutes to ~1 h each: only when named
+        if (only and fn.__name__ not in only) or (heavy and not only):
             continue
         fn(ref)
         print("wrote", fn.__name__)

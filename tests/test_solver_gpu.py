@@ -106,25 +106,51 @@ def test_certificate_golden(api, golden):
     assert cert.e_norm == pytest.approx(float(d["zero_cert"][0]), rel=1e-12)
 
 
-def test_certificate_subspace_matches_dense(api):
-    """The streaming subspace-iteration t4 (large-problem route) equals the
-    dense-SVD t4 on an under-ranked C1 iterate (several sigma(P) > 1)."""
+def test_certificate_t4_routes(api, golden):
+    """t4 is never a dense SVD (certificate.py:70-74 restated as streaming block
+    subspace iteration on P): the under-ranked C1 iterate has several
+    sigma(P) > 1 and converged Ritz values matching the reference's dense t4;
+    the converged full-rank iterate gets t4 = 0 from sigma_max(P) < 1."""
     from oracle import spcp_oracle as orc
 
+    d = golden("c1")
     x, _, _ = orc.gen_low_rank_plus_sparse(1000, 1000, 10, 0.05, 1e-3, seed=0)
     x = x.astype(np.float32).astype(np.float64)
     spec = api.ProblemSpec(x=x, lambda_l=10.0, lambda_s=0.1)
-    rep = api.solve_split_spcp(spec, 5, api.SolverConfig(max_iter=60))
-    dense = api.certificate(rep.factors, spec)
-    sub = api.certificate(rep.factors, spec, dense_limit=0)
-    assert sub.info["t4_method"] == "subspace"
-    assert dense.info["n_sigma_over_1"] >= 1
-    assert sub.terms[3] == pytest.approx(dense.terms[3], rel=1e-6)
-    assert sub.e_norm == pytest.approx(dense.e_norm, rel=1e-6)
-    # converged full-rank iterate: t4 = 0 on both routes
-    rep = api.solve_split_spcp(spec, 10, api.SolverConfig())
-    sub = api.certificate(rep.factors, spec, dense_limit=0)
+    fp5 = api.FactorPair(d["k5_u"], d["k5_v"])
+    sub = api.certificate(fp5, spec)
+    assert sub.info["t4_method"] == "subspace" and sub.info["converged"]
+    assert sub.info["n_sigma_over_1"] >= 1 and sub.info["products"] == "fp64"
+    assert sub.terms[3] == pytest.approx(float(d["k5_cert"][4]), rel=1e-7)
+    fp10 = api.FactorPair(d["k10_u"], d["k10_v"])
+    sub = api.certificate(fp10, spec)
     assert sub.terms[3] == 0.0 and sub.info["sigma_p_max"] < 1.0
+
+
+def test_certificate_fp32_products_route(api):
+    """Above FP32_PRODUCTS_MIN_ELEMS the subspace iteration streams the fp32
+    copy of X; its verdict and t4 agree with the fp64 products."""
+    from oracle import spcp_oracle as orc
+    from paper_1702_02241_b200 import certificate as cm
+
+    m, n = 2600, 1700
+    x, _, _ = orc.gen_low_rank_plus_sparse(m, n, 8, 0.05, 1e-3, seed=4)
+    x = x.astype(np.float32).astype(np.float64)
+    spec = api.ProblemSpec(x=x, lambda_l=0.3 * np.sqrt(n), lambda_s=0.1)
+    for k in (4, 8):
+        rep = api.solve_split_spcp(spec, k, api.SolverConfig(max_iter=80))
+        c32 = api.certificate(rep.factors, spec, f_bound_hint=rep.best_objective)
+        assert c32.info["products"] == "fp32"
+        old = cm.FP32_PRODUCTS_MIN_ELEMS
+        cm.FP32_PRODUCTS_MIN_ELEMS = 1 << 40
+        try:
+            c64 = api.certificate(rep.factors, spec, f_bound_hint=rep.best_objective)
+        finally:
+            cm.FP32_PRODUCTS_MIN_ELEMS = old
+        assert c64.info["products"] == "fp64"
+        assert c32.info["n_sigma_over_1"] == c64.info["n_sigma_over_1"]
+        assert c32.terms[3] == pytest.approx(c64.terms[3], rel=1e-5, abs=1e-9)
+        assert warns(c32, rep.objective) == warns(c64, rep.objective)
 
 
 def test_mixed_precision_solve_matches_oracle(api):
