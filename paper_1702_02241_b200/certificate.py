@@ -143,7 +143,9 @@ class _ProjectedOperator:
         return self.proj_v(w.mul_(-1.0 / self.lam))
 
 
-_SUBSPACE_TOL = 1e-9
+# Ritz-value convergence tolerance by product precision: fp64 streaming
+# products resolve sigma(P) to ~1e-15, the fp32 ones to ~1e-7
+_SUBSPACE_TOL = {"fp64": 1e-9, "fp32": 1e-6}
 _FAIL_PROB = 1e-6
 # (1 - eps, certified factor): after the bound's iteration count, with
 # probability >= 1 - fail, theta^2 >= (1 - eps) sigma_max^2, i.e.
@@ -178,7 +180,7 @@ def _subspace_sigmas(op, n_total, m, r, block=16, max_iter=400, tol=None, seed=0
     import torch
 
     dp, ops = op.dp, op.ops
-    tol = _SUBSPACE_TOL if tol is None else tol
+    tol = _SUBSPACE_TOL[op.precision] if tol is None else tol
     cap = max(1, min(m, n_total) - r)
     b = min(block, cap)
     n_loc = dp.n

@@ -21,6 +21,7 @@
 
 #include "aux_kernels.cuh"
 #include "common.cuh"
+#include "stream_f64.cuh"
 #include "stream_simt.cuh"
 #include "stream_tc.cuh"
 
@@ -221,39 +222,87 @@ static int launch_stream(spcp_problem* p, StreamParams sp, LaunchShape& shape, b
   return SPCP_OK;
 }
 
+// fp64 register-blocked streaming pass (stream_f64.cuh)
+template <int KP, int PW, int MODE, bool MASK, typename TX>
+static int launch_f64(spcp_problem* p, StreamParams sp, LaunchShape& shape) {
+  using G = F64Geom<KP, PW, MODE, TX>;
+  auto kern = f64_stream_kernel<KP, PW, MODE, MASK, TX>;
+  constexpr size_t smem = G::SMEM;
+  static DevFlags occ_dev = {};
+  int occ = occ_dev[dev_slot(p->device)].load(std::memory_order_relaxed);
+  if (occ == 0) {
+    SPCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int o = 0;
+    SPCP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, G::NT, smem));
+    occ = std::max(o, 1);
+    occ_dev[dev_slot(p->device)].store(occ, std::memory_order_relaxed);
+  }
+  const int64_t nrb = p->m_pad / G::BM;
+  const int64_t ntiles = p->n_pad / G::BN;
+  // ~2 waves of resident CTAs, each chunk >= 4 tiles when possible (the left
+  // product is flushed once per chunk)
+  const int64_t target = int64_t(kSMs) * occ * 2;
+  int64_t nch = ceil_div(target, nrb);
+  nch = std::max<int64_t>(1, std::min<int64_t>(nch, std::max<int64_t>(1, ntiles / 4)));
+  const int64_t tiles_per = ceil_div(ntiles, nch);
+  nch = ceil_div(ntiles, tiles_per);
+  sp.chunk_cols = tiles_per * G::BN;
+  sp.nchunks = int(nch);
+  shape.nchunks = int(nch);
+  shape.nrb = int(nrb);
+  shape.chunk_cols = sp.chunk_cols;
+  int rc;
+  if ((rc = p->pleft.ensure(size_t(nch) * p->m_pad * PW * sizeof(double)))) return rc;
+  if ((rc = p->pright.ensure(size_t(nrb) * p->n_pad * PW * sizeof(double)))) return rc;
+  if ((rc = p->pphi.ensure(size_t(nrb * nch) * sizeof(double)))) return rc;
+  sp.pleft = p->pleft.ptr;
+  sp.pright = p->pright.ptr;
+  sp.pphi = p->pphi.as<double>();
+  dim3 grid{unsigned(nch), unsigned(nrb), 1u};
+  if (p->prof && prof_begin(p)) return SPCP_ERR_CUDA;
+  kern<<<grid, G::NT, smem, p->stream>>>(sp);
+  SPCP_CHECK_LAUNCH("f64_stream_kernel");
+  if (p->prof && prof_end(p)) return SPCP_ERR_CUDA;
+  p->launches++;
+  return SPCP_OK;
+}
+
 // fused EVAL kernel widths
 #define SPCP_EVAL_F32_LIST(X) X(4) X(8) X(12) X(16) X(20) X(24) X(28) X(32) X(40) X(48) X(56) X(64)
-#define SPCP_EVAL_F64_LIST(X) X(4) X(8) X(12) X(16) X(20) X(24) X(28) X(32)
+#define SPCP_EVAL_F64_LIST(X) X(8) X(16) X(24) X(32) X(40) X(48) X(56) X(64)
 
 static int eval_kp(int dtype, int64_t k) {
   if (dtype == SPCP_F32) {
     static const int l[] = {4, 8, 12, 16, 20, 24, 28, 32, 40, 48, 56, 64};
     for (int v : l)
       if (k <= v) return v;
-  } else {
-    static const int l[] = {4, 8, 12, 16, 20, 24, 28, 32};
-    for (int v : l)
-      if (k <= v) return v;
+  } else if (k <= 64) {
+    return int(round_up(k, 8));  // fp64: f64_stream_kernel, rank padded to 8
   }
-  return 0;  // beyond the fused kernel: dense fallback
+  return 0;  // beyond the fused kernels: dense fallback
 }
 
 template <typename T, typename TX, bool MASK>
 static int dispatch_eval(spcp_problem* p, int kp, StreamParams sp, LaunchShape& sh) {
   bool prof = p->prof;
+  (void)prof;
+  if constexpr (sizeof(T) == 4) {
 #define SPCP_CASE(K) \
   case K:            \
     return launch_stream<T, TX, K, K, MODE_EVAL, MASK>(p, sp, sh, prof);
-  if constexpr (sizeof(T) == 4) {
     switch (kp) { SPCP_EVAL_F32_LIST(SPCP_CASE) }
-  } else {
-    switch (kp) { SPCP_EVAL_F64_LIST(SPCP_CASE) }
-  }
 #undef SPCP_CASE
+  } else {
+#define SPCP_CASE(K) \
+  case K:            \
+    return launch_f64<K, K, MODE_EVAL, MASK, TX>(p, sp, sh);
+    switch (kp) { SPCP_EVAL_F64_LIST(SPCP_CASE) }
+#undef SPCP_CASE
+  }
   return fail(SPCP_ERR_UNSUPPORTED, "no fused kernel for this rank bound");
 }
 
-// APPLY / RAW (float64 only)
+// APPLY / RAW widths: fp32 SIMT stream_kernel (k <= 32), fp64 f64_stream_kernel (k <= 64)
 static int apply_kr(int64_t k) {
   if (k == 0) return 0;
   if (k <= 8) return 8;
@@ -261,22 +310,45 @@ static int apply_kr(int64_t k) {
   if (k <= 32) return 32;
   return -1;
 }
+static int apply_kr64(int64_t k) {
+  if (k == 0) return 0;
+  if (k <= 64) return int(round_up(k, 16));
+  return -1;
+}
 
 template <typename T, typename TX, bool MASK>
 static int dispatch_apply(spcp_problem* p, int kr, int pw, StreamParams sp, LaunchShape& sh) {
+  if constexpr (sizeof(T) == 4) {
 #define SPCP_AP(KR, PW)                                                            \
   if (kr == KR && pw == PW)                                                      \
     return KR == 0 ? launch_stream<T, TX, 0, PW, MODE_RAW, MASK>(p, sp, sh, false) \
                    : launch_stream<T, TX, KR, PW, MODE_APPLY, MASK>(p, sp, sh, false);
-  SPCP_AP(0, 8)
-  SPCP_AP(0, 32)
-  SPCP_AP(8, 8)
-  SPCP_AP(8, 32)
-  SPCP_AP(16, 8)
-  SPCP_AP(16, 32)
-  SPCP_AP(32, 8)
-  SPCP_AP(32, 32)
+    SPCP_AP(0, 8)
+    SPCP_AP(0, 32)
+    SPCP_AP(8, 8)
+    SPCP_AP(8, 32)
+    SPCP_AP(16, 8)
+    SPCP_AP(16, 32)
+    SPCP_AP(32, 8)
+    SPCP_AP(32, 32)
 #undef SPCP_AP
+  } else {
+#define SPCP_AP(KR, PW)                                                 \
+  if (kr == KR && pw == PW)                                           \
+    return KR == 0 ? launch_f64<0, PW, MODE_RAW, MASK, TX>(p, sp, sh) \
+                   : launch_f64<KR, PW, MODE_APPLY, MASK, TX>(p, sp, sh);
+    SPCP_AP(0, 8)
+    SPCP_AP(0, 32)
+    SPCP_AP(16, 8)
+    SPCP_AP(16, 32)
+    SPCP_AP(32, 8)
+    SPCP_AP(32, 32)
+    SPCP_AP(48, 8)
+    SPCP_AP(48, 32)
+    SPCP_AP(64, 8)
+    SPCP_AP(64, 32)
+#undef SPCP_AP
+  }
   return fail(SPCP_ERR_UNSUPPORTED, "no apply kernel for this width");
 }
 
@@ -792,7 +864,7 @@ static int dense_fallback_eval(spcp_problem* p, int64_t k, const double* z, cons
     sp.do_left = 1;
     sp.do_right = 1;
     LaunchShape s2;
-    if ((rc = launch_stream<double, double, 0, 32, MODE_RAW, false>(p, sp, s2, false))) return rc;
+    if ((rc = launch_f64<0, 32, MODE_RAW, false, double>(p, sp, s2))) return rc;
     // fold partials of this column block into pl / pr column slots c0..c0+bw
     // (pl: one chunk; pr: per row band) — reduce chunks now into pl
     double* srcl = p->pleft.as<double>();
@@ -956,7 +1028,7 @@ static int apply_impl(spcp_problem* p, int64_t k, const double* z, int64_t b,
   if (k < 0 || b < 1) return fail(SPCP_ERR_DIMENSION, "bad apply shape");
   SPCP_CUDA(cudaSetDevice(p->device));
   const bool x64 = p->x64.ptr != nullptr;
-  int kr = apply_kr(k);
+  int kr = std::is_same<T, float>::value ? apply_kr(k) : apply_kr64(k);
   // residual operands (T)
   if (kr > 0) {
     if ((rc = prep<T>(p, k, kr, z, nullptr, 0.0))) return rc;
@@ -1004,8 +1076,8 @@ static int apply_impl(spcp_problem* p, int64_t k, const double* z, int64_t b,
     if (kr < 0) {
       sp.x = p->gu_tmp.ptr;
       sp.mbits = nullptr;
-      rc = pw == 8 ? launch_stream<double, double, 0, 8, MODE_RAW, false>(p, sp, sh, false)
-                   : launch_stream<double, double, 0, 32, MODE_RAW, false>(p, sp, sh, false);
+      rc = pw == 8 ? launch_f64<0, 8, MODE_RAW, false, double>(p, sp, sh)
+                   : launch_f64<0, 32, MODE_RAW, false, double>(p, sp, sh);
     } else {
       sp.x = x64 ? p->x64.ptr : p->x32.ptr;
       sp.mbits = p->masked ? p->mbits.as<uint32_t>() : nullptr;
@@ -1370,7 +1442,7 @@ int spcp_apply_f32(spcp_problem* p, int64_t k, const double* z, int64_t b,
                    double* right_out) {
   if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
   // fp32 streaming products need the fp32 copy of X and the fused widths
-  if (!p->x32.ptr || apply_kr(k) < 0)
+  if (!p->x32.ptr || apply_kr(k) < 0)  // fp64 kernels cover k <= 64
     return apply_impl<double>(p, k, z, b, w_right, left_out, w_left, right_out);
   return apply_impl<float>(p, k, z, b, w_right, left_out, w_left, right_out);
 }

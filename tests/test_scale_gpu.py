@@ -23,6 +23,8 @@ CONFIGS = {
     "C2": (20000, 20000, 20, 20, 40.0, None),
     "C3": (110592, 2000, 5, 3, 30.0, None),
     "C4": (50000, 10000, 30, 30, 20.0, 0.3),
+    # configs[4] per-GPU shard at 8 GPUs: 200000 x 2500, rank 50, k = 50
+    "C5shard": (200000, 2500, 50, 50, 100.0, None),
 }
 
 
@@ -68,5 +70,27 @@ def test_full_size_column_blocks(name):
         mb = mask[:, c0:c1] if mask is not None else None
         _, _, gvr = orc.split_objective(u, v[c0:c1], xb, ll, ls, mb)
         assert rel(gv32[c0:c1], gvr) <= FP32_TOL, (name, c0, c1, rel(gv32[c0:c1], gvr))
+        gv64 = g64[m * k:].view(n, k).cpu().numpy()
+        assert rel(gv64[c0:c1], gvr) <= 1e-10, (name, c0, c1, rel(gv64[c0:c1], gvr))
+    # row blocks: grad_U[R] = G[R, :] V + lambda U[R] needs X[R, :] (all columns)
+    gu32 = g32[: m * k].view(m, k).cpu().numpy()
+    gu64 = g64[: m * k].view(m, k).cpu().numpy()
+    for r0, r1 in [(0, 128), (m // 2 - 64, m // 2 + 61), (m - 37, m)]:
+        xb = x[r0:r1].double().cpu().numpy()
+        mb = mask[r0:r1] if mask is not None else None
+        _, gur, _ = orc.split_objective(u[r0:r1], v, xb, ll, ls, mb)
+        assert rel(gu32[r0:r1], gur) <= FP32_TOL, (name, r0, r1, rel(gu32[r0:r1], gur))
+        assert rel(gu64[r0:r1], gur) <= 1e-10, (name, r0, r1, rel(gu64[r0:r1], gur))
+    # f over the whole matrix, summed over column blocks by the oracle
+    # (separable: f = sum_b phi_b + lambda/2 (|U|^2 + |V|^2))
+    phi = 0.0
+    for c0 in range(0, n, 2000):
+        c1 = min(n, c0 + 2000)
+        xb = x[:, c0:c1].double().cpu().numpy()
+        mb = mask[:, c0:c1] if mask is not None else None
+        phi += orc.phi_value_grad(u @ v[c0:c1].T, xb, ls, mb)[0]
+    f_ref = phi + 0.5 * ll * (float(np.sum(u * u)) + float(np.sum(v * v)))
+    assert abs(out32[0] - f_ref) <= FP32_TOL * abs(f_ref), (name, out32[0], f_ref)
+    assert abs(out64[0] - f_ref) <= 1e-10 * abs(f_ref), (name, out64[0], f_ref)
     del dp, x
     torch.cuda.empty_cache()

@@ -130,8 +130,10 @@ def test_certificate_t4_routes(api, golden):
 def test_certificate_fp32_products_route(api):
     """Above FP32_PRODUCTS_MIN_ELEMS the subspace iteration streams the fp32
     copy of X; its verdict and t4 agree with the fp64 products."""
+    import importlib
+
     from oracle import spcp_oracle as orc
-    from paper_1702_02241_b200 import certificate as cm
+    cm = importlib.import_module("paper_1702_02241_b200.certificate")
 
     m, n = 2600, 1700
     x, _, _ = orc.gen_low_rank_plus_sparse(m, n, 8, 0.05, 1e-3, seed=4)
