@@ -313,6 +313,8 @@ def _time_evals(dp, step, steps, warmup, dist, stream):
     ms, launches, burst dict, clocks)."""
     import torch
 
+    clocks = ClockSampler()
+    clocks.start()  # NVML up before the timed region; samples kept only inside it
     # burst: 20 steps on a cold clock (after 3 that absorb first-call setup)
     for i in range(3):
         step(i)
@@ -343,9 +345,6 @@ def _time_evals(dp, step, steps, warmup, dist, stream):
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks = ClockSampler()
-    clocks.start()
-    time.sleep(0.02)
     dp.prof_enable(True)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)

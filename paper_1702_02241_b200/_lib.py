@@ -21,7 +21,9 @@ from .errors import (
 __all__ = ["lib", "check", "LIB_PATH", "SPCP_F32", "SPCP_F64", "SPCP_U8", "STORE_F32",
            "STORE_F64", "EXPORTS"]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libspcp_b200.so")
+# SPCP_LIB_PATH: an alternative build of the same ABI (A/B timing tools only)
+LIB_PATH = os.environ.get("SPCP_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "libspcp_b200.so")
 
 SPCP_OK, SPCP_ERR_VALUE, SPCP_ERR_DIMENSION, SPCP_ERR_NUMERICAL, SPCP_ERR_CUDA, \
     SPCP_ERR_UNSUPPORTED, SPCP_ERR_IO, SPCP_ERR_MALFORMED_HEADER, SPCP_ERR_TRUNCATED, \

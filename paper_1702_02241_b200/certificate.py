@@ -210,6 +210,11 @@ def _subspace_sigmas(op, n_total, m, r, block=16, max_iter=400, tol=None, seed=0
             ev = np.linalg.eigvalsh(ops.gram_rows(dp, wz, wz))
             sig = np.sqrt(np.clip(ev[::-1], 0.0, None))
             iters_total += 1
+            if sig.size == b and sig[-1] >= 1.0 and b < cap:
+                # Ritz values are lower bounds of the top b singular values:
+                # sigma_b(P) >= 1 already, so this block cannot hold every
+                # sigma > 1 -- grow it now rather than converge a clustered tail
+                break
             t4 = float(np.sum(np.maximum(sig - 1.0, 0.0) ** 2))
             if prev is not None and abs(sig[0] - prev[0]) <= tol * max(1.0, sig[0]) and \
                     abs(t4 - prev[1]) <= tol * max(1.0, t4):
@@ -229,6 +234,9 @@ def _subspace_sigmas(op, n_total, m, r, block=16, max_iter=400, tol=None, seed=0
             q, _ = device_thin_qr(dp, wz, ops.host if ops.sharded else None)
         info = {"t4_method": "subspace", "block": b, "iters": iters_total,
                 "sigma_p_max": float(sig[0]) if sig.size else 0.0, "converged": converged}
+        if sig.size == b and sig[-1] >= 1.0 and b < cap:
+            b = min(2 * b, cap)
+            continue
         if not converged:
             warnings.warn(f"certificate: subspace iteration for sigma(P) did not converge in "
                           f"{max_iter} passes; t4 is a lower bound", RuntimeWarning)

@@ -269,15 +269,20 @@ static int launch_f64(spcp_problem* p, StreamParams sp, LaunchShape& shape) {
 
 // fused EVAL kernel widths
 #define SPCP_EVAL_F32_LIST(X) X(4) X(8) X(12) X(16) X(20) X(24) X(28) X(32) X(40) X(48) X(56) X(64)
-#define SPCP_EVAL_F64_LIST(X) X(8) X(16) X(24) X(32) X(40) X(48) X(56) X(64)
+// fp64: the per-row SIMT stream_kernel up to k = 32 (measured faster there:
+// 4.15 vs 5.7 ms at C2), the register-blocked f64_stream_kernel above
+#define SPCP_EVAL_F64_LIST(X) X(4) X(8) X(12) X(16) X(20) X(24) X(28) X(32)
+#define SPCP_EVAL_F64W_LIST(X) X(40) X(48) X(56) X(64)
 
 static int eval_kp(int dtype, int64_t k) {
   if (dtype == SPCP_F32) {
     static const int l[] = {4, 8, 12, 16, 20, 24, 28, 32, 40, 48, 56, 64};
     for (int v : l)
       if (k <= v) return v;
+  } else if (k <= 32) {
+    return int(round_up(k, 4));  // fp64 stream_kernel
   } else if (k <= 64) {
-    return int(round_up(k, 8));  // fp64: f64_stream_kernel, rank padded to 8
+    return int(round_up(k, 8));  // fp64 f64_stream_kernel
   }
   return 0;  // beyond the fused kernels: dense fallback
 }
@@ -295,8 +300,13 @@ static int dispatch_eval(spcp_problem* p, int kp, StreamParams sp, LaunchShape& 
   } else {
 #define SPCP_CASE(K) \
   case K:            \
-    return launch_f64<K, K, MODE_EVAL, MASK, TX>(p, sp, sh);
+    return launch_stream<T, TX, K, K, MODE_EVAL, MASK>(p, sp, sh, prof);
     switch (kp) { SPCP_EVAL_F64_LIST(SPCP_CASE) }
+#undef SPCP_CASE
+#define SPCP_CASE(K) \
+  case K:            \
+    return launch_f64<K, K, MODE_EVAL, MASK, TX>(p, sp, sh);
+    switch (kp) { SPCP_EVAL_F64W_LIST(SPCP_CASE) }
 #undef SPCP_CASE
   }
   return fail(SPCP_ERR_UNSUPPORTED, "no fused kernel for this rank bound");
@@ -311,7 +321,7 @@ static int apply_kr(int64_t k) {
   return -1;
 }
 static int apply_kr64(int64_t k) {
-  if (k == 0) return 0;
+  if (k <= 32) return apply_kr(k);
   if (k <= 64) return int(round_up(k, 16));
   return -1;
 }
@@ -333,16 +343,22 @@ static int dispatch_apply(spcp_problem* p, int kr, int pw, StreamParams sp, Laun
     SPCP_AP(32, 32)
 #undef SPCP_AP
   } else {
-#define SPCP_AP(KR, PW)                                                 \
-  if (kr == KR && pw == PW)                                           \
-    return KR == 0 ? launch_f64<0, PW, MODE_RAW, MASK, TX>(p, sp, sh) \
-                   : launch_f64<KR, PW, MODE_APPLY, MASK, TX>(p, sp, sh);
+#define SPCP_AP(KR, PW)                                                            \
+  if (kr == KR && pw == PW)                                                      \
+    return KR == 0 ? launch_stream<T, TX, 0, PW, MODE_RAW, MASK>(p, sp, sh, false) \
+                   : launch_stream<T, TX, KR, PW, MODE_APPLY, MASK>(p, sp, sh, false);
     SPCP_AP(0, 8)
     SPCP_AP(0, 32)
+    SPCP_AP(8, 8)
+    SPCP_AP(8, 32)
     SPCP_AP(16, 8)
     SPCP_AP(16, 32)
     SPCP_AP(32, 8)
     SPCP_AP(32, 32)
+#undef SPCP_AP
+#define SPCP_AP(KR, PW)            \
+  if (kr == KR && pw == PW)      \
+    return launch_f64<KR, PW, MODE_APPLY, MASK, TX>(p, sp, sh);
     SPCP_AP(48, 8)
     SPCP_AP(48, 32)
     SPCP_AP(64, 8)
@@ -632,10 +648,10 @@ static int tc_images(spcp_problem* p, int64_t k, const double* z, const double* 
 template <int SEG>
 static int tc_images_kc(spcp_problem* p, int64_t k, const double* z, const double* dz,
                         double alpha) {
-  constexpr int RB = TcCfg<16, false, SEG>::RB;
+  using C = TcCfg<16, false, SEG>;
   int rc;
-  if ((rc = p->tc_uimg.ensure(size_t(p->tc_nsb) * 128 * RB))) return rc;
-  if ((rc = p->tc_vimg.ensure(size_t(p->tc_ntc) * 64 * RB))) return rc;
+  if ((rc = p->tc_uimg.ensure(size_t(p->tc_nsb) * C::U_BYTES))) return rc;
+  if ((rc = p->tc_vimg.ensure(size_t(p->tc_ntc) * C::V_BYTES))) return rc;
   const int64_t total = (p->m_pad + p->n_pad) * SEG;
   SPCP_CUDA(launch_pdl(tc_images_kc_kernel<SEG>, dim3(grid_for(total)), dim3(256), 0, p->stream,
                        z, dz, alpha, p->m, p->n, k, p->m_pad, p->n_pad,
@@ -646,21 +662,57 @@ static int tc_images_kc(spcp_problem* p, int64_t k, const double* z, const doubl
   return SPCP_OK;
 }
 
-// K-concatenated layout (k <= 20): SEG = round_up(k, 4)
+// 1: max + scales + images in one launch (tc_prep_kc); 0: tc_max + tc_images_kc
+#ifndef SPCP_TC_PREP_FUSED
+#define SPCP_TC_PREP_FUSED 1
+#endif
+// max + scales + images in one launch (tc_prep_kc_kernel: grid barrier, so
+// the grid is sized to be fully resident)
+template <int SEG>
+static int tc_prep_kc(spcp_problem* p, int64_t k, const double* z, const double* dz,
+                      double alpha) {
+  using C = TcCfg<16, false, SEG>;
+  int rc;
+  if ((rc = ensure_common(p))) return rc;
+  if ((rc = p->tc_uimg.ensure(size_t(p->tc_nsb) * C::U_BYTES))) return rc;
+  if ((rc = p->tc_vimg.ensure(size_t(p->tc_ntc) * C::V_BYTES))) return rc;
+  static DevFlags occ_dev = {};
+  int per_sm = occ_dev[dev_slot(p->device)].load(std::memory_order_relaxed);
+  if (per_sm == 0) {
+    SPCP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tc_prep_kc_kernel<SEG>, 256,
+                                                            0));
+    per_sm = std::max(1, std::min(per_sm, 4));
+    occ_dev[dev_slot(p->device)].store(per_sm, std::memory_order_relaxed);
+  }
+  unsigned* ctr = p->counter.as<unsigned>();
+  SPCP_CUDA(launch_pdl(tc_prep_kc_kernel<SEG>, dim3(kSMs * per_sm), dim3(256), 0, p->stream, z,
+                       dz, alpha, p->m, p->n, k, p->m_pad, p->n_pad, p->tc_scales.as<TcScales>(),
+                       p->lambda_s, p->tc_uimg.as<unsigned char>(),
+                       p->tc_vimg.as<unsigned char>(), ctr + 4, ctr + 5));
+  SPCP_CHECK_LAUNCH("tc_prep_kc");
+  p->launches++;
+  return SPCP_OK;
+}
+
+// K-concatenated layout (k <= 20): SEG = round_up(k, 4).  The two-atom rows of
+// k = 21..32 (SEG 24-32) build and are exact, but their shared-memory budget
+// leaves two X stages and one U buffer: measured at C4 (k = 30, mask) 0.68 ms
+// against 0.59 ms for the split-image layout, so they stay off.
 static bool tc_use_kc(int64_t k) {
   static const bool split = env_str("SPCP_TC_LAYOUT") == "split";
   return k <= 20 && !split;
 }
 
+#define SPCP_KC_SEGS(X) X(4) X(8) X(12) X(16) X(20)
 template <bool MASK>
 static int tc_launch_kc(spcp_problem* p, int64_t k) {
   switch (int(round_up(k, 4))) {
-    case 4: return tc_launch<16, MASK, 4>(p, k);
-    case 8: return tc_launch<16, MASK, 8>(p, k);
-    case 12: return tc_launch<16, MASK, 12>(p, k);
-    case 16: return tc_launch<16, MASK, 16>(p, k);
-    default: return tc_launch<16, MASK, 20>(p, k);
+#define SPCP_KC_CASE(S) \
+    case S: return tc_launch<16, MASK, S>(p, k);
+    SPCP_KC_SEGS(SPCP_KC_CASE)
+#undef SPCP_KC_CASE
   }
+  return fail(SPCP_ERR_UNSUPPORTED, "no K-concatenated kernel for this rank bound");
 }
 
 static int tc_eval(spcp_problem* p, int64_t k, const double* z, const double* dz, double alpha,
@@ -668,6 +720,15 @@ static int tc_eval(spcp_problem* p, int64_t k, const double* z, const double* dz
   int rc;
   if ((rc = tc_build(p))) return rc;
   if (tc_use_kc(k)) {
+#if SPCP_TC_PREP_FUSED
+    switch (int(round_up(k, 4))) {
+#define SPCP_KC_CASE(S) \
+      case S: rc = tc_prep_kc<S>(p, k, z, dz, alpha); break;
+      SPCP_KC_SEGS(SPCP_KC_CASE)
+#undef SPCP_KC_CASE
+      default: rc = fail(SPCP_ERR_UNSUPPORTED, "no K-concatenated image kernel");
+    }
+#else
     TcScales* sc = p->tc_scales.as<TcScales>();
     const int64_t nu = p->m * k, nv = p->n * k;
     SPCP_CUDA(launch_pdl(tc_max_kernel, dim3(grid_for(nu + nv, 256, 148 * 4)), dim3(256), 0,
@@ -675,22 +736,24 @@ static int tc_eval(spcp_problem* p, int64_t k, const double* z, const double* dz
     SPCP_CHECK_LAUNCH("tc_max");
     p->launches += 1;
     switch (int(round_up(k, 4))) {
-      case 4: rc = tc_images_kc<4>(p, k, z, dz, alpha); break;
-      case 8: rc = tc_images_kc<8>(p, k, z, dz, alpha); break;
-      case 12: rc = tc_images_kc<12>(p, k, z, dz, alpha); break;
-      case 16: rc = tc_images_kc<16>(p, k, z, dz, alpha); break;
-      default: rc = tc_images_kc<20>(p, k, z, dz, alpha); break;
+#define SPCP_KC_CASE(S) \
+      case S: rc = tc_images_kc<S>(p, k, z, dz, alpha); break;
+      SPCP_KC_SEGS(SPCP_KC_CASE)
+#undef SPCP_KC_CASE
+      default: rc = fail(SPCP_ERR_UNSUPPORTED, "no K-concatenated image kernel");
     }
+#endif
     if (rc) return rc;
     const int kst = int(round_up(k, 4));
     if ((rc = p->pleft.ensure(size_t(p->tc_runs) * 128 * kst * sizeof(float)))) return rc;
-    if ((rc = p->pright.ensure(size_t(p->tc_slots) * 128 * kst * sizeof(float)))) return rc;
+    constexpr int gt_rows = SPCP_TC_GT_FOLD ? 64 : 128;
+    if ((rc = p->pright.ensure(size_t(p->tc_slots) * gt_rows * kst * sizeof(float)))) return rc;
     if ((rc = p->pphi.ensure(size_t(p->tc_grid) * sizeof(double)))) return rc;
     rc = p->masked ? tc_launch_kc<true>(p, k) : tc_launch_kc<false>(p, k);
     if (rc) return rc;
     sh.tc = 1;
     sh.kst = kst;
-    sh.gt_rows = 128;
+    sh.gt_rows = gt_rows;  // 64: gh + gl parts folded in the drain
     sh.chunked = 1;
     sh.nchunks = 1;
     sh.nrb = 1;
@@ -864,7 +927,7 @@ static int dense_fallback_eval(spcp_problem* p, int64_t k, const double* z, cons
     sp.do_left = 1;
     sp.do_right = 1;
     LaunchShape s2;
-    if ((rc = launch_f64<0, 32, MODE_RAW, false, double>(p, sp, s2))) return rc;
+    if ((rc = launch_stream<double, double, 0, 32, MODE_RAW, false>(p, sp, s2, false))) return rc;
     // fold partials of this column block into pl / pr column slots c0..c0+bw
     // (pl: one chunk; pr: per row band) — reduce chunks now into pl
     double* srcl = p->pleft.as<double>();
@@ -1076,8 +1139,8 @@ static int apply_impl(spcp_problem* p, int64_t k, const double* z, int64_t b,
     if (kr < 0) {
       sp.x = p->gu_tmp.ptr;
       sp.mbits = nullptr;
-      rc = pw == 8 ? launch_f64<0, 8, MODE_RAW, false, double>(p, sp, sh)
-                   : launch_f64<0, 32, MODE_RAW, false, double>(p, sp, sh);
+      rc = pw == 8 ? launch_stream<double, double, 0, 8, MODE_RAW, false>(p, sp, sh, false)
+                   : launch_stream<double, double, 0, 32, MODE_RAW, false>(p, sp, sh, false);
     } else {
       sp.x = x64 ? p->x64.ptr : p->x32.ptr;
       sp.mbits = p->masked ? p->mbits.as<uint32_t>() : nullptr;

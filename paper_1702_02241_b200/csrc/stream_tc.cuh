@@ -49,6 +49,14 @@
 #define SPCP_TC_DEBUG_BITS 0
 #endif
 
+// 1: the G^T U drain folds the gh / gl halves through shared memory (64-row
+// slots, two named barriers per tile); 0: 128-row slots folded by the reduce.
+// Measured same-box at C2: 0.372 vs 0.348 ms (the barriers cost more than the
+// halved slot traffic saves), so 0.
+#ifndef SPCP_TC_GT_FOLD
+#define SPCP_TC_GT_FOLD 0
+#endif
+
 #ifndef SPCP_TC_XPF
 #define SPCP_TC_XPF 0  // X tiles prefetched into L2 ahead of the stage ring (measured: no gain)
 #endif
@@ -92,20 +100,25 @@ struct TcParams {
 
 template <int KP16, bool MASK, int SEG = 0>
 struct TcCfg {
-  // SEG > 0: K-concatenated single images (rank k <= SEG, SEG = round_up(k, 4) <= 20):
-  //   U row = [uh | uh | um] and V row = [vh | vm | vh], segments SEG entries
-  //   apart, so the residual uh.vh + uh.vm + um.vh is ONE K-sum of 3 SEG
-  //   entries (ceil(3 SEG / 16) MMAs), and the reductions read the same images
-  //   as N = RB / 2 wide B operands (useful columns: segment 0 and 2 for G^T U,
-  //   segment 0 and 1 for G.V).  SEG == 0: two split images [uh|um], [vh|vm].
+  // SEG > 0: K-concatenated single images (rank k <= SEG, SEG = round_up(k, 4) <= 32):
+  //   U row = [um | uh | uh] and V row = [vh | vm | vh], segments SEG entries
+  //   apart, so the residual um.vh + uh.vm + uh.vh is ONE K-sum of 3 SEG
+  //   entries (ceil(3 SEG / 16) MMAs), and both reductions read the first two
+  //   segments of the same images as N = 2 SEG wide B operands: [um | uh] for
+  //   G^T U, [vh | vm] for G.V (the drains add the two halves).  Rows longer
+  //   than one 128-byte swizzle atom (3 SEG > 64 entries, k > 20) are stored
+  //   as NA K-atoms, atom a of every row at a * rows * 128 bytes; the
+  //   reductions only read atom 0.  SEG == 0: two split images [uh|um], [vh|vm].
   static constexpr bool KC = SEG > 0;
   static constexpr int KE = 3 * SEG;
-  static constexpr int RB = KC ? (KE <= 16 ? 32 : (KE <= 32 ? 64 : 128)) : KP16 * 2;
+  static constexpr int NA = KC ? (KE * 2 + 127) / 128 : 1;  // K-atoms per image row
+  static constexpr int RB = KC ? (NA > 1 ? 128 : (KE <= 16 ? 32 : (KE <= 32 ? 64 : 128)))
+                               : KP16 * 2;
   static constexpr uint32_t SWK = RB == 128 ? tc::SW_128 : (RB == 64 ? tc::SW_64 : tc::SW_32);
   static constexpr int NSPLIT = KC ? 1 : 2;
-  static constexpr int RT = RB * NSPLIT;  // image bytes per row over all splits
+  static constexpr int RT = RB * NSPLIT * NA;  // image bytes per row over all splits / atoms
   static constexpr int NKS = KC ? (KE + 15) / 16 : 0;  // residual K-steps (KC)
-  static constexpr int NB = RB / 2;                    // reduction N (KC)
+  static_assert(!KC || 2 * SEG <= RB / 2, "the reductions' B operand lies in atom 0");
   // X ring (released by the epilogue as soon as it has read the tile), V ring
   // (released when the tile's G.V MMA has finished), U buffers (per run)
 #ifndef SPCP_TC_GB
@@ -118,9 +131,11 @@ struct TcCfg {
   static constexpr int UB = RT == 256 ? 1 : 2;
   static constexpr int LOOKAHEAD = NSV - 1 < 2 ? NSV - 1 : 2;  // residual issue lead (tiles)
   static constexpr int X_BYTES = 128 * 64 * 4;
-  static constexpr int V_SPLIT = 64 * RB;
+  static constexpr int V_SPLIT = 64 * RB * NA;  // V_ATOM * NA
+  static constexpr int V_ATOM = 64 * RB;
   static constexpr int V_BYTES = NSPLIT * V_SPLIT;
-  static constexpr int U_SPLIT = 128 * RB;
+  static constexpr int U_ATOM = 128 * RB;
+  static constexpr int U_SPLIT = 128 * RB * NA;
   static constexpr int U_BYTES = NSPLIT * U_SPLIT;
   static constexpr int M_BYTES = MASK ? 128 * 4 * 4 : 0;  // box {4 words, 128 rows}
   static constexpr int G_SPLIT = 128 * 64 * 2;            // one fp16 G image (MN-major SW128)
@@ -141,7 +156,7 @@ struct TcCfg {
   static constexpr int GVC = KP16 <= 32 ? 2 : 1;
   // KC: G.V needs output columns [0, 2 SEG) only ([vh|vm] segments)
   static constexpr int GVW = KC ? ((2 * SEG + 15) / 16) * 16 : GVC * KP16;
-  static constexpr int GTW = KC ? NB : GCAT * KP16;
+  static constexpr int GTW = KC ? GVW : GCAT * KP16;
   // KC: the epilogue overwrites its S columns with G (fp16 pairs: gh at +0,
   // gl at +16 of each warp's 32 columns) and G.V reads A from TMEM; three S
   // buffers (the next writer of a buffer is the other group's tile) and three
@@ -151,13 +166,15 @@ struct TcCfg {
 #endif
   static constexpr int NSB = KC ? SPCP_TC_NSB : 2;
   static_assert(NSB <= 4, "TcBarriers holds four S buffers");
-  static constexpr int NGT = KC ? (SPCP_TC_NSB >= 4 ? 2 : 3) : 4;
   static constexpr uint32_t T_S = 0, T_GV = 64 * NSB;
   static constexpr uint32_t T_GT = T_GV + 2 * GVW;
-  // KC: the run's U image also lives in TMEM (tcgen05.cp), so the residual is a
-  // TS MMA that reads only V from shared memory
+  // KC: the run's U image also lives in TMEM (tcgen05.cp, 8 columns per K-step),
+  // so the residual is a TS MMA that reads only V from shared memory
+  static constexpr int U_COLS = KC ? NKS * 8 : 0;
+  // three G^T U accumulators when they fit next to U, else two
+  static constexpr int NGT = KC ? ((SPCP_TC_NSB < 4 && T_GT + 3 * GTW + U_COLS <= 512) ? 3 : 2)
+                                : 4;
   static constexpr uint32_t T_U = T_GT + NGT * GTW;
-  static constexpr int U_COLS = KC ? RB / 4 : 0;
   static_assert(T_U + U_COLS <= 512, "TMEM budget");
   static constexpr uint32_t TMEM_COLS = 512;
   static constexpr int NEPI = 16;  // epilogue warps: 2 groups x 4 quarters x 2 halves
@@ -287,8 +304,9 @@ __device__ __noinline__ void tc_residual_issuer(unsigned char* sm, TcBarriers* b
         tc_fence_after();
         const uint64_t du = dU_k + uint64_t(ubuf * (C::U_BYTES >> 4));
         if (do_mma && !(SPCP_TC_DEBUG_BITS & 64)) {
-          static_for<C::NKS>([&](auto I) {
-            tmem_cp_128x256b_w(tm + C::T_U + 8 * I, du + uint64_t(2 * I));
+          static_for<C::NKS>([&](auto I) {  // K-step I: atom I / 4, 32 B step I % 4
+            tmem_cp_128x256b_w(tm + C::T_U + 8 * I,
+                               du + uint64_t((I / 4) * (C::U_ATOM >> 4) + 2 * (I % 4)));
           });
         }
       }
@@ -306,9 +324,16 @@ __device__ __noinline__ void tc_residual_issuer(unsigned char* sm, TcBarriers* b
       // uh.vh + uh.vm + um.vh: product q uses U split (q == 2), V split (q == 1)
       const uint32_t dt = tm + C::T_S + b * 64;
       if constexpr (C::KC) {
-        // one K-sum over the concatenated segments: [uh|uh|um] . [vh|vm|vh]
-        // (warp-wide batch: one elect, descriptors stepped by 32 B)
-        mma_ts_batch<C::NKS, 2>(dt, tm + C::T_U, db, ID_RES, 0u);
+        // one K-sum over the concatenated segments: [um|uh|uh] . [vh|vm|vh]
+        // (warp-wide batch: one elect, descriptors stepped by 32 B; a second
+        // batch for the K-steps in atom 1)
+        if constexpr (C::NKS <= 4) {
+          mma_ts_batch<C::NKS, 2>(dt, tm + C::T_U, db, ID_RES, 0u);
+        } else {
+          mma_ts_batch<4, 2>(dt, tm + C::T_U, db, ID_RES, 0u);
+          mma_ts_batch<C::NKS - 4, 2>(dt, tm + C::T_U + 32, db + uint64_t(C::V_ATOM >> 4),
+                                      ID_RES, 1u);
+        }
       } else {
         static_for<3 * KS>([&](auto I) {
           constexpr int q = I / KS, ks = I % KS;
@@ -613,10 +638,62 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK, SEG>::NTHREADS, 1)
       tc_fence_after();
       if constexpr (C::KC) {
         if (!(SPCP_TC_DEBUG_BITS & 1)) {
+#if SPCP_TC_GT_FOLD
+          // M = 128 stacked accumulator: lanes 0..63 hold the gh part of tile
+          // columns 0..63, lanes 64..127 the gl part; output column c = D[c]
+          // (um) + D[SEG + c] (uh).  Quarters 2, 3 park their gl part in the
+          // group's G image (free: its last reader, this tile's G^T U, has
+          // completed), quarters 0, 1 add it to the gh part (fixed order) and
+          // write 64-row slots: half the slot bytes, half the L2 reductions
+          // and half the reduce kernel's gather of a 128-row slot.
+          // slot layout [kst / 4][64 rows][4]: a warp's float4 stores cover 512
+          // contiguous bytes (coalesced)
+          constexpr int NC = C::CW / 4;
+          const bool hi_q = q >= 2;
+          const int r64 = 32 * (q & 1) + lane;
+          float* xb = reinterpret_cast<float*>(gimg);  // [SEG / 4][64 rows][4]
+          float* dst = p.pright + size_t(u2.gt_slot) * 64 * kst + r64 * 4;
+          const bool first = (u2.flags & TCU_FIRST_TOUCH) != 0;
+          const uint32_t col = tm + lane_addr + C::T_GT + b * C::GTW;
+          float4 o[NC];
+          static_for<NC>([&](auto I) {
+            constexpr int c = I * 4;
+            const int cc = h * C::CW + c;
+            if (cc < SEG) {  // warp-uniform
+              uint32_t v[4], w[4];
+              tmem_ld4(col + cc, v);
+              tmem_ld4(col + SEG + cc, w);
+              tmem_wait_ld();
+              o[I] = make_float4(__uint_as_float(v[0]) + __uint_as_float(w[0]),
+                                 __uint_as_float(v[1]) + __uint_as_float(w[1]),
+                                 __uint_as_float(v[2]) + __uint_as_float(w[2]),
+                                 __uint_as_float(v[3]) + __uint_as_float(w[3]));
+              if (hi_q) *reinterpret_cast<float4*>(xb + (cc * 64 + r64 * 4)) = o[I];
+            }
+          });
+          named_bar_sync(1 + grp, 32 * C::NEG);  // gl parts parked
+          if (!hi_q) {
+            static_for<NC>([&](auto I) {
+              constexpr int c = I * 4;
+              const int cc = h * C::CW + c;
+              if (cc < SEG) {
+                const float4 l4 = *reinterpret_cast<const float4*>(xb + (cc * 64 + r64 * 4));
+                const float4 s4 = make_float4(o[I].x + l4.x, o[I].y + l4.y, o[I].z + l4.z,
+                                              o[I].w + l4.w);
+                float* d4 = dst + cc * 64;  // chunk cc / 4 of 64 rows x 4
+                if (first)
+                  *reinterpret_cast<float4*>(d4) = s4;
+                else
+                  red_add_v4(d4, __float_as_uint(s4.x), __float_as_uint(s4.y),
+                             __float_as_uint(s4.z), __float_as_uint(s4.w));
+              }
+            });
+          }
+          named_bar_sync(1 + grp, 32 * C::NEG);  // read before G(t) reuses the image
+#else
           // M = 128 stacked accumulator: lane = slot row (0..63 gh part, 64..127 gl
-          // part); output column c = D[c] (uh) + D[2 SEG + c] (um)
-          // slot layout [kst / 4][128 rows][4]: a warp's float4 stores cover 512
-          // contiguous bytes (coalesced), not 32 rows 4 * kst bytes apart
+          // part), kept as separate 128-row slots (summed by the reduce kernel);
+          // output column c = D[c] (um) + D[SEG + c] (uh)
           float* dst = p.pright + size_t(u2.gt_slot) * 128 * kst + (32 * q + lane) * 4;
           const bool first = (u2.flags & TCU_FIRST_TOUCH) != 0;
           const uint32_t col = tm + lane_addr + C::T_GT + b * C::GTW;
@@ -626,23 +703,21 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK, SEG>::NTHREADS, 1)
             if (cc < SEG) {  // warp-uniform
               uint32_t v[4], w[4];
               tmem_ld4(col + cc, v);
-              tmem_ld4(col + 2 * SEG + cc, w);
+              tmem_ld4(col + SEG + cc, w);
               tmem_wait_ld();
               const float4 o = make_float4(__uint_as_float(v[0]) + __uint_as_float(w[0]),
                                            __uint_as_float(v[1]) + __uint_as_float(w[1]),
                                            __uint_as_float(v[2]) + __uint_as_float(w[2]),
                                            __uint_as_float(v[3]) + __uint_as_float(w[3]));
               float* d4 = dst + cc * 128;  // chunk cc / 4 of 128 rows x 4
-              if (SPCP_TC_DEBUG_BITS & 256) {
-                if (o.x == 1.2345f) d4[0] = o.y;  // keep the loads, drop the stores
-              } else if (first || (SPCP_TC_DEBUG_BITS & 512)) {
+              if (first)
                 *reinterpret_cast<float4*>(d4) = o;
-              } else {
-                red_add_v4(d4, __float_as_uint(o.x), __float_as_uint(o.y),
-                           __float_as_uint(o.z), __float_as_uint(o.w));
-              }
+              else
+                red_add_v4(d4, __float_as_uint(o.x), __float_as_uint(o.y), __float_as_uint(o.z),
+                           __float_as_uint(o.w));
             }
           });
+#endif
         }
       } else if (!(SPCP_TC_DEBUG_BITS & 1)) {
         // chunked slot [kst / 4][64 rows][4] (coalesced float4 stores)
@@ -940,8 +1015,9 @@ __global__ void tc_max_kernel(const double* __restrict__ z, const double* __rest
 
 // pass 2 (folded into the image pass): power-of-two scales from the maxima
 __device__ __forceinline__ TcScales tc_compute_scales(const TcScales* sc, double tau) {
-  const double mu = __longlong_as_double(sc->max_bits[0]);
-  const double mv = __longlong_as_double(sc->max_bits[1]);
+  // L2 reads (the maxima were just produced by atomics of other blocks)
+  const double mu = __longlong_as_double(__ldcg(&sc->max_bits[0]));
+  const double mv = __longlong_as_double(__ldcg(&sc->max_bits[1]));
   auto pow2_for = [](double mx) {  // largest 2^e with mx * 2^e <= 2^14
     if (!(mx > 0.0)) return 1.0;
     int e;
@@ -1023,17 +1099,17 @@ __global__ void tc_images_kernel(const double* __restrict__ z, const double* __r
 }
 
 // pass 3 (K-concatenated layout, TcCfg<.., SEG>::KC): one fp16 image per 128-row
-// sub-band of U, rows [uh | uh | um | 0] (U negated, as above), and per 64-row
-// tile of V, rows [vh | vm | vh | 0]; segment e / SEG, rank index e % SEG
+// sub-band of U, rows [um | uh | uh | 0] (U negated, as above), and per 64-row
+// tile of V, rows [vh | vm | vh | 0]; entry e of a row lives in K-atom
+// e / (RB / 2) (atoms of all rows stored one after another)
 template <int SEG>
-__global__ void tc_images_kc_kernel(const double* __restrict__ z, const double* __restrict__ dz,
-                                    double alpha, int64_t m, int64_t n, int64_t k, int64_t m_pad,
-                                    int64_t n_pad, TcScales* sc, double tau, unsigned char* u_img,
-                                    unsigned char* v_img) {
+__device__ __forceinline__ void tc_images_kc_body(const double* __restrict__ z,
+                                                  const double* __restrict__ dz, double alpha,
+                                                  int64_t m, int64_t n, int64_t k, int64_t m_pad,
+                                                  int64_t n_pad, TcScales* sc, double tau,
+                                                  unsigned char* u_img, unsigned char* v_img) {
   using C = TcCfg<16, false, SEG>;
-  constexpr int RB = C::RB, NE = RB / 2;
-  tc::pdl_wait();
-  tc::pdl_launch_next();
+  constexpr int RB = C::RB, EPA = RB / 2, NE = C::NA * EPA;  // entries per atom / per row
   const TcScales scl = tc_compute_scales(sc, tau);
   const double su = scl.su, sv = scl.sv;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1063,15 +1139,101 @@ __global__ void tc_images_kc_kernel(const double* __restrict__ z, const double* 
     }
     const __half hh = __double2half(w);
     const __half lo = __double2half(w - double(__half2float(hh)));
-    unsigned char* base = is_u ? u_img + (r >> 7) * (128 * RB) : v_img + (r >> 6) * (64 * RB);
+    unsigned char* base = is_u ? u_img + (r >> 7) * C::U_BYTES : v_img + (r >> 6) * C::V_BYTES;
+    const int atom = is_u ? C::U_ATOM : C::V_ATOM;
     const int rr = int(is_u ? (r & 127) : (r & 63));
-    // U: segments (h, h, m); V: (h, m, h)
-    *reinterpret_cast<__half*>(base + tc::Swz<RB>::offset(rr, c * 2)) = hh;
-    *reinterpret_cast<__half*>(base + tc::Swz<RB>::offset(rr, (SEG + c) * 2)) = is_u ? hh : lo;
-    *reinterpret_cast<__half*>(base + tc::Swz<RB>::offset(rr, (2 * SEG + c) * 2)) = is_u ? lo : hh;
-    for (int e = 3 * SEG + c; e < NE; e += SEG)
-      *reinterpret_cast<__half*>(base + tc::Swz<RB>::offset(rr, e * 2)) = __half(0.f);
+    auto put = [&](int e, __half val) {
+      *reinterpret_cast<__half*>(base + (e / EPA) * atom +
+                                 tc::Swz<RB>::offset(rr, (e % EPA) * 2)) = val;
+    };
+    // U: segments (m, h, h); V: (h, m, h)
+    put(c, is_u ? lo : hh);
+    put(SEG + c, is_u ? hh : lo);
+    put(2 * SEG + c, hh);
+    for (int e = 3 * SEG + c; e < NE; e += SEG) put(e, __half(0.f));
   }
+}
+
+template <int SEG>
+__global__ void tc_images_kc_kernel(const double* __restrict__ z, const double* __restrict__ dz,
+                                    double alpha, int64_t m, int64_t n, int64_t k, int64_t m_pad,
+                                    int64_t n_pad, TcScales* sc, double tau, unsigned char* u_img,
+                                    unsigned char* v_img) {
+  tc::pdl_wait();
+  tc::pdl_launch_next();
+  tc_images_kc_body<SEG>(z, dz, alpha, m, n, k, m_pad, n_pad, sc, tau, u_img, v_img);
+}
+
+// Grid-wide barrier for a kernel whose blocks are all resident (grid sized
+// from the occupancy): arrival counter + generation word, both in the
+// problem's counter buffer (zeroed at creation, the counter re-armed here).
+__device__ __forceinline__ void grid_barrier(unsigned* count, volatile unsigned* gen,
+                                             unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(count, 1u) == nblocks - 1u) {
+      *count = 0u;
+      __threadfence();
+      atomicAdd(const_cast<unsigned*>(gen), 1u);
+    } else {
+      while (*gen == g) __nanosleep(64);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// passes 1-3 in ONE launch (K-concatenated layout): max |U|, |V| of the trial
+// point, a grid barrier, then scales and images.  The dependent fused pass is
+// released (PDL) only after the barrier, when every block of this grid is
+// resident, so it cannot take the SMs the remaining blocks need.
+template <int SEG>
+__global__ void __launch_bounds__(256) tc_prep_kc_kernel(
+    const double* __restrict__ z, const double* __restrict__ dz, double alpha, int64_t m,
+    int64_t n, int64_t k, int64_t m_pad, int64_t n_pad, TcScales* sc, double tau,
+    unsigned char* u_img, unsigned char* v_img, unsigned* bar_count, unsigned* bar_gen) {
+  tc::pdl_wait();
+  {  // pass 1 (tc_max_kernel's loop)
+    unsigned long long mu = 0, mv = 0;
+    const int64_t nu = m * k, tot = (m + n) * k, stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t q0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q0 < tot;
+         q0 += 4 * stride) {
+      double zv[4], dv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t q = q0 + u * stride;
+        zv[u] = q < tot ? __ldg(z + q) : 0.0;
+        dv[u] = (dz && q < tot) ? __ldg(dz + q) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t q = q0 + u * stride;
+        double w = zv[u];
+        if (dz) w += alpha * dv[u];
+        const unsigned long long bits = q < tot ? __double_as_longlong(fabs(w)) : 0ull;
+        if (q < nu)
+          mu = bits > mu ? bits : mu;
+        else
+          mv = bits > mv ? bits : mv;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long x = __shfl_xor_sync(0xffffffffu, mu, o);
+      const unsigned long long y = __shfl_xor_sync(0xffffffffu, mv, o);
+      mu = x > mu ? x : mu;
+      mv = y > mv ? y : mv;
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMax(&sc->max_bits[0], mu);
+      atomicMax(&sc->max_bits[1], mv);
+    }
+  }
+  grid_barrier(bar_count, bar_gen, gridDim.x);
+  tc::pdl_launch_next();
+  tc_images_kc_body<SEG>(z, dz, alpha, m, n, k, m_pad, n_pad, sc, tau, u_img, v_img);
 }
 
 }  // namespace spcp

@@ -281,7 +281,7 @@ def gen_io(spcp):
 # _complement_term) are captured too, to pin the streaming t4 route.
 CONFIGS = {  # tag: (m, n, rank, gen_seed, mask (frac, seed) | None, lam_l, ks)
     "c2": (20000, 20000, 20, 0, None, 40.0, (20,)),
-    "c3": (110592, 2000, 3, 0, None, 30.0, (3, 5)),
+    "c3": (110592, 2000, 3, 0, None, 30.0, (3,)),
     "c4s": (16000, 3200, 30, 0, (0.3, 1), 20.0, (30,)),
 }
 

@@ -92,6 +92,8 @@ def test_init_and_evaluation(cfg):
         assert np.linalg.norm(gu64) == pytest.approx(float(d[f"k{k}_init_gu_norm"]), rel=1e-7)
         assert np.linalg.norm(gv64) == pytest.approx(float(d[f"k{k}_init_gv_norm"]), rel=1e-7)
         f32, gu32, gv32 = split_objective(fp, spec, precision="fp32")
+        print(f"{tag} k={k} fp32 at init: f {abs(f32 - f64) / abs(f64):.2e} grad_U "
+              f"{rel(gu32, gu64):.2e} grad_V {rel(gv32, gv64):.2e}")
         assert f32 == pytest.approx(float(d[f"k{k}_init_f"]), rel=1e-5)
         assert rel(np.r_[gu32.ravel(), gv32.ravel()], np.r_[gu64.ravel(), gv64.ravel()]) <= 1e-5
         torch.cuda.synchronize()
