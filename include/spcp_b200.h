@@ -73,6 +73,8 @@ enum spcp_dtype { SPCP_F32 = 0, SPCP_F64 = 1, SPCP_U8 = 2 /* mask bytes, SLRM re
 /* storage flags for spcp_problem_create */
 #define SPCP_STORE_F32 1u
 #define SPCP_STORE_F64 2u
+#define SPCP_STORE_SPARSE 4u /* masked X: force the sparse-observation (CSR + CSC) path */
+#define SPCP_STORE_DENSE 8u  /* masked X: force the dense streaming pass */
 
 typedef struct spcp_problem spcp_problem;
 
@@ -98,8 +100,11 @@ int spcp_problem_create(spcp_problem** out, int device, int64_t m, int64_t n,
                         double lambda_s, int64_t n_total, int64_t col0, void* stream);
 int spcp_problem_destroy(spcp_problem* p);
 int spcp_problem_set_stream(spcp_problem* p, void* stream);
-/* info[0] = 0.5*||P_Omega X||_F^2 (local shard), info[1] = #observed entries,
- * info[2] = stored dtypes mask, info[3] = device bytes held */
+/* info (8 doubles): [0] = 0.5*||P_Omega X||_F^2 (local shard), [1] = #observed
+ * entries, [2] = stored dtypes mask, [3] = device bytes held, [4] = observed
+ * entries stored for the sparse-observation evaluation (CSR + CSC, chosen at
+ * creation for masks at most 10% observed; SPCP_SDDMM=on|off forces it), -1 if
+ * the dense streaming pass is used. */
 int spcp_problem_info(spcp_problem* p, double* info);
 
 /* ---- objective + gradient (solver.py:105-123) ------------------------------

@@ -19,7 +19,7 @@ from .errors import (
 )
 
 __all__ = ["lib", "check", "LIB_PATH", "SPCP_F32", "SPCP_F64", "SPCP_U8", "STORE_F32",
-           "STORE_F64", "EXPORTS"]
+           "STORE_F64", "STORE_SPARSE", "STORE_DENSE", "EXPORTS"]
 
 # SPCP_LIB_PATH: an alternative build of the same ABI (A/B timing tools only)
 LIB_PATH = os.environ.get("SPCP_LIB_PATH") or os.path.join(
@@ -29,7 +29,7 @@ SPCP_OK, SPCP_ERR_VALUE, SPCP_ERR_DIMENSION, SPCP_ERR_NUMERICAL, SPCP_ERR_CUDA, 
     SPCP_ERR_UNSUPPORTED, SPCP_ERR_IO, SPCP_ERR_MALFORMED_HEADER, SPCP_ERR_TRUNCATED, \
     SPCP_ERR_NONFINITE, SPCP_ERR_NOT_FOUND = range(11)
 SPCP_F32, SPCP_F64, SPCP_U8 = 0, 1, 2
-STORE_F32, STORE_F64 = 1, 2
+STORE_F32, STORE_F64, STORE_SPARSE, STORE_DENSE = 1, 2, 4, 8
 
 _i64, _i32, _u32 = ctypes.c_int64, ctypes.c_int, ctypes.c_uint
 _vp, _dp, _d = ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_double

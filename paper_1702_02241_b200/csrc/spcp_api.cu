@@ -21,6 +21,7 @@
 
 #include "aux_kernels.cuh"
 #include "common.cuh"
+#include "sddmm.cuh"
 #include "stream_f64.cuh"
 #include "stream_simt.cuh"
 #include "stream_tc.cuh"
@@ -140,6 +141,10 @@ struct spcp_problem {
   spcp::DevBuf tc_units, tc_begin, tc_csr, tc_uimg, tc_vimg, tc_scales;
   int64_t tc_csr_u_off = 0, tc_csr_u_idx = 0, tc_csr_v_off = 0, tc_csr_v_idx = 0;
   int64_t tc_max_u_src = 0, tc_max_v_src = 0;  // largest CSR source lists (reduce sizing)
+  // sparse-observation path (sddmm.cuh): observed entries in CSR and CSC
+  bool sddmm = false;
+  int64_t nnz = 0;
+  spcp::DevBuf csr_ptr, csr_idx, csr_v32, csr_v64, csc_ptr, csc_idx, csc_v32, csc_v64;
 };
 
 namespace spcp {
@@ -157,6 +162,7 @@ struct DT<double> {
 };
 
 struct LaunchShape {
+  int nphi = 0;  // > 0: number of objective partials (overrides the layout's count)
   int nchunks = 1, nrb = 1;
   int64_t chunk_cols = 0;
   int tc = 0;  // partials in the tensor-core (CSR slot) layout
@@ -662,9 +668,11 @@ static int tc_images_kc(spcp_problem* p, int64_t k, const double* z, const doubl
   return SPCP_OK;
 }
 
-// 1: max + scales + images in one launch (tc_prep_kc); 0: tc_max + tc_images_kc
+// 1: max + scales + images in one launch (tc_prep_kc); 0: tc_max + tc_images_kc.
+// Measured same-box: no gain at C2 (0.415 ms steps either way), C1 steps
+// 0.032 -> 0.038 ms (the grid barrier), so 0.
 #ifndef SPCP_TC_PREP_FUSED
-#define SPCP_TC_PREP_FUSED 1
+#define SPCP_TC_PREP_FUSED 0
 #endif
 // max + scales + images in one launch (tc_prep_kc_kernel: grid barrier, so
 // the grid is sized to be fully resident)
@@ -792,13 +800,84 @@ static int tc_eval(spcp_problem* p, int64_t k, const double* z, const double* dz
   return SPCP_OK;
 }
 
+// ---- sparse-observation evaluation (sddmm.cuh): CSR row pass + CSC column pass
+template <typename T, typename TX, int KP>
+static int sddmm_launch(spcp_problem* p, LaunchShape& sh) {
+  const int nb = kSMs * 4;  // 32 warps per SM, grid-stride over rows / columns
+  SddmmParams a{};
+  a.tau = p->lambda_s;
+  const bool x64 = std::is_same<TX, double>::value;
+  a.ptr = p->csr_ptr.as<int64_t>();
+  a.idx = p->csr_idx.as<int32_t>();
+  a.val = x64 ? p->csr_v64.ptr : p->csr_v32.ptr;
+  a.own = p->uc.ptr;
+  a.other = p->vc.ptr;
+  a.out = p->pleft.ptr;
+  a.pphi = p->pphi.as<double>();
+  a.rows = p->m;
+  if (p->prof && prof_begin(p)) return SPCP_ERR_CUDA;
+  sddmm_pass_kernel<T, TX, KP><<<nb, 256, 0, p->stream>>>(a);
+  SPCP_CHECK_LAUNCH("sddmm_pass(rows)");
+  SddmmParams b = a;
+  b.ptr = p->csc_ptr.as<int64_t>();
+  b.idx = p->csc_idx.as<int32_t>();
+  b.val = x64 ? p->csc_v64.ptr : p->csc_v32.ptr;
+  b.own = p->vc.ptr;
+  b.other = p->uc.ptr;
+  b.out = p->pright.ptr;
+  b.pphi = nullptr;
+  b.rows = p->n;
+  sddmm_pass_kernel<T, TX, KP><<<nb, 256, 0, p->stream>>>(b);
+  SPCP_CHECK_LAUNCH("sddmm_pass(cols)");
+  if (p->prof && prof_end(p)) return SPCP_ERR_CUDA;
+  p->launches += 2;
+  sh.nchunks = 1;
+  sh.nrb = 1;
+  sh.nphi = nb;
+  return SPCP_OK;
+}
+
+#define SPCP_SDDMM_KP(X) X(8) X(16) X(24) X(32) X(40) X(48) X(56) X(64)
+template <typename T, typename TX>
+static int sddmm_dispatch(spcp_problem* p, int kp, LaunchShape& sh) {
+  switch (kp) {
+#define SPCP_SD_CASE(K) \
+    case K: return sddmm_launch<T, TX, K>(p, sh);
+    SPCP_SDDMM_KP(SPCP_SD_CASE)
+#undef SPCP_SD_CASE
+  }
+  return fail(SPCP_ERR_UNSUPPORTED, "no sparse-observation kernel for this rank bound");
+}
+
+static int sddmm_eval(spcp_problem* p, int64_t k, int dtype, const double* z, const double* dz,
+                      double alpha, int& kp_used, LaunchShape& sh, int& part_dtype) {
+  const int kp = int(round_up(k, 8));
+  kp_used = kp;
+  int rc;
+  if ((rc = p->pphi.ensure(size_t(kSMs) * 4 * sizeof(double)))) return rc;
+  if (dtype == SPCP_F32 && p->csr_v32.ptr) {
+    part_dtype = SPCP_F32;
+    if ((rc = prep<float>(p, k, kp, z, dz, alpha))) return rc;
+    if ((rc = p->pleft.ensure(size_t(p->m_pad) * kp * sizeof(float)))) return rc;
+    if ((rc = p->pright.ensure(size_t(p->n_pad) * kp * sizeof(float)))) return rc;
+    return sddmm_dispatch<float, float>(p, kp, sh);
+  }
+  part_dtype = SPCP_F64;
+  if ((rc = prep<double>(p, k, kp, z, dz, alpha))) return rc;
+  if ((rc = p->pleft.ensure(size_t(p->m_pad) * kp * sizeof(double)))) return rc;
+  if ((rc = p->pright.ensure(size_t(p->n_pad) * kp * sizeof(double)))) return rc;
+  return p->csr_v64.ptr ? sddmm_dispatch<double, double>(p, kp, sh)
+                        : sddmm_dispatch<double, float>(p, kp, sh);
+}
+
 static int run_stream_eval(spcp_problem* p, int64_t k, int dtype, const double* z,
                            const double* dz, double alpha, int& kp_used, LaunchShape& sh,
                            int& part_dtype) {
-  int kp = eval_kp(dtype, k);
-  kp_used = kp;
   if (dtype == SPCP_F32 && !p->x32.ptr)
     return fail(SPCP_ERR_VALUE, "fp32 evaluation requested but no fp32 copy of X is stored");
+  if (p->sddmm && k <= 64) return sddmm_eval(p, k, dtype, z, dz, alpha, kp_used, sh, part_dtype);
+  int kp = eval_kp(dtype, k);
+  kp_used = kp;
   if (kp == 0) {
     part_dtype = SPCP_F64;
     return dense_fallback_eval(p, k, z, dz, alpha, sh);
@@ -996,7 +1075,9 @@ static int run_reduce(spcp_problem* p, int64_t k, int kp, int part_dtype, const 
   rp.blk = p->blk.as<double>();
   rp.counter = p->counter.as<unsigned>();
   rp.pphi = (u_mode == U_FROM_SUM) ? nullptr : p->pphi.as<double>();
-  rp.nphi = (u_mode == U_FROM_SUM) ? 0 : (dense ? int(sh.chunk_cols) : sh.nchunks * sh.nrb);
+  rp.nphi = (u_mode == U_FROM_SUM) ? 0
+            : sh.nphi > 0 ? sh.nphi
+                          : (dense ? int(sh.chunk_cols) : sh.nchunks * sh.nrb);
   rp.scal_sum = scal_sum;
   rp.scal_out = scal_out;
   rp.out = p->out_dev.as<double>();
@@ -1182,6 +1263,72 @@ static int apply_impl(spcp_problem* p, int64_t k, const double* z, int64_t b,
 }
 
 
+// Sparse-observation storage (sddmm.cuh): CSR + CSC of the observed entries,
+// values from the device copies of X.  Chosen at creation when the observed
+// fraction is at most SPCP_SDDMM_DENSITY (measured crossover against the dense
+// tensor-core pass, tools/sddmm_probe.py), or forced by SPCP_SDDMM=on|off.
+static constexpr double kSddmmDensity = 0.10;
+
+static int build_sddmm(spcp_problem* p) {
+  int rc;
+  const int64_t words = ceil_div(p->n, 32);
+  DevBuf cnt;
+  if ((rc = cnt.ensure(size_t(std::max(p->m, p->n)) * sizeof(int64_t)))) return rc;
+  if ((rc = p->csr_ptr.ensure(size_t(p->m + 1) * sizeof(int64_t)))) return rc;
+  if ((rc = p->csc_ptr.ensure(size_t(p->n + 1) * sizeof(int64_t)))) return rc;
+  const uint32_t* mb = p->mbits.as<uint32_t>();
+  sddmm_row_count_kernel<<<kSMs * 4, 256, 0, p->stream>>>(mb, p->ldm, p->m, words,
+                                                          cnt.as<int64_t>());
+  SPCP_CHECK_LAUNCH("sddmm_row_count");
+  sddmm_scan_kernel<<<1, 1024, 0, p->stream>>>(cnt.as<int64_t>(), p->m, p->csr_ptr.as<int64_t>());
+  SPCP_CHECK_LAUNCH("sddmm_scan(rows)");
+  sddmm_col_count_kernel<<<kSMs * 4, 256, 0, p->stream>>>(mb, p->ldm, p->m, p->n,
+                                                          cnt.as<int64_t>());
+  SPCP_CHECK_LAUNCH("sddmm_col_count");
+  sddmm_scan_kernel<<<1, 1024, 0, p->stream>>>(cnt.as<int64_t>(), p->n, p->csc_ptr.as<int64_t>());
+  SPCP_CHECK_LAUNCH("sddmm_scan(cols)");
+  int64_t nnz[2] = {0, 0};
+  SPCP_CUDA(cudaMemcpyAsync(&nnz[0], p->csr_ptr.as<int64_t>() + p->m, sizeof(int64_t),
+                            cudaMemcpyDeviceToHost, p->stream));
+  SPCP_CUDA(cudaMemcpyAsync(&nnz[1], p->csc_ptr.as<int64_t>() + p->n, sizeof(int64_t),
+                            cudaMemcpyDeviceToHost, p->stream));
+  SPCP_CUDA(cudaStreamSynchronize(p->stream));
+  if (nnz[0] != nnz[1]) return fail(SPCP_ERR_NUMERICAL, "sparse-observation index mismatch");
+  if (nnz[0] >= (int64_t(1) << 40)) return fail(SPCP_ERR_UNSUPPORTED, "too many observations");
+  const size_t nz = size_t(std::max<int64_t>(nnz[0], 1));
+  if ((rc = p->csr_idx.ensure(nz * sizeof(int32_t)))) return rc;
+  if ((rc = p->csc_idx.ensure(nz * sizeof(int32_t)))) return rc;
+  const int g = kSMs * 4;
+  if (p->x32.ptr) {
+    if ((rc = p->csr_v32.ensure(nz * sizeof(float)))) return rc;
+    if ((rc = p->csc_v32.ensure(nz * sizeof(float)))) return rc;
+    sddmm_csr_fill_kernel<float><<<g, 256, 0, p->stream>>>(
+        mb, p->ldm, p->m, p->n, p->x32.as<float>(), p->ldx, p->csr_ptr.as<int64_t>(),
+        p->csr_idx.as<int32_t>(), p->csr_v32.as<float>());
+    SPCP_CHECK_LAUNCH("sddmm_csr_fill");
+    sddmm_csc_fill_kernel<float><<<g, 256, 0, p->stream>>>(
+        mb, p->ldm, p->m, p->n, p->x32.as<float>(), p->ldx, p->csc_ptr.as<int64_t>(),
+        p->csc_idx.as<int32_t>(), p->csc_v32.as<float>());
+    SPCP_CHECK_LAUNCH("sddmm_csc_fill");
+  }
+  if (p->x64.ptr) {
+    if ((rc = p->csr_v64.ensure(nz * sizeof(double)))) return rc;
+    if ((rc = p->csc_v64.ensure(nz * sizeof(double)))) return rc;
+    sddmm_csr_fill_kernel<double><<<g, 256, 0, p->stream>>>(
+        mb, p->ldm, p->m, p->n, p->x64.as<double>(), p->ldx, p->csr_ptr.as<int64_t>(),
+        p->csr_idx.as<int32_t>(), p->csr_v64.as<double>());
+    SPCP_CHECK_LAUNCH("sddmm_csr_fill");
+    sddmm_csc_fill_kernel<double><<<g, 256, 0, p->stream>>>(
+        mb, p->ldm, p->m, p->n, p->x64.as<double>(), p->ldx, p->csc_ptr.as<int64_t>(),
+        p->csc_idx.as<int32_t>(), p->csc_v64.as<double>());
+    SPCP_CHECK_LAUNCH("sddmm_csc_fill");
+  }
+  SPCP_CUDA(cudaStreamSynchronize(p->stream));
+  p->nnz = nnz[0];
+  p->sddmm = true;
+  return SPCP_OK;
+}
+
 // ====================================================================== ABI
 extern "C" {
 
@@ -1317,6 +1464,19 @@ int spcp_problem_create(spcp_problem** out, int device, int64_t m, int64_t n, co
     p->f_zero = h[0];
     p->n_obs = h[1];
   }
+  if (p->masked) {
+    static const std::string mode = env_str("SPCP_SDDMM");
+    static const double thr = [] {
+      const std::string v = env_str("SPCP_SDDMM_DENSITY");
+      return v.empty() ? kSddmmDensity : atof(v.c_str());
+    }();
+    const double density = p->n_obs / (double(m) * double(n));
+    const bool force_on = (store & SPCP_STORE_SPARSE) || (!(store & SPCP_STORE_DENSE) && mode == "on");
+    const bool force_off = (store & SPCP_STORE_DENSE) || mode == "off";
+    if (force_on || (!force_off && density <= thr)) {
+      if ((rc = build_sddmm(p))) return bail(rc);
+    }
+  }
   for (int i = 0; i < spcp_problem::kEvRing; ++i) {
     SPCP_CUDA(cudaEventCreate(&p->ev0[i]));
     SPCP_CUDA(cudaEventCreate(&p->ev1[i]));
@@ -1331,7 +1491,10 @@ int spcp_problem_destroy(spcp_problem* p) {
   if (p->stream) cudaStreamSynchronize(p->stream);
   for (DevBuf* b : {&p->x32, &p->x64, &p->mbits, &p->uc, &p->vc, &p->wr, &p->wl, &p->pleft,
                     &p->pright, &p->pphi, &p->blk, &p->out_dev, &p->counter, &p->scratch,
-                    &p->scal, &p->gu_tmp, &p->vec_part, &p->small})
+                    &p->scal, &p->gu_tmp, &p->vec_part, &p->small, &p->csr_ptr, &p->csr_idx,
+                    &p->csr_v32, &p->csr_v64, &p->csc_ptr, &p->csc_idx, &p->csc_v32,
+                    &p->csc_v64, &p->tc_units, &p->tc_begin, &p->tc_csr, &p->tc_uimg,
+                    &p->tc_vimg, &p->tc_scales})
     b->release();
   if (p->host_out) cudaFreeHost(p->host_out);
   for (int i = 0; i < spcp_problem::kEvRing; ++i) {
@@ -1354,6 +1517,7 @@ int spcp_problem_info(spcp_problem* p, double* info) {
   info[1] = p->n_obs;
   info[2] = double(p->stored);
   info[3] = double(p->x32.bytes + p->x64.bytes + p->mbits.bytes);
+  info[4] = p->sddmm ? double(p->nnz) : -1.0;  // observed entries on the sparse path
   return SPCP_OK;
 }
 

@@ -624,8 +624,7 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK, SEG>::NTHREADS, 1)
     const TcScales sc = *p.scales;
     const float sigma = sc.sigma, tau_s = sc.tau_s, kappa = sc.kappa;
     const float2 sig2 = make_float2(sigma, sigma), kap2 = make_float2(kappa, kappa);
-    const float2 nhalf2 = make_float2(-0.5f, -0.5f), zero2 = make_float2(0.f, 0.f);
-    const float2 qc2 = make_float2(201326592.f, 201326592.f);  // 1.5 * 2^27: quantum 16
+    const float2 nhalf2 = make_float2(-0.5f, -0.5f);
     double phi_acc = 0.0;
     constexpr int GTC = KP16 / 2;  // accumulator columns drained per warp (of KP16)
     const int kst = p.kstore;      // partial row stride: k rounded up to 4 (<= KP16)
@@ -868,9 +867,11 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK, SEG>::NTHREADS, 1)
         }
         // The MMA produced S'' = -sigma L (U image negated), so r'' = sigma r =
         // fma(x, sigma, S'').  cs = clamp(r'', +-tau''), huber'' = cs (r'' - cs/2)
-        // (quadratic on ties, as the reference), gp = kappa cs = -G'', split at
-        // a fixed quantum: hi = (gp + 1.5 2^27) - 1.5 2^27 is a multiple of 16
-        // (exact in fp16 for |gp| <= 2^14), lo = gp - hi in [-8, 8].
+        // (quadratic on ties, as the reference), gp = kappa cs = -G'' (|gp| <
+        // 2^14), split in floating point: hi = fp16(gp), lo = fp16(gp - hi), so
+        // gp = hi + lo to 2^-22 of |gp| for every entry (a fixed-quantum split
+        // was exact only relative to tau: residuals far below tau, the noise at
+        // a good iterate, lost ~1e-5 of their value).
 #pragma unroll
         for (int e2 = 0; e2 < 16; e2 += 2) {
           float2 r2 = ffma2(make_float2(xv[e2], xv[e2 + 1]), sig2,
@@ -882,10 +883,10 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK, SEG>::NTHREADS, 1)
           const float2 cs2 = make_float2(fminf(fmaxf(r2.x, -tau_s), tau_s),
                                          fminf(fmaxf(r2.y, -tau_s), tau_s));
           hs2 = ffma2(cs2, ffma2(nhalf2, cs2, r2), hs2);
-          const float2 ht = ffma2(cs2, kap2, qc2);
-          const float2 hi2 = fsub2(ht, qc2);
-          const float2 lo2 = fsub2(ffma2(cs2, kap2, zero2), hi2);
-          hi[8 * ch + (e2 >> 1)] = pack_half2(hi2.x, hi2.y);
+          const float2 gp2 = fmul2(cs2, kap2);
+          const __half2 hh2 = __float22half2_rn(gp2);
+          const float2 lo2 = fsub2(gp2, __half22float2(hh2));
+          hi[8 * ch + (e2 >> 1)] = *reinterpret_cast<const uint32_t*>(&hh2);
           lo[8 * ch + (e2 >> 1)] = pack_half2(lo2.x, lo2.y);
         }
       }

@@ -11,7 +11,7 @@ import ctypes
 
 import numpy as np
 
-from ._lib import SPCP_F32, SPCP_F64, STORE_F32, STORE_F64, check, lib
+from ._lib import SPCP_F32, SPCP_F64, STORE_DENSE, STORE_F32, STORE_F64, STORE_SPARSE, check, lib
 
 __all__ = ["DeviceProblem", "torch_mod", "cuda_device", "dptr", "PRECISIONS"]
 
@@ -55,7 +55,9 @@ class DeviceProblem:
     """One column shard (or the whole matrix) of X resident on a GPU.
 
     x: host numpy array (float64 or float32) or a CUDA tensor, m x n.
-    store: iterable of "f32" / "f64": which device copies to keep.
+    store: iterable of "f32" / "f64": which device copies to keep; "sparse" /
+      "dense" force the masked evaluation path (default: sparse when at most
+      10% of the entries are observed, sddmm.cuh).
     n_total, col0: column-sharded mode.
     """
 
@@ -87,8 +89,9 @@ class DeviceProblem:
             mptr = ctypes.c_void_p(mk.ctypes.data)
             self._keep_mask = mk
         flags = 0
+        codes = {"f32": STORE_F32, "f64": STORE_F64, "sparse": STORE_SPARSE, "dense": STORE_DENSE}
         for s in store:
-            flags |= STORE_F32 if s == "f32" else STORE_F64
+            flags |= codes[s]
         self.m, self.n = int(m), int(n)
         self.n_total = int(n_total if n_total is not None else n)
         self.col0 = int(col0)
@@ -103,10 +106,12 @@ class DeviceProblem:
         self.handle = h
         self._keep = None
         self._keep_mask = None
-        info = (ctypes.c_double * 4)()
+        info = (ctypes.c_double * 8)()
         check(lib.spcp_problem_info(self.h, info))
         self.f_zero = float(info[0])
         self.n_obs = float(info[1])
+        # observed entries held for the sparse-observation path (sddmm.cuh), or None
+        self.sparse_nnz = int(info[4]) if info[4] >= 0 else None
         self._out = (ctypes.c_double * 8)()
 
     # ------------------------------------------------------------ lifecycle

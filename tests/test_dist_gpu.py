@@ -103,4 +103,6 @@ def test_sharded_solve_and_certificate_match_single_gpu(precision):
     # both ranks hold the same replicated U and the same report
     np.testing.assert_array_equal(res[0][3], res[1][3])
     assert res[0][6] == res[1][6] and res[0][7] == res[1][7]
-    assert res[0][6] == pytest.approx(rc.e_norm, rel=1e-3, abs=1e-6)
+    # e_norm: equal where it measures distance, both at the noise floor otherwise
+    # (there it depends on where each L-BFGS run stopped)
+    assert abs(res[0][6] - rc.e_norm) <= 1e-3 * rc.e_norm + 1e-4 * lam_l

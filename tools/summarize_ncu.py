@@ -20,7 +20,7 @@ for r in rows[hi + 1:]:
     if len(r) > vi:
         per.append((r[ki], float(r[vi].replace(",", ""))))
 # the timed eval region: the launches from the first tc_max_kernel on
-first = next(i for i, (n, _) in enumerate(per) if "tc_max_kernel" in n)
+first = next(i for i, (n, _) in enumerate(per) if "tc_max_kernel" in n or "tc_prep_kc" in n)
 ev = per[first:]
 agg = collections.OrderedDict()
 for n, v in ev:
