@@ -7,12 +7,12 @@
 //        g_ij = -clip(r_ij, +-tau), phi += huber(r_ij), (G V)_i = sum_j g_ij v_j
 //   CSC (col_ptr, row, x) for the column pass: (G^T U)_j = sum_i g_ij u_i
 //        (the residual is recomputed: no g buffer, one read of each copy)
-// Both passes put one warp on a row (column): the warp's lanes walk its
-// nonzeros, u_i (v_j) sits in shared memory and is read as a broadcast, the
-// other factor's row is gathered from L2 (U, V are small), the rank-k
-// accumulators live in registers and are folded by a fixed butterfly — the
-// summation order depends only on the sparsity pattern, so results are
-// bitwise reproducible.  Outputs use the one-chunk / one-band partial layout
+// Both passes put one warp on a row (column): sub-groups of lanes walk its
+// nonzeros, each lane holding a 16-byte slice of the rank dimension, u_i
+// (v_j) in registers, the other factor's row gathered from L2 with coalesced
+// 16-byte loads (U, V are small), the rank-k accumulators in registers folded
+// by fixed butterflies — the summation order depends only on the sparsity
+// pattern, so results are bitwise reproducible.  Outputs use the one-chunk / one-band partial layout
 // of the streaming kernels (pleft[m_pad][KP], pright[n_pad][KP]), folded by
 // reduce_kernel<T> with the objective partials per block.
 //
@@ -153,14 +153,26 @@ struct SddmmParams {
   int64_t rows;
 };
 
-// One warp per row (CSR) or column (CSC): see the file comment.  KP = rank
-// padded to 4 (float4 / double2 gathers), KC = gather chunk.
+// One warp per row (CSR) or column (CSC).  The warp splits into NPW
+// sub-groups of G lanes; a sub-group takes one nonzero at a time and its lanes
+// hold VEC consecutive rank columns each (G * VEC >= KP): the gathered row of
+// the other factor is one coalesced 16-byte load per lane, the dot product is
+// reduced over the sub-group by xor shuffles, and each lane accumulates g times
+// its columns.  At the end of the row the NPW sub-group accumulators are folded
+// by a fixed xor butterfly.  The walked factor's row stays in registers.
 template <typename T, typename TX, int KP>
 __global__ void __launch_bounds__(256) sddmm_pass_kernel(const SddmmParams p) {
-  constexpr int KC = 8;  // gathered entries held at once
-  __shared__ T own_s[8][KP];
+  constexpr int VEC = 16 / int(sizeof(T));
+  constexpr int G0 = (KP + VEC - 1) / VEC;
+  constexpr int G = G0 <= 1 ? 1 : G0 <= 2 ? 2 : G0 <= 4 ? 4 : G0 <= 8 ? 8 : G0 <= 16 ? 16 : 32;
+  constexpr int NPW = 32 / G;  // nonzeros per warp step
+  static_assert(G * VEC >= KP, "lane columns cover the rank");
+  using VT = VecT<T, VEC>;
   __shared__ double red[8];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cg = lane % G, sg = lane / G;  // column group, sub-group
+  const int c0 = cg * VEC;
+  const bool live_c = c0 < KP;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   const T* __restrict__ own = reinterpret_cast<const T*>(p.own);
@@ -170,64 +182,61 @@ __global__ void __launch_bounds__(256) sddmm_pass_kernel(const SddmmParams p) {
   const T tau = T(p.tau);
   double phi = 0.0;
   for (int64_t i = warp; i < p.rows; i += nw) {
-    for (int c = lane; c < KP; c += 32) own_s[wib][c] = own[i * KP + c];
-    __syncwarp();
-    T acc[KP];
+    VT u{};
+    if (live_c) u = *reinterpret_cast<const VT*>(own + i * KP + c0);
+    T acc[VEC];
 #pragma unroll
-    for (int c = 0; c < KP; ++c) acc[c] = T(0);
+    for (int c = 0; c < VEC; ++c) acc[c] = T(0);
     T hs = T(0);
-    const int64_t e1 = p.ptr[i + 1];
-    for (int64_t e = p.ptr[i] + lane; e < e1; e += 32) {
-      const int64_t j = p.idx[e];
-      const T* oj = oth + j * KP;
-      // residual: x - own_i . other_j (gathered in chunks of KC)
-      T d0 = T(0), d1 = T(0);
-#pragma unroll
-      for (int c0 = 0; c0 < KP; c0 += KC) {
-        T o[KC];
-#pragma unroll
-        for (int c = 0; c < KC; ++c) o[c] = c0 + c < KP ? oj[c0 + c] : T(0);
-#pragma unroll
-        for (int c = 0; c < KC; ++c) {
-          if (c0 + c < KP) {
-            if (c & 1)
-              d1 = fma(own_s[wib][c0 + c], o[c], d1);
-            else
-              d0 = fma(own_s[wib][c0 + c], o[c], d0);
-          }
-        }
+    const int64_t eb = p.ptr[i], e1 = p.ptr[i + 1];
+    for (int64_t e0 = eb; e0 < e1; e0 += NPW) {  // warp-uniform trip count
+      const int64_t e = e0 + sg;
+      const bool live = e < e1;
+      VT v{};
+      T x = T(0);
+      if (live) {
+        const int64_t j = p.idx[e];
+        x = T(val[e]);
+        if (live_c) v = *reinterpret_cast<const VT*>(oth + j * KP + c0);
       }
-      const T r = T(val[e]) - (d0 + d1);
-      const T g = huber_clip<T>(r, tau, hs);
+      T d = T(0);
 #pragma unroll
-      for (int c0 = 0; c0 < KP; c0 += KC) {
+      for (int c = 0; c < VEC; ++c) d = fma(u.v[c], v.v[c], d);
 #pragma unroll
-        for (int c = 0; c < KC; ++c)
-          if (c0 + c < KP) acc[c0 + c] = fma(g, oj[c0 + c], acc[c0 + c]);
+      for (int o = 1; o < G; o <<= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+      T g = T(0);
+      if (live) {
+        T h = T(0);
+        g = huber_clip<T>(x - d, tau, h);
+        if (cg == 0) hs += h;
       }
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) acc[c] = fma(g, v.v[c], acc[c]);
     }
     phi += double(hs);
-    // fixed butterfly over the lanes, then lane c writes column c
+    // fold the NPW sub-groups (lanes with the same column group), fixed order
 #pragma unroll
-    for (int c = 0; c < KP; ++c) {
-      T v = acc[c];
+    for (int c = 0; c < VEC; ++c) {
+      T a = acc[c];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      acc[c] = v;
+      for (int o = G; o < 32; o <<= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+      acc[c] = a;
     }
+    if (sg == 0 && live_c) {
+      VT o;
 #pragma unroll
-    for (int c = 0; c < KP; ++c)
-      if (lane == (c & 31)) out[i * KP + c] = acc[c];
-    __syncwarp();
+      for (int c = 0; c < VEC; ++c) o.v[c] = acc[c];
+      *reinterpret_cast<VT*>(out + i * KP + c0) = o;
+    }
   }
   if (p.pphi) {
     phi = warp_sum(phi);
     if (lane == 0) red[wib] = phi;
     __syncthreads();
     if (threadIdx.x == 0) {
-      double s = 0.0;
-      for (int w = 0; w < (blockDim.x >> 5); ++w) s += red[w];
-      p.pphi[blockIdx.x] = s;
+      double s2 = 0.0;
+      for (int w = 0; w < (blockDim.x >> 5); ++w) s2 += red[w];
+      p.pphi[blockIdx.x] = s2;
     }
   }
 }
