@@ -102,9 +102,10 @@ int spcp_problem_destroy(spcp_problem* p);
 int spcp_problem_set_stream(spcp_problem* p, void* stream);
 /* info (8 doubles): [0] = 0.5*||P_Omega X||_F^2 (local shard), [1] = #observed
  * entries, [2] = stored dtypes mask, [3] = device bytes held, [4] = observed
- * entries stored for the sparse-observation evaluation (CSR + CSC, chosen at
- * creation for masks at most 10% observed; SPCP_SDDMM=on|off forces it), -1 if
- * the dense streaming pass is used. */
+ * entries stored for the sparse-observation evaluation (CSR + CSC, built at
+ * creation for masks at most 12% observed and used by fp64 evaluations, and by
+ * fp32 ones below 2.5%; SPCP_STORE_SPARSE / SPCP_SDDMM=on use it for both),
+ * -1 if only the dense streaming passes are used. */
 int spcp_problem_info(spcp_problem* p, double* info);
 
 /* ---- objective + gradient (solver.py:105-123) ------------------------------

@@ -150,7 +150,7 @@ _FAIL_PROB = 1e-6
 # (1 - eps, certified factor): after the bound's iteration count, with
 # probability >= 1 - fail, theta^2 >= (1 - eps) sigma_max^2, i.e.
 # sigma_max <= theta / sqrt(1 - eps)
-_TIERS = ((0.25, 2.0), (0.5, math.sqrt(2.0)))
+_TIERS = ((1.0 / 64.0, 8.0), (1.0 / 16.0, 4.0), (0.25, 2.0), (0.5, math.sqrt(2.0)))
 
 
 def _power_bound_iters(dim, one_minus_eps, fail):
@@ -165,10 +165,10 @@ def _power_bound_iters(dim, one_minus_eps, fail):
     steps of its first start vector, and its top Ritz value theta satisfies
     theta^2 >= xi_{q-1} (Cauchy-Schwarz), so the power-method bound applies
     with k = q - 1.  The iteration tests the bound at every step: a union bound
-    over steps (geometric in q) and over the two tiers gives the factor
-    2 / eps on top of `fail`."""
+    over steps (geometric in q) and over the len(_TIERS) tiers gives the factor
+    len(_TIERS) / eps on top of `fail`."""
     eps = 1.0 - one_minus_eps
-    budget = fail * eps / 2.0
+    budget = fail * eps / len(_TIERS)
     k = math.log(0.824 * math.sqrt(max(dim, 1)) / budget) / -math.log(one_minus_eps) + 0.5
     return int(math.ceil(k)) + 1
 

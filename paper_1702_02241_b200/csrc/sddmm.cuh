@@ -189,29 +189,41 @@ __global__ void __launch_bounds__(256) sddmm_pass_kernel(const SddmmParams p) {
     for (int c = 0; c < VEC; ++c) acc[c] = T(0);
     T hs = T(0);
     const int64_t eb = p.ptr[i], e1 = p.ptr[i + 1];
-    for (int64_t e0 = eb; e0 < e1; e0 += NPW) {  // warp-uniform trip count
-      const int64_t e = e0 + sg;
-      const bool live = e < e1;
-      VT v{};
-      T x = T(0);
-      if (live) {
-        const int64_t j = p.idx[e];
-        x = T(val[e]);
-        if (live_c) v = *reinterpret_cast<const VT*>(oth + j * KP + c0);
-      }
-      T d = T(0);
+    for (int64_t e0 = eb; e0 < e1; e0 += 32) {  // warp-uniform trip count
+      // 32 nonzeros per round: indices and values in one coalesced load
+      // (lane l holds nonzero e0 + l), then every sub-group's gathers of the
+      // round are issued before any is used (memory-level parallelism)
+      constexpr int NS = 32 / NPW;  // steps per round
+      const int64_t el = e0 + lane;
+      const int32_t jl = el < e1 ? p.idx[el] : -1;
+      const T xl = el < e1 ? T(val[el]) : T(0);
+      VT v[NS];
 #pragma unroll
-      for (int c = 0; c < VEC; ++c) d = fma(u.v[c], v.v[c], d);
-#pragma unroll
-      for (int o = 1; o < G; o <<= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-      T g = T(0);
-      if (live) {
-        T h = T(0);
-        g = huber_clip<T>(x - d, tau, h);
-        if (cg == 0) hs += h;
+      for (int st = 0; st < NS; ++st) {
+        const int j = __shfl_sync(0xffffffffu, jl, st * NPW + sg);
+        VT t{};
+        if (j >= 0 && live_c) t = *reinterpret_cast<const VT*>(oth + int64_t(j) * KP + c0);
+        v[st] = t;
       }
 #pragma unroll
-      for (int c = 0; c < VEC; ++c) acc[c] = fma(g, v.v[c], acc[c]);
+      for (int st = 0; st < NS; ++st) {
+        const int src = st * NPW + sg;
+        const int j = __shfl_sync(0xffffffffu, jl, src);
+        const T x = __shfl_sync(0xffffffffu, xl, src);
+        T d = T(0);
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) d = fma(u.v[c], v[st].v[c], d);
+#pragma unroll
+        for (int o = 1; o < G; o <<= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+        T g = T(0);
+        if (j >= 0) {
+          T h = T(0);
+          g = huber_clip<T>(x - d, tau, h);
+          if (cg == 0) hs += h;
+        }
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) acc[c] = fma(g, v[st].v[c], acc[c]);
+      }
     }
     phi += double(hs);
     // fold the NPW sub-groups (lanes with the same column group), fixed order

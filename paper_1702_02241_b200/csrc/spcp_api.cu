@@ -142,7 +142,7 @@ struct spcp_problem {
   int64_t tc_csr_u_off = 0, tc_csr_u_idx = 0, tc_csr_v_off = 0, tc_csr_v_idx = 0;
   int64_t tc_max_u_src = 0, tc_max_v_src = 0;  // largest CSR source lists (reduce sizing)
   // sparse-observation path (sddmm.cuh): observed entries in CSR and CSC
-  bool sddmm = false;
+  bool sddmm = false, sddmm32 = false;  // built; used by fp32 evaluations too
   int64_t nnz = 0;
   spcp::DevBuf csr_ptr, csr_idx, csr_v32, csr_v64, csc_ptr, csc_idx, csc_v32, csc_v64;
 };
@@ -321,9 +321,7 @@ static int dispatch_eval(spcp_problem* p, int kp, StreamParams sp, LaunchShape& 
 // APPLY / RAW widths: fp32 SIMT stream_kernel (k <= 32), fp64 f64_stream_kernel (k <= 64)
 static int apply_kr(int64_t k) {
   if (k == 0) return 0;
-  if (k <= 8) return 8;
-  if (k <= 16) return 16;
-  if (k <= 32) return 32;
+  if (k <= 32) return int(round_up(k, 8));
   return -1;
 }
 static int apply_kr64(int64_t k) {
@@ -332,36 +330,21 @@ static int apply_kr64(int64_t k) {
   return -1;
 }
 
+// rank widths {8, 16, 24, 32} x product widths {8, 16, 32} for the SIMT
+// stream_kernel (the certificate's subspace blocks are 16 wide, C2's k = 20
+// pads to 24: each padding step is a third of the kernel's FMAs)
+#define SPCP_AP_LIST(AP)                                                                 \
+  AP(0, 8) AP(0, 16) AP(0, 32) AP(8, 8) AP(8, 16) AP(8, 32) AP(16, 8) AP(16, 16) AP(16, 32) \
+      AP(24, 8) AP(24, 16) AP(24, 32) AP(32, 8) AP(32, 16) AP(32, 32)
 template <typename T, typename TX, bool MASK>
 static int dispatch_apply(spcp_problem* p, int kr, int pw, StreamParams sp, LaunchShape& sh) {
-  if constexpr (sizeof(T) == 4) {
 #define SPCP_AP(KR, PW)                                                            \
   if (kr == KR && pw == PW)                                                      \
     return KR == 0 ? launch_stream<T, TX, 0, PW, MODE_RAW, MASK>(p, sp, sh, false) \
                    : launch_stream<T, TX, KR, PW, MODE_APPLY, MASK>(p, sp, sh, false);
-    SPCP_AP(0, 8)
-    SPCP_AP(0, 32)
-    SPCP_AP(8, 8)
-    SPCP_AP(8, 32)
-    SPCP_AP(16, 8)
-    SPCP_AP(16, 32)
-    SPCP_AP(32, 8)
-    SPCP_AP(32, 32)
+  SPCP_AP_LIST(SPCP_AP)
 #undef SPCP_AP
-  } else {
-#define SPCP_AP(KR, PW)                                                            \
-  if (kr == KR && pw == PW)                                                      \
-    return KR == 0 ? launch_stream<T, TX, 0, PW, MODE_RAW, MASK>(p, sp, sh, false) \
-                   : launch_stream<T, TX, KR, PW, MODE_APPLY, MASK>(p, sp, sh, false);
-    SPCP_AP(0, 8)
-    SPCP_AP(0, 32)
-    SPCP_AP(8, 8)
-    SPCP_AP(8, 32)
-    SPCP_AP(16, 8)
-    SPCP_AP(16, 32)
-    SPCP_AP(32, 8)
-    SPCP_AP(32, 32)
-#undef SPCP_AP
+  if constexpr (sizeof(T) == 8) {
 #define SPCP_AP(KR, PW)            \
   if (kr == KR && pw == PW)      \
     return launch_f64<KR, PW, MODE_APPLY, MASK, TX>(p, sp, sh);
@@ -803,7 +786,18 @@ static int tc_eval(spcp_problem* p, int64_t k, const double* z, const double* dz
 // ---- sparse-observation evaluation (sddmm.cuh): CSR row pass + CSC column pass
 template <typename T, typename TX, int KP>
 static int sddmm_launch(spcp_problem* p, LaunchShape& sh) {
-  const int nb = kSMs * 4;  // 32 warps per SM, grid-stride over rows / columns
+  // one wave of resident blocks, grid-stride over rows / columns
+  static DevFlags occ_dev = {};
+  int per_sm = occ_dev[dev_slot(p->device)].load(std::memory_order_relaxed);
+  if (per_sm == 0) {
+    SPCP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sddmm_pass_kernel<T, TX, KP>,
+                                                            256, 0));
+    per_sm = std::max(1, std::min(per_sm, 8));
+    occ_dev[dev_slot(p->device)].store(per_sm, std::memory_order_relaxed);
+  }
+  const int nb = kSMs * per_sm;
+  int rc;
+  if ((rc = p->pphi.ensure(size_t(nb) * sizeof(double)))) return rc;
   SddmmParams a{};
   a.tau = p->lambda_s;
   const bool x64 = std::is_same<TX, double>::value;
@@ -854,7 +848,6 @@ static int sddmm_eval(spcp_problem* p, int64_t k, int dtype, const double* z, co
   const int kp = int(round_up(k, 8));
   kp_used = kp;
   int rc;
-  if ((rc = p->pphi.ensure(size_t(kSMs) * 4 * sizeof(double)))) return rc;
   if (dtype == SPCP_F32 && p->csr_v32.ptr) {
     part_dtype = SPCP_F32;
     if ((rc = prep<float>(p, k, kp, z, dz, alpha))) return rc;
@@ -875,7 +868,8 @@ static int run_stream_eval(spcp_problem* p, int64_t k, int dtype, const double* 
                            int& part_dtype) {
   if (dtype == SPCP_F32 && !p->x32.ptr)
     return fail(SPCP_ERR_VALUE, "fp32 evaluation requested but no fp32 copy of X is stored");
-  if (p->sddmm && k <= 64) return sddmm_eval(p, k, dtype, z, dz, alpha, kp_used, sh, part_dtype);
+  if (p->sddmm && k <= 64 && (dtype == SPCP_F64 || p->sddmm32))
+    return sddmm_eval(p, k, dtype, z, dz, alpha, kp_used, sh, part_dtype);
   int kp = eval_kp(dtype, k);
   kp_used = kp;
   if (kp == 0) {
@@ -1191,7 +1185,8 @@ static int apply_impl(spcp_problem* p, int64_t k, const double* z, int64_t b,
   }
   for (int64_t c0 = 0; c0 < b; c0 += 32) {
     const int64_t bw = std::min<int64_t>(32, b - c0);
-    const int pw = bw <= 8 ? 8 : 32;
+    int pw = bw <= 8 ? 8 : (bw <= 16 ? 16 : 32);
+    if ((kr > 32 || kr < 0) && pw == 16) pw = 32;  // f64_stream_kernel / dense widths: 8, 32
     if (w_right) {
       if ((rc = p->wr.ensure(size_t(p->n_pad) * pw * sizeof(T)))) return rc;
       stage_cols_kernel<T><<<grid_for(p->n_pad * pw), 256, 0, p->stream>>>(
@@ -1264,10 +1259,17 @@ static int apply_impl(spcp_problem* p, int64_t k, const double* z, int64_t b,
 
 
 // Sparse-observation storage (sddmm.cuh): CSR + CSC of the observed entries,
-// values from the device copies of X.  Chosen at creation when the observed
-// fraction is at most SPCP_SDDMM_DENSITY (measured crossover against the dense
-// tensor-core pass, tools/sddmm_probe.py), or forced by SPCP_SDDMM=on|off.
-static constexpr double kSddmmDensity = 0.10;
+// values from the device copies of X.  Built at creation when the observed
+// fraction is at most SPCP_SDDMM_DENSITY, or forced by SPCP_SDDMM=on|off (or
+// the SPCP_STORE_SPARSE / SPCP_STORE_DENSE flags).  Measured crossovers against
+// the dense passes at the C4 shape (tools/sddmm_probe.py,
+// profiles/r02_sddmm_probe.txt): fp64 ~12% observed (the dense fp64 pass is
+// FP64-bound), fp32 ~2.5% (the tensor-core pass is ~0.69 ms whatever the mask;
+// the sparse passes are bound by the L2 gathers of the other factor's rows, one
+// 4k-byte row per observed entry per pass).  fp64 evaluations take the sparse
+// path whenever it is built, fp32 ones below kSddmmDensity32.
+static constexpr double kSddmmDensity = 0.12;
+static constexpr double kSddmmDensity32 = 0.025;
 
 static int build_sddmm(spcp_problem* p) {
   int rc;
@@ -1475,6 +1477,7 @@ int spcp_problem_create(spcp_problem** out, int device, int64_t m, int64_t n, co
     const bool force_off = (store & SPCP_STORE_DENSE) || mode == "off";
     if (force_on || (!force_off && density <= thr)) {
       if ((rc = build_sddmm(p))) return bail(rc);
+      p->sddmm32 = force_on || density <= kSddmmDensity32;
     }
   }
   for (int i = 0; i < spcp_problem::kEvRing; ++i) {

@@ -56,8 +56,9 @@ class DeviceProblem:
 
     x: host numpy array (float64 or float32) or a CUDA tensor, m x n.
     store: iterable of "f32" / "f64": which device copies to keep; "sparse" /
-      "dense" force the masked evaluation path (default: sparse when at most
-      10% of the entries are observed, sddmm.cuh).
+      "dense" force the masked evaluation path (default: the sparse copy is
+      built at <= 12% observed and used by fp64 evaluations, and by fp32 ones
+      below 2.5%, sddmm.cuh).
     n_total, col0: column-sharded mode.
     """
 

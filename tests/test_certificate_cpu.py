@@ -69,14 +69,16 @@ def test_rank_deficient_factor_qr(oracle):
 def test_power_bound_iterations():
     from paper_1702_02241_b200.certificate import _power_bound_iters
 
-    # 0.824 sqrt(n) (1 - eps)^(q - 3/2) <= fail * eps / 2 at the returned q
+    from paper_1702_02241_b200.certificate import _TIERS
+
+    # 0.824 sqrt(n) (1 - eps)^(q - 3/2) <= fail * eps / tiers at the returned q
     for n in (10, 1000, 20000, 200000):
-        for ome in (0.25, 0.5):
+        for ome, _ in _TIERS:
             q = _power_bound_iters(n, ome, 1e-6)
             eps = 1.0 - ome
-            assert 0.824 * np.sqrt(n) * ome ** (q - 1.5) <= 1e-6 * eps / 2
-    assert _power_bound_iters(20000, 0.25, 1e-6) == 16
-    assert _power_bound_iters(20000, 0.5, 1e-6) == 31
+            assert 0.824 * np.sqrt(n) * ome ** (q - 1.5) <= 1e-6 * eps / len(_TIERS)
+            assert 0.824 * np.sqrt(n) * ome ** (q - 2.5) > 1e-6 * eps / len(_TIERS)
+    assert [_power_bound_iters(20000, ome, 1e-6) for ome, _ in _TIERS] == [7, 9, 17, 32]
 
 
 def _free_port():
