@@ -239,6 +239,25 @@ def reference_c1_ttc(ref):
             "objective": rep.objective, "e_norm": cert.e_norm, "r": cert.r}
 
 
+def reference_c3_ttc(ref, ks=(3,)):
+    """The reference's time-to-certificate at C3 (110592 x 2000, lambda_L 30):
+    minutes of CPU, so only with --ref-c3."""
+    x, _, _ = ref.gen_low_rank_plus_sparse(110592, 2000, 3, 0.05, 1e-3, seed=0)
+    x = x.astype(np.float32).astype(np.float64)
+    spec = ref.ProblemSpec(x=x, lambda_l=30.0, lambda_s=0.1)
+    out = {}
+    for k in ks:
+        t0 = time.perf_counter()
+        rep = ref.solve_split_spcp(spec, k, ref.SolverConfig())
+        t1 = time.perf_counter()
+        cert = ref.certificate(rep.factors, spec, f_bound_hint=rep.best_objective)
+        t2 = time.perf_counter()
+        out[f"k{k}"] = {"seconds": t2 - t0, "solve_s": t1 - t0, "certificate_s": t2 - t1,
+                        "termination": rep.termination, "iterations": len(rep.iterations) - 1,
+                        "objective": rep.objective, "e_norm": cert.e_norm, "r": cert.r}
+    return out
+
+
 def run_reference(args, rank, world):
     """--impl reference: the unmodified reference on the box's host cores,
     rank 0 only.  One full C2 split_objective per step (the same X and
@@ -271,6 +290,7 @@ def run_reference(args, rank, world):
     per = float(np.mean(times))
     val = 1.0 / per
     ttc = reference_c1_ttc(ref) if ref is not None else None
+    ttc3 = reference_c3_ttc(ref) if (ref is not None and args.ref_c3) else None
     info = cpu_info()
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "evals/s",
@@ -282,7 +302,7 @@ def run_reference(args, rank, world):
                                    f"split_objective on the full C2 matrix ({M}x{N_COLS}, "
                                    f"float64 numpy/OpenBLAS, all host threads), one evaluation "
                                    f"per step, {args.steps} timed steps",
-                         "cpu": info, "ttc_c1": ttc},
+                         "cpu": info, "ttc_c1": ttc, "ttc_c3": ttc3},
         "e2e": {"value": val, "unit": "evals/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -345,6 +365,7 @@ def _time_evals(dp, step, steps, warmup, dist, stream):
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
+    dp.prof_read()  # reset the launch counter: gpu_launches counts the timed steps only
     dp.prof_enable(True)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -818,6 +839,8 @@ def main():
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-ttc", action="store_true")
     ap.add_argument("--skip-c5", action="store_true")
+    ap.add_argument("--ref-c3", action="store_true",
+                    help="reference arm: also time the reference's C3 solve + certificate")
     args, _ = ap.parse_known_args()
     if args.impl == "b200":
         args.warmup = max(args.warmup, 3)
