@@ -22,6 +22,7 @@
 #include "aux_kernels.cuh"
 #include "common.cuh"
 #include "sddmm.cuh"
+#include "stream_f64mma.cuh"
 #include "stream_f64.cuh"
 #include "stream_simt.cuh"
 #include "stream_tc.cuh"
@@ -273,11 +274,54 @@ static int launch_f64(spcp_problem* p, StreamParams sp, LaunchShape& shape) {
   return SPCP_OK;
 }
 
+// fp64 evaluation on the FP64 tensor cores (stream_f64mma.cuh; fp32-exact X)
+#ifndef SPCP_F64_MMA
+#define SPCP_F64_MMA 1
+#endif
+template <int KP, bool MASK>
+static int launch_f64mma(spcp_problem* p, StreamParams sp, LaunchShape& shape) {
+  using G = MmaGeom<KP>;
+  auto kern = f64_mma_kernel<KP, MASK>;
+  constexpr size_t smem = G::SMEM;
+  static DevFlags attr = {};
+  if (!attr[dev_slot(p->device)].load(std::memory_order_relaxed)) {
+    SPCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr[dev_slot(p->device)].store(1, std::memory_order_relaxed);
+  }
+  const int64_t nrb = p->m_pad / G::BM;
+  const int64_t ntiles = p->n_pad / G::BN;
+  // ~2 waves of one-CTA-per-SM blocks, chunks >= 4 tiles when possible
+  const int64_t target = int64_t(kSMs) * 2;
+  int64_t nch = ceil_div(target, nrb);
+  nch = std::max<int64_t>(1, std::min<int64_t>(nch, std::max<int64_t>(1, ntiles / 4)));
+  const int64_t tiles_per = ceil_div(ntiles, nch);
+  nch = ceil_div(ntiles, tiles_per);
+  sp.chunk_cols = tiles_per * G::BN;
+  sp.nchunks = int(nch);
+  shape.nchunks = int(nch);
+  shape.nrb = int(nrb);
+  shape.chunk_cols = sp.chunk_cols;
+  int rc;
+  if ((rc = p->pleft.ensure(size_t(nch) * p->m_pad * KP * sizeof(double)))) return rc;
+  if ((rc = p->pright.ensure(size_t(nrb) * p->n_pad * KP * sizeof(double)))) return rc;
+  if ((rc = p->pphi.ensure(size_t(nrb * nch) * sizeof(double)))) return rc;
+  sp.pleft = p->pleft.ptr;
+  sp.pright = p->pright.ptr;
+  sp.pphi = p->pphi.as<double>();
+  dim3 grid{unsigned(nch), unsigned(nrb), 1u};
+  if (p->prof && prof_begin(p)) return SPCP_ERR_CUDA;
+  kern<<<grid, G::NT, smem, p->stream>>>(sp);
+  SPCP_CHECK_LAUNCH("f64_mma_kernel");
+  if (p->prof && prof_end(p)) return SPCP_ERR_CUDA;
+  p->launches++;
+  return SPCP_OK;
+}
+
 // fused EVAL kernel widths
 #define SPCP_EVAL_F32_LIST(X) X(4) X(8) X(12) X(16) X(20) X(24) X(28) X(32) X(40) X(48) X(56) X(64)
 // fp64: the per-row SIMT stream_kernel up to k = 32 (measured faster there:
 // 4.15 vs 5.7 ms at C2), the register-blocked f64_stream_kernel above
-#define SPCP_EVAL_F64_LIST(X) X(4) X(8) X(12) X(16) X(20) X(24) X(28) X(32)
+#define SPCP_EVAL_F64_LIST(X) X(8) X(16) X(24) X(32)
 #define SPCP_EVAL_F64W_LIST(X) X(40) X(48) X(56) X(64)
 
 static int eval_kp(int dtype, int64_t k) {
@@ -285,10 +329,8 @@ static int eval_kp(int dtype, int64_t k) {
     static const int l[] = {4, 8, 12, 16, 20, 24, 28, 32, 40, 48, 56, 64};
     for (int v : l)
       if (k <= v) return v;
-  } else if (k <= 32) {
-    return int(round_up(k, 4));  // fp64 stream_kernel
   } else if (k <= 64) {
-    return int(round_up(k, 8));  // fp64 f64_stream_kernel
+    return int(round_up(k, 8));  // fp64: f64_mma_kernel / stream_kernel / f64_stream_kernel
   }
   return 0;  // beyond the fused kernels: dense fallback
 }
@@ -304,6 +346,16 @@ static int dispatch_eval(spcp_problem* p, int kp, StreamParams sp, LaunchShape& 
     switch (kp) { SPCP_EVAL_F32_LIST(SPCP_CASE) }
 #undef SPCP_CASE
   } else {
+    if constexpr (std::is_same<TX, float>::value) {
+      if (SPCP_F64_MMA) {  // fp32-exact X: the FP64 tensor-core pass
+#define SPCP_CASE(K) \
+  case K:            \
+    return launch_f64mma<K, MASK>(p, sp, sh);
+        switch (kp) { SPCP_CASE(8) SPCP_CASE(16) SPCP_CASE(24) SPCP_CASE(32) SPCP_CASE(40)
+                      SPCP_CASE(48) SPCP_CASE(56) SPCP_CASE(64) }
+#undef SPCP_CASE
+      }
+    }
 #define SPCP_CASE(K) \
   case K:            \
     return launch_stream<T, TX, K, K, MODE_EVAL, MASK>(p, sp, sh, prof);
