@@ -297,8 +297,11 @@ def certificate(l_factors, spec, f_bound_hint=None, rank_tol=1e-10):
     """Certify L = U V^T for the convex objective (certificate.py:77-141)."""
     import torch
 
+    from .device import nvtx_range
+
     m, n = spec.shape
     dp = spec.device("fp64")
     z = torch.from_numpy(np.ascontiguousarray(l_factors.flatten())).to(dp.device)
-    return certificate_core(dp, z, m, n, l_factors.k, spec.lambda_l, rank_tol, dp.f_zero,
-                            f_bound_hint, CertOps(n_total=n))
+    with nvtx_range("spcp.certificate"):
+        return certificate_core(dp, z, m, n, l_factors.k, spec.lambda_l, rank_tol, dp.f_zero,
+                                f_bound_hint, CertOps(n_total=n))

@@ -13,7 +13,7 @@ import numpy as np
 
 from ._lib import SPCP_F32, SPCP_F64, STORE_DENSE, STORE_F32, STORE_F64, STORE_SPARSE, check, lib
 
-__all__ = ["DeviceProblem", "torch_mod", "cuda_device", "dptr", "PRECISIONS"]
+__all__ = ["DeviceProblem", "torch_mod", "cuda_device", "dptr", "PRECISIONS", "nvtx_range"]
 
 PRECISIONS = ("fp32", "fp64", "mixed")
 
@@ -27,6 +27,27 @@ def torch_mod():
 
         _torch = torch
     return _torch
+
+
+class nvtx_range:
+    """NVTX range around a solver phase (rSVD init, L-BFGS, certificate), so
+    an nsys / ncu timeline of a solve shows where the time goes."""
+
+    def __init__(self, name):
+        self.name = name
+        self.on = False
+
+    def __enter__(self):
+        torch = torch_mod()
+        if torch.cuda.is_available():
+            torch.cuda.nvtx.range_push(self.name)
+            self.on = True
+        return self
+
+    def __exit__(self, *exc):
+        if self.on:
+            torch_mod().cuda.nvtx.range_pop()
+        return False
 
 
 def cuda_device():

@@ -58,12 +58,32 @@ def _dist():
     return dist
 
 
+class _Collective:
+    """Maps a failing collective (NCCL / gloo raise RuntimeError or
+    DistBackendError) to the package's DeviceError, a NumericalError subclass
+    like every CUDA failure of the C ABI (SURVEY §8(b) error conventions)."""
+
+    def __init__(self, what):
+        self.what = what
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, et, ev, tb):
+        if et is not None and issubclass(et, RuntimeError):
+            from .errors import DeviceError
+
+            raise DeviceError(f"collective {self.what} failed: {ev}") from ev
+        return False
+
+
 def allreduce_host(arr, device, group=None):
     """Sum a small host array across ranks (on `device` so NCCL can carry it)."""
     import torch
 
     t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(device)
-    _dist().all_reduce(t, group=group)
+    with _Collective("all_reduce(host array)"):
+        _dist().all_reduce(t, group=group)
     return t.cpu().numpy()
 
 
@@ -72,14 +92,16 @@ def allreduce_fused(tensors, group=None):
     NCCL group (torch's coalescing manager) when the backend is NCCL, plain
     calls otherwise (gloo on CPU tests)."""
     dist = _dist()
-    if dist.get_backend(group) == "nccl" and hasattr(dist, "_coalescing_manager"):
-        with dist._coalescing_manager(group=group, device=tensors[0].device, async_ops=True) as cm:
-            for t in tensors:
-                dist.all_reduce(t, group=group)
-        cm.wait()
-        return
-    for t in tensors:
-        dist.all_reduce(t, group=group)
+    with _Collective("all_reduce(evaluation)"):
+        if dist.get_backend(group) == "nccl" and hasattr(dist, "_coalescing_manager"):
+            with dist._coalescing_manager(group=group, device=tensors[0].device,
+                                          async_ops=True) as cm:
+                for t in tensors:
+                    dist.all_reduce(t, group=group)
+            cm.wait()
+            return
+        for t in tensors:
+            dist.all_reduce(t, group=group)
 
 
 class ShardedSpace:
@@ -134,7 +156,8 @@ class ShardedSpace:
 
         u_part = dev(ua, ub)
         v_part = dev(va, vb) if self.n > 0 else torch.zeros_like(u_part)
-        _dist().all_reduce(v_part, group=self.group)
+        with _Collective("all_reduce(dots)"):
+            _dist().all_reduce(v_part, group=self.group)
         return (u_part + v_part).cpu().numpy()
 
     def lincomb(self, coefs, vecs, out):
@@ -160,13 +183,15 @@ def _sharded_rsvd(dp, k, n_total, col0, oversample, power_iters, seed, group, co
         return allreduce_host(g, comm_device, group)
 
     y, _ = dp.apply(0, None, w_right=om)
-    dist.all_reduce(y, group=group)
+    with _Collective("all_reduce(rsvd sketch)"):
+        dist.all_reduce(y, group=group)
     q, _ = device_thin_qr(dp, y)
     for _ in range(int(power_iters)):
         _, zl = dp.apply(0, None, w_left=q)
         q2, _ = device_thin_qr(dp, zl, gram_reduce=red)
         y, _ = dp.apply(0, None, w_right=q2)
-        dist.all_reduce(y, group=group)
+        with _Collective("all_reduce(rsvd sketch)"):
+            dist.all_reduce(y, group=group)
         q, _ = device_thin_qr(dp, y)
     _, bt = dp.apply(0, None, w_left=q)  # (n_p x width) rows of B^T
     world = dist.get_world_size(group)
@@ -174,7 +199,8 @@ def _sharded_rsvd(dp, k, n_total, col0, oversample, power_iters, seed, group, co
     pad = torch.zeros((nmax, width), dtype=torch.float64, device=bt.device)
     pad[:n] = bt
     parts = [torch.empty_like(pad) for _ in range(world)]
-    dist.all_gather(parts, pad, group=group)
+    with _Collective("all_gather(rsvd core)"):
+        dist.all_gather(parts, pad, group=group)
     full = torch.cat([parts[r][: shard_bounds(n_total, world, r)[1]] for r in range(world)])
     inner = svd_small(full.cpu().numpy().T)
     u = dp.matmul_small(q, inner.u[:, :k])
@@ -261,7 +287,8 @@ def certificate_sharded(report, lambda_l=None, f_bound_hint=None, rank_tol=1e-10
         return allreduce_host(a, dp.device, group)
 
     def red_dev(t):
-        dist.all_reduce(t, group=group)
+        with _Collective("all_reduce(certificate product)"):
+            dist.all_reduce(t, group=group)
 
     ops = CertOps(host=red_host, dev=red_dev, n_total=ex["n_total"], col0=ex["col0"])
     f_zero = float(red_host(np.array([dp.f_zero]))[0])

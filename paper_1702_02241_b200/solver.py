@@ -297,7 +297,10 @@ def solve_split_spcp(spec, k, cfg=None, init="rsvd", iter_hook=None, timer=None,
     precision = _effective_precision(cfg.precision, spec.shape)
     make_space = space_factory or (lambda dpk, kk: _space_ops(SplitSpace(dpk, kk)))
     dp = spec.device(precision)
-    fp = init_factors(spec, k, strategy=init, seed=cfg.seed)
+    from .device import nvtx_range
+
+    with nvtx_range("spcp.init_factors"):
+        fp = init_factors(spec, k, strategy=init, seed=cfg.seed)
     z = torch.from_numpy(fp.flatten()).to(dp.device)
     cap = cfg.max_k if cfg.max_k is not None else min(m, n)
     records, n_evals, offset, grown = [], 0, 0, 0
@@ -318,7 +321,8 @@ def solve_split_spcp(spec, k, cfg=None, init="rsvd", iter_hook=None, timer=None,
                           max_iter=cfg.max_iter, c1=cfg.wolfe_c1, c2=cfg.wolfe_c2,
                           precision=precision, switch_tol=cfg.switch_tol, iter_hook=hook,
                           timer=timer)
-        res = eng.run(z)
+        with nvtx_range(f"spcp.lbfgs k={kk}"):
+            res = eng.run(z)
         n_evals += res.n_evals
         if eng.switched_at is not None:
             switches.append(offset + eng.switched_at)

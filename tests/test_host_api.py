@@ -110,3 +110,21 @@ def test_factor_svd_host():
     t = api.factor_svd(fp)
     np.testing.assert_allclose(t.sigma, [6.0], atol=1e-14)
     assert api.factor_svd(api.FactorPair(np.zeros((5, 2)), np.zeros((4, 2)))).rank == 0
+
+
+def test_collective_failure_maps_to_device_error(monkeypatch):
+    """A failing collective (NCCL/gloo RuntimeError) surfaces as DeviceError,
+    a NumericalError like every CUDA failure."""
+    import numpy as np
+    import torch.distributed as tdist
+
+    from paper_1702_02241_b200 import dist as pdist
+    from paper_1702_02241_b200.errors import DeviceError, NumericalError
+
+    def boom(*a, **k):
+        raise RuntimeError("NCCL error: unhandled system error")
+
+    monkeypatch.setattr(tdist, "all_reduce", boom)
+    with pytest.raises(DeviceError) as ei:
+        pdist.allreduce_host(np.zeros(3), "cpu")
+    assert isinstance(ei.value, NumericalError)
