@@ -185,6 +185,30 @@ static int prof_end(spcp_problem* p) {
   return SPCP_OK;
 }
 
+// Column chunks per row band for the (band x chunk) grids of the streaming
+// kernels: the smallest count whose last wave is nearly full (waste < 5% of
+// the resident slots) with at least `min_waves` waves and >= 2 tiles per
+// chunk.  (C2 in fp64: 157 bands; 2 chunks gave 2.12 waves of one-CTA-per-SM
+// blocks, a third wave 12% full.)
+static int64_t pick_chunks(int64_t nrb, int64_t ntiles, int per_sm, int min_waves) {
+  const int64_t slots = int64_t(kSMs) * std::max(per_sm, 1);
+  const int64_t cap = std::max<int64_t>(1, ntiles / 2);
+  int64_t best = std::min<int64_t>(cap, std::max<int64_t>(1, ceil_div(slots * min_waves, nrb)));
+  double best_waste = 1e9;
+  for (int64_t nch = best; nch <= std::min<int64_t>(cap, best + 64); ++nch) {
+    const int64_t per = ceil_div(ntiles, nch);
+    const int64_t real = ceil_div(ntiles, per);  // chunks actually launched
+    const int64_t u = real * nrb;
+    const double waste = double(ceil_div(u, slots) * slots) / double(u) - 1.0;
+    if (waste < best_waste - 1e-12) {
+      best_waste = waste;
+      best = nch;
+    }
+    if (waste < 0.05) break;
+  }
+  return best;
+}
+
 template <typename T, typename TX, int KR, int PW, int MODE, bool MASK>
 static int launch_stream(spcp_problem* p, StreamParams sp, LaunchShape& shape, bool prof) {
   using G = StreamGeom<T>;
@@ -201,10 +225,7 @@ static int launch_stream(spcp_problem* p, StreamParams sp, LaunchShape& shape, b
   }
   const int64_t nrb = p->m_pad / G::BM;
   const int64_t ntiles = p->n_pad / G::BN;
-  // enough CTAs for ~4 waves, but keep each chunk >= 4 tiles when possible
-  const int64_t target = int64_t(kSMs) * occ * 4;
-  int64_t nch = ceil_div(target, nrb);
-  nch = std::max<int64_t>(1, std::min<int64_t>(nch, std::max<int64_t>(1, ntiles / 4)));
+  int64_t nch = pick_chunks(nrb, ntiles, occ, 4);
   const int64_t tiles_per = ceil_div(ntiles, nch);
   nch = ceil_div(ntiles, tiles_per);
   sp.chunk_cols = tiles_per * G::BN;
@@ -246,11 +267,7 @@ static int launch_f64(spcp_problem* p, StreamParams sp, LaunchShape& shape) {
   }
   const int64_t nrb = p->m_pad / G::BM;
   const int64_t ntiles = p->n_pad / G::BN;
-  // ~2 waves of resident CTAs, each chunk >= 4 tiles when possible (the left
-  // product is flushed once per chunk)
-  const int64_t target = int64_t(kSMs) * occ * 2;
-  int64_t nch = ceil_div(target, nrb);
-  nch = std::max<int64_t>(1, std::min<int64_t>(nch, std::max<int64_t>(1, ntiles / 4)));
+  int64_t nch = pick_chunks(nrb, ntiles, occ, 2);
   const int64_t tiles_per = ceil_div(ntiles, nch);
   nch = ceil_div(ntiles, tiles_per);
   sp.chunk_cols = tiles_per * G::BN;
@@ -290,10 +307,7 @@ static int launch_f64mma(spcp_problem* p, StreamParams sp, LaunchShape& shape) {
   }
   const int64_t nrb = p->m_pad / G::BM;
   const int64_t ntiles = p->n_pad / G::BN;
-  // ~2 waves of one-CTA-per-SM blocks, chunks >= 4 tiles when possible
-  const int64_t target = int64_t(kSMs) * 2;
-  int64_t nch = ceil_div(target, nrb);
-  nch = std::max<int64_t>(1, std::min<int64_t>(nch, std::max<int64_t>(1, ntiles / 4)));
+  int64_t nch = pick_chunks(nrb, ntiles, 1, 2);
   const int64_t tiles_per = ceil_div(ntiles, nch);
   nch = ceil_div(ntiles, tiles_per);
   sp.chunk_cols = tiles_per * G::BN;
