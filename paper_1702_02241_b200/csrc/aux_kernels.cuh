@@ -565,6 +565,83 @@ __global__ void __launch_bounds__(256, 4) tc_reduce_kernel(const ReduceParams p,
   reduce_tail(p, s, scratch, am_last);
 }
 
+// Fold of the tensor-core partial slots, one block per output segment: a
+// 128-row sub-band of grad_U or a 64-row column tile of grad_V.  The
+// segment's CSR source list sits in shared memory; one thread per (row, 4
+// columns) item sums its sources in CSR order in fp64, batches of 8 loads in
+// flight (consecutive threads take consecutive rows of a chunk: coalesced).
+// Every item has one fixed summation order: bitwise reproducible.
+constexpr int kFoldMaxSrc = 64;
+__global__ void __launch_bounds__(256, 4) tc_fold_kernel(const ReduceParams p, int nsb) {
+  tc::pdl_wait();  // the fused pass's partial slots are complete
+  tc::pdl_launch_next();
+  __shared__ double scratch[6 * 32];
+  __shared__ bool am_last;
+  __shared__ int64_t src[2 * kFoldMaxSrc];  // element offsets of the segment's slots
+  double s[6] = {0, 0, 0, 0, 0, 0};
+  const int seg = blockIdx.x;
+  const bool is_u = seg < nsb;
+  const int tile = is_u ? seg : seg - nsb;
+  const int* off = is_u ? p.csr_u_off : p.csr_v_off;
+  const int* idxs = is_u ? p.csr_u_idx : p.csr_v_idx;
+  const int e0 = off[tile], ne = off[tile + 1] - e0;
+  const int slot_rows = is_u ? 128 : p.gt_rows;
+  const bool two = !is_u && p.gt_rows == 128;  // gh part + gl part rows: two sources
+  const int64_t sst = int64_t(slot_rows) * p.kst;
+  const int nsrc = two ? 2 * ne : ne;
+  for (int i = threadIdx.x; i < nsrc; i += blockDim.x)
+    src[i] = two ? int64_t(idxs[e0 + (i >> 1)]) * sst + (i & 1) * 64 * 4
+                 : int64_t(idxs[e0 + i]) * sst;
+  __syncthreads();
+  const int tile_rows = is_u ? 128 : 64;
+  const int64_t rows_total = is_u ? p.m : p.n;
+  const int64_t r_base = int64_t(tile) * tile_rows;
+  const int c4n = p.kst >> 2;
+  const float* part = reinterpret_cast<const float*>(is_u ? p.pleft : p.pright);
+  const double sc = double(p.tc_unscale[is_u ? 0 : 1]);
+  for (int it = threadIdx.x; it < tile_rows * c4n; it += blockDim.x) {
+    const int chunk = it / tile_rows, rr = it - chunk * tile_rows;
+    const int64_t r = r_base + rr;
+    if (r >= rows_total) continue;
+    const float* base = part + (int64_t(chunk) * slot_rows + rr) * 4;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (int eb = 0; eb < nsrc; eb += 8) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        v[u] = eb + u < nsrc ? *reinterpret_cast<const float4*>(base + src[eb + u])
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        a0 += v[u].x; a1 += v[u].y; a2 += v[u].z; a3 += v[u].w;
+      }
+    }
+    const double acc[4] = {a0 * sc, a1 * sc, a2 * sc, a3 * sc};
+    const int c0 = chunk * 4;
+    const int64_t obase = (is_u ? 0 : p.m * p.k) + r * p.k;
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int c = c0 + jj;
+      if (c >= p.k) break;
+      const int64_t o = obase + c;
+      if (is_u && p.u_mode == U_PARTIAL) {
+        reinterpret_cast<float*>(p.gu_part)[r * p.k + c] = float(acc[jj]);
+        continue;
+      }
+      double wv = p.z[o];
+      const double d = p.dz ? p.dz[o] : 0.0;
+      wv += p.alpha * d;
+      const double g = acc[jj] + p.lambda_l * wv;
+      p.g_out[o] = g;
+      const int sidx = is_u ? 0 : 3;
+      s[sidx] += g * g;
+      s[sidx + 1] += g * d;
+      s[sidx + 2] += wv * wv;
+    }
+  }
+  reduce_tail(p, s, scratch, am_last);
+}
+
 // Reduce apply() partials to float64 outputs (rows x b, b <= bp).
 template <typename T>
 __global__ void reduce_apply_kernel(const T* __restrict__ part, int nparts, int64_t rows,

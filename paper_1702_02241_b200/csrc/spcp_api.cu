@@ -1153,7 +1153,19 @@ static int run_reduce(spcp_problem* p, int64_t k, int kp, int part_dtype, const 
     rp.chunked = sh.chunked;
     rp.tc_unscale = &p->tc_scales.as<TcScales>()->gv_unscale;
   }
-  if (sh.tc && (u_mode == U_FULL || u_mode == U_PARTIAL) && v_mode) {
+  // SPCP_TC_FOLD=1: one block per sub-band / column tile (tc_fold_kernel).
+  // Measured same-box against the LPI kernel: C2 step 0.412 vs 0.415 ms, C4
+  // 0.678 vs 0.701, C3 (k = 5) 0.223 vs 0.213, C1 0.034 vs 0.032 — a wash, so
+  // the LPI kernel stays the default.
+  static const bool fold_env = env_str("SPCP_TC_FOLD") == "1";
+  if (sh.tc && sh.chunked && (u_mode == U_FULL || u_mode == U_PARTIAL) && v_mode && fold_env &&
+      p->tc_max_u_src <= kFoldMaxSrc && p->tc_max_v_src <= kFoldMaxSrc) {
+    // one block per sub-band / column tile (tc_fold_kernel)
+    const int nb = int(p->tc_nsb + p->tc_ntc);
+    if ((rc = p->blk.ensure(size_t(nb) * 6 * sizeof(double)))) return rc;
+    rp.blk = p->blk.as<double>();
+    SPCP_CUDA(launch_pdl(tc_fold_kernel, dim3(nb), dim3(256), 0, p->stream, rp, int(p->tc_nsb)));
+  } else if (sh.tc && (u_mode == U_FULL || u_mode == U_PARTIAL) && v_mode) {
 // lanes per output item from the largest source count of each side:
     // about four partial loads per lane, a power of two in [1, 32]
     auto lanes = [](int64_t loads) {
