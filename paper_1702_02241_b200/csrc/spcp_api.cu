@@ -139,9 +139,10 @@ struct spcp_problem {
   int tc_grid = 0, tc_runs = 0, tc_slots = 0;
   int64_t tc_nsb = 0, tc_ntc = 0;
   CUtensorMap tc_xmap, tc_mmap;
-  spcp::DevBuf tc_units, tc_begin, tc_csr, tc_uimg, tc_vimg, tc_scales;
+  spcp::DevBuf tc_units, tc_begin, tc_csr, tc_uimg, tc_vimg, tc_scales, tc_bmax;
   int64_t tc_csr_u_off = 0, tc_csr_u_idx = 0, tc_csr_v_off = 0, tc_csr_v_idx = 0;
   int64_t tc_max_u_src = 0, tc_max_v_src = 0;  // largest CSR source lists (reduce sizing)
+  int tc_nbmax = 0;                             // blocks of the last tc_max launch
   // sparse-observation path (sddmm.cuh): observed entries in CSR and CSC
   bool sddmm = false, sddmm32 = false;  // built; used by fp32 evaluations too
   int64_t nnz = 0;
@@ -390,6 +391,12 @@ static int apply_kr(int64_t k) {
   if (k <= 32) return int(round_up(k, 8));
   return -1;
 }
+// fp32 products (the certificate's subspace iteration): k <= 64
+static int apply_kr32(int64_t k) {
+  if (k <= 32) return apply_kr(k);
+  if (k <= 64) return int(round_up(k, 16));
+  return -1;
+}
 static int apply_kr64(int64_t k) {
   if (k <= 32) return apply_kr(k);
   if (k <= 64) return int(round_up(k, 16));
@@ -409,6 +416,14 @@ static int dispatch_apply(spcp_problem* p, int kr, int pw, StreamParams sp, Laun
     return KR == 0 ? launch_stream<T, TX, 0, PW, MODE_RAW, MASK>(p, sp, sh, false) \
                    : launch_stream<T, TX, KR, PW, MODE_APPLY, MASK>(p, sp, sh, false);
   SPCP_AP_LIST(SPCP_AP)
+  if constexpr (sizeof(T) == 4) {  // wide ranks for the fp32 certificate products
+    SPCP_AP(48, 8)
+    SPCP_AP(48, 16)
+    SPCP_AP(48, 32)
+    SPCP_AP(64, 8)
+    SPCP_AP(64, 16)
+    SPCP_AP(64, 32)
+  }
 #undef SPCP_AP
   if constexpr (sizeof(T) == 8) {
 #define SPCP_AP(KR, PW)            \
@@ -635,6 +650,7 @@ static int tc_build(spcp_problem* p) {
   if ((rc = p->tc_csr.ensure(csr.size() * sizeof(int32_t)))) return rc;
   if ((rc = p->tc_scales.ensure(sizeof(TcScales)))) return rc;
   SPCP_CUDA(cudaMemset(p->tc_scales.ptr, 0, sizeof(TcScales)));
+  if ((rc = p->tc_bmax.ensure(2 * kTcMaxBlocks * sizeof(unsigned long long)))) return rc;
   SPCP_CUDA(cudaMemcpy(p->tc_units.ptr, units.data(), units.size() * sizeof(TcUnit),
                        cudaMemcpyHostToDevice));
   SPCP_CUDA(cudaMemcpy(p->tc_begin.ptr, begin.data(), begin.size() * sizeof(int32_t),
@@ -694,7 +710,8 @@ static int tc_images(spcp_problem* p, int64_t k, const double* z, const double* 
   const int64_t total = (p->m_pad + p->n_pad) * KP16;
   tc_images_kernel<KP16><<<grid_for(total), 256, 0, p->stream>>>(
       z, dz, alpha, p->m, p->n, k, p->m_pad, p->n_pad, p->tc_scales.as<TcScales>(),
-      p->lambda_s, p->tc_uimg.as<unsigned char>(), p->tc_vimg.as<unsigned char>());
+      p->lambda_s, p->tc_uimg.as<unsigned char>(), p->tc_vimg.as<unsigned char>(),
+      p->tc_bmax.as<unsigned long long>(), p->tc_nbmax);
   SPCP_CHECK_LAUNCH("tc_images");
   p->launches++;
   return SPCP_OK;
@@ -711,7 +728,8 @@ static int tc_images_kc(spcp_problem* p, int64_t k, const double* z, const doubl
   SPCP_CUDA(launch_pdl(tc_images_kc_kernel<SEG>, dim3(grid_for(total)), dim3(256), 0, p->stream,
                        z, dz, alpha, p->m, p->n, k, p->m_pad, p->n_pad,
                        p->tc_scales.as<TcScales>(), p->lambda_s, p->tc_uimg.as<unsigned char>(),
-                       p->tc_vimg.as<unsigned char>()));
+                       p->tc_vimg.as<unsigned char>(), p->tc_bmax.as<unsigned long long>(),
+                       p->tc_nbmax));
   SPCP_CHECK_LAUNCH("tc_images_kc");
   p->launches++;
   return SPCP_OK;
@@ -786,10 +804,10 @@ static int tc_eval(spcp_problem* p, int64_t k, const double* z, const double* dz
       default: rc = fail(SPCP_ERR_UNSUPPORTED, "no K-concatenated image kernel");
     }
 #else
-    TcScales* sc = p->tc_scales.as<TcScales>();
     const int64_t nu = p->m * k, nv = p->n * k;
-    SPCP_CUDA(launch_pdl(tc_max_kernel, dim3(grid_for(nu + nv, 256, 148 * 4)), dim3(256), 0,
-                         p->stream, z, dz, alpha, nu, nv, sc));
+    p->tc_nbmax = int(grid_for(nu + nv, 1024, kTcMaxBlocks));
+    SPCP_CUDA(launch_pdl(tc_max_kernel, dim3(p->tc_nbmax), dim3(256), 0, p->stream, z, dz, alpha,
+                         nu, nv, p->tc_bmax.as<unsigned long long>()));
     SPCP_CHECK_LAUNCH("tc_max");
     p->launches += 1;
     switch (int(round_up(k, 4))) {
@@ -820,9 +838,10 @@ static int tc_eval(spcp_problem* p, int64_t k, const double* z, const double* dz
   const int kp16 = k <= 16 ? 16 : (k <= 32 ? 32 : 64);
   // operand scales (max |U|, |V| of the trial point -> powers of two)
   // the maxima are zero here: zeroed at build time and reset by every fused launch
-  TcScales* sc = p->tc_scales.as<TcScales>();
   const int64_t nu = p->m * k, nv = p->n * k;
-  tc_max_kernel<<<grid_for(nu + nv, 256, 148 * 4), 256, 0, p->stream>>>(z, dz, alpha, nu, nv, sc);
+  p->tc_nbmax = int(grid_for(nu + nv, 1024, kTcMaxBlocks));
+  tc_max_kernel<<<p->tc_nbmax, 256, 0, p->stream>>>(z, dz, alpha, nu, nv,
+                                                    p->tc_bmax.as<unsigned long long>());
   SPCP_CHECK_LAUNCH("tc_max");
   p->launches += 1;
   rc = kp16 == 16 ? tc_images<16>(p, k, z, dz, alpha)
@@ -1244,7 +1263,7 @@ static int apply_impl(spcp_problem* p, int64_t k, const double* z, int64_t b,
   if (k < 0 || b < 1) return fail(SPCP_ERR_DIMENSION, "bad apply shape");
   SPCP_CUDA(cudaSetDevice(p->device));
   const bool x64 = p->x64.ptr != nullptr;
-  int kr = std::is_same<T, float>::value ? apply_kr(k) : apply_kr64(k);
+  int kr = std::is_same<T, float>::value ? apply_kr32(k) : apply_kr64(k);
   // residual operands (T)
   if (kr > 0) {
     if ((rc = prep<T>(p, k, kr, z, nullptr, 0.0))) return rc;
@@ -1264,7 +1283,8 @@ static int apply_impl(spcp_problem* p, int64_t k, const double* z, int64_t b,
   for (int64_t c0 = 0; c0 < b; c0 += 32) {
     const int64_t bw = std::min<int64_t>(32, b - c0);
     int pw = bw <= 8 ? 8 : (bw <= 16 ? 16 : 32);
-    if ((kr > 32 || kr < 0) && pw == 16) pw = 32;  // f64_stream_kernel / dense widths: 8, 32
+    if ((kr < 0 || (kr > 32 && sizeof(T) == 8)) && pw == 16)
+      pw = 32;  // f64_stream_kernel / dense widths: 8, 32
     if (w_right) {
       if ((rc = p->wr.ensure(size_t(p->n_pad) * pw * sizeof(T)))) return rc;
       stage_cols_kernel<T><<<grid_for(p->n_pad * pw), 256, 0, p->stream>>>(
@@ -1575,7 +1595,7 @@ int spcp_problem_destroy(spcp_problem* p) {
                     &p->scal, &p->gu_tmp, &p->vec_part, &p->small, &p->csr_ptr, &p->csr_idx,
                     &p->csr_v32, &p->csr_v64, &p->csc_ptr, &p->csc_idx, &p->csc_v32,
                     &p->csc_v64, &p->tc_units, &p->tc_begin, &p->tc_csr, &p->tc_uimg,
-                    &p->tc_vimg, &p->tc_scales})
+                    &p->tc_vimg, &p->tc_scales, &p->tc_bmax})
     b->release();
   if (p->host_out) cudaFreeHost(p->host_out);
   for (int i = 0; i < spcp_problem::kEvRing; ++i) {
@@ -1750,7 +1770,7 @@ int spcp_apply_f32(spcp_problem* p, int64_t k, const double* z, int64_t b,
                    double* right_out) {
   if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
   // fp32 streaming products need the fp32 copy of X and the fused widths
-  if (!p->x32.ptr || apply_kr(k) < 0)  // fp64 kernels cover k <= 64
+  if (!p->x32.ptr || apply_kr32(k) < 0)
     return apply_impl<double>(p, k, z, b, w_right, left_out, w_left, right_out);
   return apply_impl<float>(p, k, z, b, w_right, left_out, w_left, right_out);
 }

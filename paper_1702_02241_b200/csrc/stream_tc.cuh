@@ -973,8 +973,14 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK, SEG>::NTHREADS, 1)
 // ------------------------------------------------------------------ prep
 // pass 1: max |w| over the U and V parts of the trial point (bit patterns of
 // non-negative doubles order like unsigned integers).
-__global__ void tc_max_kernel(const double* __restrict__ z, const double* __restrict__ dz,
-                              double alpha, int64_t nu, int64_t nv, TcScales* sc) {
+// Per-block maxima go to bmax[2 b], bmax[2 b + 1] (plain stores: hundreds of
+// blocks hitting two addresses with atomicMax serialised in L2 and cost more
+// than the loads); the image pass folds them.
+constexpr int kTcMaxBlocks = 296;
+__global__ void __launch_bounds__(256) tc_max_kernel(const double* __restrict__ z,
+                                                     const double* __restrict__ dz, double alpha,
+                                                     int64_t nu, int64_t nv,
+                                                     unsigned long long* bmax) {
   tc::pdl_wait();
   tc::pdl_launch_next();
   unsigned long long mu = 0, mv = 0;
@@ -1008,17 +1014,54 @@ __global__ void tc_max_kernel(const double* __restrict__ z, const double* __rest
     mu = a > mu ? a : mu;
     mv = b > mv ? b : mv;
   }
+  __shared__ unsigned long long wm[2][8];
+  const int w = threadIdx.x >> 5;
   if ((threadIdx.x & 31) == 0) {
-    atomicMax(&sc->max_bits[0], mu);
-    atomicMax(&sc->max_bits[1], mv);
+    wm[0][w] = mu;
+    wm[1][w] = mv;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    unsigned long long m = 0ull;
+    for (int i = 0; i < int(blockDim.x >> 5); ++i) m = wm[threadIdx.x][i] > m ? wm[threadIdx.x][i] : m;
+    bmax[2 * blockIdx.x + threadIdx.x] = m;
   }
 }
 
+// fold of tc_max_kernel's per-block maxima, done by every block of the image
+// pass (2 x nblk loads, L2-resident); result in all threads
+__device__ __forceinline__ void tc_fold_max(const unsigned long long* __restrict__ bmax, int nblk,
+                                            double& mu, double& mv) {
+  __shared__ unsigned long long red[2][8];
+  unsigned long long a = 0ull, b = 0ull;
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
+    const unsigned long long x = __ldcg(bmax + 2 * i), y = __ldcg(bmax + 2 * i + 1);
+    a = x > a ? x : a;
+    b = y > b ? y : b;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long x = __shfl_xor_sync(0xffffffffu, a, o);
+    const unsigned long long y = __shfl_xor_sync(0xffffffffu, b, o);
+    a = x > a ? x : a;
+    b = y > b ? y : b;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = a;
+    red[1][threadIdx.x >> 5] = b;
+  }
+  __syncthreads();
+  a = b = 0ull;
+  for (int i = 0; i < int(blockDim.x >> 5); ++i) {
+    a = red[0][i] > a ? red[0][i] : a;
+    b = red[1][i] > b ? red[1][i] : b;
+  }
+  mu = __longlong_as_double(a);
+  mv = __longlong_as_double(b);
+}
+
 // pass 2 (folded into the image pass): power-of-two scales from the maxima
-__device__ __forceinline__ TcScales tc_compute_scales(const TcScales* sc, double tau) {
-  // L2 reads (the maxima were just produced by atomics of other blocks)
-  const double mu = __longlong_as_double(__ldcg(&sc->max_bits[0]));
-  const double mv = __longlong_as_double(__ldcg(&sc->max_bits[1]));
+__device__ __forceinline__ TcScales tc_compute_scales(double mu, double mv, double tau) {
   auto pow2_for = [](double mx) {  // largest 2^e with mx * 2^e <= 2^14
     if (!(mx > 0.0)) return 1.0;
     int e;
@@ -1058,9 +1101,11 @@ template <int KP16>
 __global__ void tc_images_kernel(const double* __restrict__ z, const double* __restrict__ dz,
                                  double alpha, int64_t m, int64_t n, int64_t k, int64_t m_pad,
                                  int64_t n_pad, TcScales* sc, double tau, unsigned char* u_img,
-                                 unsigned char* v_img) {
+                                 unsigned char* v_img, const unsigned long long* bmax, int nbmax) {
   constexpr int RB = KP16 * 2;
-  const TcScales scl = tc_compute_scales(sc, tau);  // every block: same maxima, same scales
+  double mu, mv;
+  tc_fold_max(bmax, nbmax, mu, mv);
+  const TcScales scl = tc_compute_scales(mu, mv, tau);  // every block: same maxima, same scales
   const double su = scl.su, sv = scl.sv;
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // publish for the fused kernel and the reduce
     sc->su = scl.su;
@@ -1108,10 +1153,11 @@ __device__ __forceinline__ void tc_images_kc_body(const double* __restrict__ z,
                                                   const double* __restrict__ dz, double alpha,
                                                   int64_t m, int64_t n, int64_t k, int64_t m_pad,
                                                   int64_t n_pad, TcScales* sc, double tau,
-                                                  unsigned char* u_img, unsigned char* v_img) {
+                                                  unsigned char* u_img, unsigned char* v_img,
+                                                  double mu, double mv) {
   using C = TcCfg<16, false, SEG>;
   constexpr int RB = C::RB, EPA = RB / 2, NE = C::NA * EPA;  // entries per atom / per row
-  const TcScales scl = tc_compute_scales(sc, tau);
+  const TcScales scl = tc_compute_scales(mu, mv, tau);
   const double su = scl.su, sv = scl.sv;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     sc->su = scl.su;
@@ -1159,10 +1205,13 @@ template <int SEG>
 __global__ void tc_images_kc_kernel(const double* __restrict__ z, const double* __restrict__ dz,
                                     double alpha, int64_t m, int64_t n, int64_t k, int64_t m_pad,
                                     int64_t n_pad, TcScales* sc, double tau, unsigned char* u_img,
-                                    unsigned char* v_img) {
+                                    unsigned char* v_img, const unsigned long long* bmax,
+                                    int nbmax) {
   tc::pdl_wait();
   tc::pdl_launch_next();
-  tc_images_kc_body<SEG>(z, dz, alpha, m, n, k, m_pad, n_pad, sc, tau, u_img, v_img);
+  double mu, mv;
+  tc_fold_max(bmax, nbmax, mu, mv);
+  tc_images_kc_body<SEG>(z, dz, alpha, m, n, k, m_pad, n_pad, sc, tau, u_img, v_img, mu, mv);
 }
 
 // Grid-wide barrier for a kernel whose blocks are all resident (grid sized
@@ -1234,7 +1283,10 @@ __global__ void __launch_bounds__(256) tc_prep_kc_kernel(
   }
   grid_barrier(bar_count, bar_gen, gridDim.x);
   tc::pdl_launch_next();
-  tc_images_kc_body<SEG>(z, dz, alpha, m, n, k, m_pad, n_pad, sc, tau, u_img, v_img);
+  // L2 reads (the maxima were just produced by atomics of other blocks)
+  const double mu = __longlong_as_double(__ldcg(&sc->max_bits[0]));
+  const double mv = __longlong_as_double(__ldcg(&sc->max_bits[1]));
+  tc_images_kc_body<SEG>(z, dz, alpha, m, n, k, m_pad, n_pad, sc, tau, u_img, v_img, mu, mv);
 }
 
 }  // namespace spcp

@@ -139,7 +139,7 @@ def test_certificate_fp32_products_route(api):
     x, _, _ = orc.gen_low_rank_plus_sparse(m, n, 8, 0.05, 1e-3, seed=4)
     x = x.astype(np.float32).astype(np.float64)
     spec = api.ProblemSpec(x=x, lambda_l=0.3 * np.sqrt(n), lambda_s=0.1)
-    for k in (4, 8):
+    for k in (4, 8, 36):  # 36: the wide-rank (48) fp32 apply kernels
         rep = api.solve_split_spcp(spec, k, api.SolverConfig(max_iter=80))
         c32 = api.certificate(rep.factors, spec, f_bound_hint=rep.best_objective)
         assert c32.info["products"] == "fp32"
