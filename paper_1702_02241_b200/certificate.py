@@ -173,13 +173,19 @@ def _power_bound_iters(dim, one_minus_eps, fail):
     return int(math.ceil(k)) + 1
 
 
-def _subspace_sigmas(op, n_total, m, r, block=16, max_iter=400, tol=None, seed=0):
+# starting block of the subspace iteration (grows while its smallest Ritz
+# value is >= 1, i.e. while it may miss a singular value above 1)
+SUBSPACE_BLOCK = 8
+
+
+def _subspace_sigmas(op, n_total, m, r, block=None, max_iter=400, tol=None, seed=0):
     """Top singular values of P by randomized block subspace iteration with
     Rayleigh-Ritz; the block doubles until its smallest Ritz value < 1.
     Returns (sigmas, info)."""
     import torch
 
     dp, ops = op.dp, op.ops
+    block = SUBSPACE_BLOCK if block is None else block
     tol = _SUBSPACE_TOL[op.precision] if tol is None else tol
     cap = max(1, min(m, n_total) - r)
     b = min(block, cap)

@@ -9,6 +9,10 @@ sys.path.insert(0, ".")
 from paper_1702_02241_b200 import ProblemSpec, SolverConfig, certificate, solve_split_spcp  # noqa
 from paper_1702_02241_b200.synth import gen_low_rank_plus_sparse_device  # noqa
 
+if len(sys.argv) > 1:  # starting block of the certificate's subspace iteration
+    import importlib
+
+    importlib.import_module("paper_1702_02241_b200.certificate").SUBSPACE_BLOCK = int(sys.argv[1])
 x = gen_low_rank_plus_sparse_device(20000, 20000, 20, 0.05, 1e-3, seed=0)
 spec = ProblemSpec(x=x, lambda_l=40.0, lambda_s=0.1)
 spec.device("mixed")
