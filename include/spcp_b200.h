@@ -183,6 +183,22 @@ int spcp_materialize(spcp_problem* p, int64_t k, const double* z, int64_t row0,
 int spcp_materialize_grad(spcp_problem* p, int64_t k, const double* z, double* g_out,
                           int64_t ldo);
 
+/* ---- line-restricted evaluation (the probes of one line search, lbfgs.py:64-99)
+ * On the ray z + a dz the residual is quadratic in a: R(a) = R0 - a D1 - a^2 D2
+ * on Omega with R0 = X - U V^T, D1 = dU V^T + U dV^T, D2 = dU dV^T.
+ * spcp_line_setup stores the three m x n float64 matrices (24 bytes per entry
+ * of device memory; SPCP_ERR_UNSUPPORTED when they do not fit or X is held
+ * only as sparse observations — the caller then keeps probing with
+ * spcp_eval).  spcp_line_probe(a) returns out_host[8] = [F, phi, reg,
+ * grad F . dz, 0, 0, 0, 0] at z + a dz (float64, fixed-order sums) from one
+ * pass over the stored matrices, without the gradient; spcp_line_release
+ * frees them.  Replaces the per-probe fun(x) calls of the reference's
+ * strong-Wolfe search (spcp/lbfgs.py:64-99) for the probes that are not
+ * accepted; the accepted point is re-evaluated with spcp_eval. */
+int spcp_line_setup(spcp_problem* p, int64_t k, const double* z, const double* dz);
+int spcp_line_probe(spcp_problem* p, double alpha, double* out_host);
+int spcp_line_release(spcp_problem* p);
+
 /* ---- L-BFGS vector algebra (lbfgs.py:152-188, compact form) -----------------
  * All device float64, length len.  Deterministic (fixed-order) reductions.
  * multidot: out_host[i] = <a[i], b[i]> for i < count (a, b: host arrays of

@@ -21,6 +21,7 @@
 
 #include "aux_kernels.cuh"
 #include "common.cuh"
+#include "line.cuh"
 #include "sddmm.cuh"
 #include "stream_f64mma.cuh"
 #include "stream_f64.cuh"
@@ -147,6 +148,10 @@ struct spcp_problem {
   bool sddmm = false, sddmm32 = false;  // built; used by fp32 evaluations too
   int64_t nnz = 0;
   spcp::DevBuf csr_ptr, csr_idx, csr_v32, csr_v64, csc_ptr, csc_idx, csc_v32, csc_v64;
+  // line-restricted evaluation (line.cuh): R0, D1, D2 of one ray
+  spcp::DevBuf line_ws, line_part;
+  bool line_ready = false;
+  double line_zz = 0.0, line_zd = 0.0, line_dd = 0.0;
 };
 
 namespace spcp {
@@ -1595,7 +1600,7 @@ int spcp_problem_destroy(spcp_problem* p) {
                     &p->scal, &p->gu_tmp, &p->vec_part, &p->small, &p->csr_ptr, &p->csr_idx,
                     &p->csr_v32, &p->csr_v64, &p->csc_ptr, &p->csc_idx, &p->csc_v32,
                     &p->csc_v64, &p->tc_units, &p->tc_begin, &p->tc_csr, &p->tc_uimg,
-                    &p->tc_vimg, &p->tc_scales, &p->tc_bmax})
+                    &p->tc_vimg, &p->tc_scales, &p->tc_bmax, &p->line_ws, &p->line_part})
     b->release();
   if (p->host_out) cudaFreeHost(p->host_out);
   for (int i = 0; i < spcp_problem::kEvRing; ++i) {
@@ -1825,6 +1830,94 @@ int spcp_materialize_grad(spcp_problem* p, int64_t k, const double* z, double* g
                                         p->pphi.as<double>());
   if (rc) return rc;
   SPCP_CUDA(cudaStreamSynchronize(p->stream));
+  return SPCP_OK;
+}
+
+// ---- line-restricted evaluation (line.cuh) ----------------------------------
+int spcp_line_setup(spcp_problem* p, int64_t k, const double* z, const double* dz) {
+  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
+  if (k < 1) return fail(SPCP_ERR_DIMENSION, "k must be >= 1");
+  if (!z || !dz) return fail(SPCP_ERR_VALUE, "line_setup needs z and dz");
+  int rc;
+  SPCP_CUDA(cudaSetDevice(p->device));
+  p->line_ready = false;
+  if (!p->x64.ptr && !p->x32.ptr)
+    return fail(SPCP_ERR_UNSUPPORTED, "line_setup: no dense X store (sparse-observation problem)");
+  const size_t per = size_t(p->m) * size_t(p->n);
+  const size_t ld = size_t(round_up(int64_t(per), 32));  // 256-byte aligned matrices
+  const size_t need = 3 * ld * sizeof(double);
+  if (p->line_ws.bytes < need) {
+    p->line_ws.release();
+    size_t free_b = 0, total_b = 0;
+    SPCP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    if (need + (size_t(1) << 30) > free_b)
+      return fail(SPCP_ERR_UNSUPPORTED, "line_setup: the three m x n float64 matrices do not fit");
+    if ((rc = p->line_ws.ensure(need))) return rc;
+  }
+  double* r0 = p->line_ws.as<double>();
+  dim3 grid(unsigned(ceil_div(p->n, 64)), unsigned(ceil_div(p->m, 64)));
+  const uint32_t* mb = p->masked ? p->mbits.as<uint32_t>() : nullptr;
+  if (p->x64.ptr)
+    line_setup_kernel<double><<<grid, 256, 0, p->stream>>>(z, dz, p->m, p->n, k,
+                                                           p->x64.as<double>(), p->ldx, mb, p->ldm,
+                                                           r0, r0 + ld, r0 + 2 * ld);
+  else
+    line_setup_kernel<float><<<grid, 256, 0, p->stream>>>(z, dz, p->m, p->n, k,
+                                                          p->x32.as<float>(), p->ldx, mb, p->ldm,
+                                                          r0, r0 + ld, r0 + 2 * ld);
+  SPCP_CHECK_LAUNCH("line_setup");
+  p->launches++;
+  // regulariser on the ray: |z + a dz|^2 = zz + 2 a zd + a^2 dd
+  const int64_t len = (p->m + p->n) * k;
+  const double* a[3] = {z, z, dz};
+  const double* b[3] = {z, dz, dz};
+  double dots[3];
+  if ((rc = spcp_vec_multidot(p, len, 3, a, b, dots))) return rc;
+  p->line_zz = dots[0];
+  p->line_zd = dots[1];
+  p->line_dd = dots[2];
+  p->line_ready = true;
+  return SPCP_OK;
+}
+
+int spcp_line_probe(spcp_problem* p, double alpha, double* out_host) {
+  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
+  if (!p->line_ready) return fail(SPCP_ERR_VALUE, "line_probe before line_setup");
+  int rc;
+  SPCP_CUDA(cudaSetDevice(p->device));
+  if ((rc = ensure_common(p))) return rc;
+  const int nb = kSMs * 4;
+  if ((rc = p->line_part.ensure(size_t(2 * nb) * sizeof(double)))) return rc;
+  const size_t per = size_t(p->m) * size_t(p->n);
+  const size_t ld = size_t(round_up(int64_t(per), 32));
+  const double* r0 = p->line_ws.as<double>();
+  line_probe_kernel<<<nb, 256, 0, p->stream>>>(r0, r0 + ld, r0 + 2 * ld, int64_t(per), alpha,
+                                               p->lambda_s, p->line_part.as<double>());
+  SPCP_CHECK_LAUNCH("line_probe");
+  line_fold_kernel<<<1, 256, 0, p->stream>>>(p->line_part.as<double>(), nb,
+                                             p->out_dev.as<double>());
+  SPCP_CHECK_LAUNCH("line_fold");
+  p->launches += 2;
+  SPCP_CUDA(cudaMemcpyAsync(p->host_out, p->out_dev.ptr, 2 * sizeof(double),
+                            cudaMemcpyDeviceToHost, p->stream));
+  SPCP_CUDA(cudaStreamSynchronize(p->stream));
+  const double phi = p->host_out[0], dphi = p->host_out[1];
+  const double reg = 0.5 * p->lambda_l * (p->line_zz + alpha * (2.0 * p->line_zd + alpha * p->line_dd));
+  const double dreg = p->lambda_l * (p->line_zd + alpha * p->line_dd);
+  out_host[0] = phi + reg;
+  out_host[1] = phi;
+  out_host[2] = reg;
+  out_host[3] = dphi + dreg;
+  for (int i = 4; i < 8; ++i) out_host[i] = 0.0;
+  return SPCP_OK;
+}
+
+int spcp_line_release(spcp_problem* p) {
+  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
+  SPCP_CUDA(cudaSetDevice(p->device));
+  if (p->stream) SPCP_CUDA(cudaStreamSynchronize(p->stream));
+  p->line_ws.release();
+  p->line_ready = false;
   return SPCP_OK;
 }
 

@@ -11,7 +11,8 @@ import ctypes
 
 import numpy as np
 
-from ._lib import SPCP_F32, SPCP_F64, STORE_DENSE, STORE_F32, STORE_F64, STORE_SPARSE, check, lib
+from ._lib import (SPCP_ERR_UNSUPPORTED, SPCP_F32, SPCP_F64, STORE_DENSE, STORE_F32, STORE_F64,
+                   STORE_SPARSE, check, lib)
 
 __all__ = ["DeviceProblem", "torch_mod", "cuda_device", "dptr", "PRECISIONS", "nvtx_range"]
 
@@ -245,6 +246,25 @@ class DeviceProblem:
         check(fn(self.h, int(k), dptr(z), b, dptr(w_right), dptr(left), dptr(w_left),
                  dptr(right)))
         return left, right
+
+    # ------------------------------------------------------------ line probes
+    def line_setup(self, k, z, dz):
+        """Store R0, D1, D2 of the ray z + a dz (csrc/line.cuh).  False when the
+        three m x n float64 matrices do not fit (or X is sparse-only): the
+        caller keeps probing with eval()."""
+        rc = lib.spcp_line_setup(self.h, int(k), dptr(z), dptr(dz))
+        if rc == SPCP_ERR_UNSUPPORTED:
+            return False
+        check(rc)
+        return True
+
+    def line_probe(self, alpha):
+        """[F, phi, reg, grad F . dz, 0, 0, 0, 0] at z + alpha dz of the stored ray."""
+        check(lib.spcp_line_probe(self.h, float(alpha), self._out))
+        return np.frombuffer(self._out, dtype=np.float64).copy()
+
+    def line_release(self):
+        check(lib.spcp_line_release(self.h))
 
     def materialize(self, k, z, row0=0, rows=None, want_l=True, want_s=True):
         rows = self.m - row0 if rows is None else rows

@@ -142,6 +142,37 @@ class ShardedSpace:
         out = self.dp.eval_finish(self.k, code, z, d, alpha, gu, self.scal, g_out)
         return out[0], out[3], out[4]
 
+    # stored-ray probes (DeviceLbfgs fp64 searches): every rank stores its
+    # shard's R0, D1, D2; the replicated U part of the regulariser is counted once
+    def line_setup(self, z, d):
+        setup = getattr(self.dp, "line_setup", None)
+        ok = bool(setup(self.k, z, d)) if setup is not None else False
+        if setup is None:  # host-side test doubles: no rank has it
+            return False
+        # all ranks or none (device memory may differ between ranks)
+        flag = allreduce_host(np.array([0.0 if ok else 1.0]), self.comm_device, self.group)
+        if flag[0] > 0.0:
+            if ok:
+                self.dp.line_release()
+            return False
+        g = self.dp.vec_gram([z[: self.mk], d[: self.mk]], [z[: self.mk], d[: self.mk]])
+        self._ureg = (float(g[0, 0]), float(g[0, 1]), float(g[1, 1]))
+        return True
+
+    def line_probe(self, alpha):
+        out = self.dp.line_probe(alpha)
+        uu, ud, dd = self._ureg
+        lam = self.dp.lambda_l
+        reg_u = 0.5 * lam * (uu + alpha * (2.0 * ud + alpha * dd))
+        dreg_u = lam * (ud + alpha * dd)
+        tot = allreduce_host(np.array([out[0] - reg_u, out[3] - dreg_u]), self.comm_device,
+                             self.group)
+        self.comm_calls += 1
+        return float(tot[0]) + reg_u, float(tot[1]) + dreg_u
+
+    def line_release(self):
+        self.dp.line_release()
+
     def gram(self, a_list, b_list):
         ua = [a[: self.mk] for a in a_list]
         ub = [b[: self.mk] for b in b_list]

@@ -103,6 +103,27 @@ def strong_wolfe(probe, f0, slope0, alpha0, c1, c2):
     return None
 
 
+class _ProbeBudget(Exception):
+    """An fp32 line search of the mixed solver ran out of probes."""
+
+
+# mixed precision: probes one fp32 line search may spend before it is treated
+# as failed (the fp32 noise floor) and the solver switches to fp64.  A failed
+# search leaves the iterate where it was, so the cap only saves evaluations
+# (a zoom at the fp32 floor otherwise runs ~40 probes until its interval
+# collapses); the fp64 phase then runs the reference's search unchanged.
+FP32_PROBE_CAP = 10
+
+# fp64 searches: after this many probes of one search the space stores the ray
+# (space.line_setup: R0, D1, D2 with R(a) = R0 - a D1 - a^2 D2) and answers
+# the remaining probes from it at a fraction of an evaluation (no rank-k
+# products, no gradient); the accepted point is re-evaluated in full.  Most
+# searches accept their first probe and never get here; the long ones (the
+# final search that ends in line_search_failed runs ~30 probes) do.  None
+# disables.
+LINE_PROBES_AFTER = 3
+
+
 def _check_wolfe(c1, c2, memory):
     if not 0.0 < c1 < c2 < 1.0:
         raise ValueError(f"need 0 < c1 < c2 < 1, got c1={c1}, c2={c2}")
@@ -295,6 +316,14 @@ class DeviceLbfgs:
     def run(self, x):
         """Minimise from the device vector x (updated in place).  Returns an
         LbfgsResult whose x is the same device vector."""
+        self._line_held = False
+        try:
+            return self._run(x)
+        finally:
+            if self._line_held:
+                self.sp.line_release()
+
+    def _run(self, x):
         sp = self.sp
         evals = 0
         f, _, gg = sp.eval(x, None, 0.0, self.g, self.cur)
@@ -341,16 +370,48 @@ class DeviceLbfgs:
             a0 = 1.0 if self.order else min(1.0, 1.0 / max(gnorm, 1e-12))
             state = {"n": 0, "gg": 0.0}
 
+            capped = self.precision == "mixed" and self.cur == "fp32"
+            use_line = (self.cur == "fp64" and LINE_PROBES_AFTER is not None
+                        and hasattr(sp, "line_setup"))
+            line = {"tried": False, "on": False, "last": False}
+
             def probe(alpha):
-                fv, gd, gg_t = sp.eval(x, self.d, alpha, self.g_new, self.cur)
+                if capped and state["n"] >= FP32_PROBE_CAP:
+                    raise _ProbeBudget
+                if use_line and not line["tried"] and state["n"] >= LINE_PROBES_AFTER:
+                    line["tried"] = True
+                    line["on"] = bool(sp.line_setup(x, self.d))
+                if line["on"]:
+                    fv, gd = sp.line_probe(alpha)
+                    line["last"] = True
+                else:
+                    fv, gd, gg_t = sp.eval(x, self.d, alpha, self.g_new, self.cur)
+                    state["gg"] = gg_t
+                    line["last"] = False
                 state["n"] += 1
-                state["gg"] = gg_t
                 if not math.isfinite(fv):
                     fv = math.inf  # lbfgs.py:58-59
                 return fv, gd
 
-            hit = strong_wolfe(probe, f, slope, a0, self.c1, self.c2)
+            try:
+                hit = strong_wolfe(probe, f, slope, a0, self.c1, self.c2)
+            except _ProbeBudget:
+                hit = None
+            except BaseException:
+                if line["on"]:
+                    sp.line_release()
+                raise
+            if line["on"]:
+                # the next long search reuses the stored-ray workspace; it is
+                # freed when the run ends
+                self._line_held = True
             evals += state["n"]
+            if hit is not None and line["last"]:
+                # accepted on a stored-ray probe: the full evaluation there gives
+                # the gradient (and the objective the iteration carries on with)
+                fv, _, state["gg"] = sp.eval(x, self.d, hit[0], self.g_new, self.cur)
+                evals += 1
+                hit = (hit[0], fv)
             if hit is None:
                 if self.precision == "mixed" and self.cur == "fp32":
                     to_fp64()  # the fp32 noise floor, not the reference's floor: retry

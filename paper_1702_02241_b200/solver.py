@@ -186,6 +186,17 @@ class SplitSpace:
         out = self.dp.eval(self.k, _dtype(precision), z, d, alpha, g_out)
         return out[0], out[3], out[4]
 
+    def line_setup(self, z, d):
+        """Store the ray z + a d for line_probe (DeviceLbfgs, fp64 searches)."""
+        return self.dp.line_setup(self.k, z, d)
+
+    def line_probe(self, alpha):
+        out = self.dp.line_probe(alpha)
+        return out[0], out[3]
+
+    def line_release(self):
+        self.dp.line_release()
+
     def gram(self, a_list, b_list):
         return self.dp.vec_gram(a_list, b_list)
 

@@ -135,3 +135,80 @@ class NumpyCertProblem(NumpyShardProblem):
         left = torch.from_numpy(g @ w_right.numpy()) if w_right is not None else None
         right = torch.from_numpy(g.T @ w_left.numpy()) if w_left is not None else None
         return left, right
+
+
+class NumpyLineSpace(NumpySpace):
+    """NumpySpace with the stored-ray probes of spcp_line_setup / _probe
+    (R(a) = R0 - a D1 - a^2 D2 on Omega), numpy float64."""
+
+    def __init__(self, *a, fits=True, **kw):
+        super().__init__(*a, **kw)
+        self.fits = fits
+        self.setups = self.releases = self.line_probes = 0
+        self.ray = None
+
+    def _uv(self, w):
+        mk = self.m * self.k
+        return w[:mk].reshape(self.m, self.k), w[mk:].reshape(self.n, self.k)
+
+    def line_setup(self, z, d):
+        self.setups += 1
+        if not self.fits:
+            return False
+        u, v = self._uv(z)
+        du, dv = self._uv(d)
+        obs = np.ones_like(self.x, bool) if self.mask is None else self.mask.astype(bool)
+        r0 = np.where(obs, self.x - u @ v.T, 0.0)
+        d1 = np.where(obs, du @ v.T + u @ dv.T, 0.0)
+        d2 = np.where(obs, du @ dv.T, 0.0)
+        self.ray = (r0, d1, d2, float(z @ z), float(z @ d), float(d @ d))
+        return True
+
+    def line_probe(self, alpha):
+        r0, d1, d2, zz, zd, dd = self.ray
+        r = r0 - alpha * (d1 + alpha * d2)
+        c = np.clip(r, -self.lam_s, self.lam_s)
+        phi = float(np.sum(np.abs(c) * (np.abs(r) - 0.5 * np.abs(c))))
+        dphi = float(np.sum(-c * (d1 + 2.0 * alpha * d2)))
+        reg = 0.5 * self.lam_l * (zz + alpha * (2.0 * zd + alpha * dd))
+        dreg = self.lam_l * (zd + alpha * dd)
+        self.line_probes += 1
+        return phi + reg, dphi + dreg
+
+    def line_release(self):
+        self.releases += 1
+        self.ray = None
+
+
+class NumpyLineShardProblem(NumpyShardProblem):
+    """NumpyShardProblem with the stored-ray probes (spcp_line_*) of one shard:
+    out = [F_p, phi_p, reg_p, gd_p, 0...] where reg_p covers [U | V_p]."""
+
+    def __init__(self, *a, **kw):
+        super().__init__(*a, **kw)
+        self.lambda_l = self.lam_l
+        self.ray = None
+        self.setups = self.releases = 0
+
+    def line_setup(self, k, z, d):
+        zz, dd = z.double().numpy(), d.double().numpy()
+        u, v = self._split(zz, k)
+        du, dv = self._split(dd, k)
+        self.ray = (self.x - u @ v.T, du @ v.T + u @ dv.T, du @ dv.T,
+                    float(zz @ zz), float(zz @ dd), float(dd @ dd))
+        self.setups += 1
+        return True
+
+    def line_probe(self, alpha):
+        r0, d1, d2, zz, zd, dd = self.ray
+        r = r0 - alpha * (d1 + alpha * d2)
+        c = np.clip(r, -self.lam_s, self.lam_s)
+        phi = float(np.sum(np.abs(c) * (np.abs(r) - 0.5 * np.abs(c))))
+        dphi = float(np.sum(-c * (d1 + 2.0 * alpha * d2)))
+        reg = 0.5 * self.lam_l * (zz + alpha * (2.0 * zd + alpha * dd))
+        dreg = self.lam_l * (zd + alpha * dd)
+        return np.array([phi + reg, phi, reg, dphi + dreg, 0.0, 0.0, 0.0, 0.0])
+
+    def line_release(self):
+        self.releases += 1
+        self.ray = None

@@ -21,7 +21,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, out_q):
+def _worker(rank, world, port, out_q, line=False):
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -30,9 +30,10 @@ def _worker(rank, world, port, out_q):
     import torch
     import torch.distributed as dist
 
-    from fakes import NumpyShardProblem
+    from fakes import NumpyLineShardProblem, NumpyShardProblem
     from oracle import spcp_oracle as orc
     from paper_1702_02241_b200.dist import ShardedSpace, shard_bounds
+    import paper_1702_02241_b200.lbfgs as lb
     from paper_1702_02241_b200.lbfgs import DeviceLbfgs
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -42,7 +43,10 @@ def _worker(rank, world, port, out_q):
         m, n, k, lam_l, lam_s = 60, 45, 4, 1.0, 0.3
         x, _, _ = orc.gen_low_rank_plus_sparse(m, n, 4, 0.1, 1e-3, seed=21)
         c0, nl = shard_bounds(n, world, rank)
-        dp = NumpyShardProblem(np.ascontiguousarray(x[:, c0:c0 + nl]), lam_l, lam_s)
+        cls = NumpyLineShardProblem if line else NumpyShardProblem
+        if line:  # every fp64 probe from the stored ray
+            lb.LINE_PROBES_AFTER = 0
+        dp = cls(np.ascontiguousarray(x[:, c0:c0 + nl]), lam_l, lam_s)
         sp = ShardedSpace(dp, k, m, nl, comm_device=torch.device("cpu"))
         u0, v0 = orc.init_factors(x, k, strategy="rsvd", seed=0)
         z = torch.from_numpy(np.concatenate([u0.ravel(), v0[c0:c0 + nl].ravel()]))
@@ -50,17 +54,22 @@ def _worker(rank, world, port, out_q):
         f, gd, gg = sp.eval(z, None, 0.0, g, "fp64")
         eng = DeviceLbfgs(sp, grad_tol=1e-9, max_iter=400, precision="fp64")
         res = eng.run(z)
+        if line:
+            assert dp.setups > 0 and dp.releases == 1
         out_q.put((rank, f, gg, g.numpy().copy(), [r.objective for r in res.records],
                    res.termination, c0, nl))
     finally:
         dist.destroy_process_group()
 
 
-def test_sharded_eval_and_lbfgs_match_unsharded(oracle):
+@pytest.mark.parametrize("line", [False, True])
+def test_sharded_eval_and_lbfgs_match_unsharded(oracle, line):
+    """line=True: the fp64 searches answer their probes from each shard's
+    stored ray (ShardedSpace.line_probe: replicated U regulariser once)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, line)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(2)]

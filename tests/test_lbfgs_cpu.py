@@ -91,3 +91,35 @@ def test_mixed_precision_switch_logic(golden, oracle):
     res = eng.run(z.copy())
     assert eng.switched_at is not None
     assert res.objective == pytest.approx(float(d["s4_obj"]), rel=1e-9)
+
+
+@pytest.mark.parametrize("after", [0, 1, 3])
+def test_stored_ray_probes_follow_the_direct_search(golden, oracle, after, monkeypatch):
+    """fp64 searches answering probes from the stored ray (line_setup /
+    line_probe) reach the direct run's objective and termination; every setup
+    is released; a space whose ray does not fit keeps probing directly."""
+    import paper_1702_02241_b200.lbfgs as lb
+
+    from fakes import NumpyLineSpace
+
+    d = golden("solve")
+    m, n, k = 120, 90, 8
+    x = d["s4_x"]
+    u0, v0 = oracle.init_factors(x, k, strategy="rsvd", seed=0)
+    z = np.concatenate([u0.ravel(), v0.ravel()])
+    monkeypatch.setattr(lb, "LINE_PROBES_AFTER", None)
+    direct = DeviceLbfgs(NumpySpace(x, 3.0, 0.2, m, n, k), grad_tol=1e-9, max_iter=2000,
+                         precision="fp64").run(z.copy())
+    monkeypatch.setattr(lb, "LINE_PROBES_AFTER", after)
+    sp = NumpyLineSpace(x, 3.0, 0.2, m, n, k)
+    res = DeviceLbfgs(sp, grad_tol=1e-9, max_iter=2000, precision="fp64").run(z.copy())
+    assert res.objective == pytest.approx(direct.objective, rel=1e-10)
+    assert res.termination == direct.termination
+    assert sp.releases == (1 if sp.setups else 0)  # the workspace is freed when the run ends
+    if after == 0:
+        assert sp.line_probes > 0 and sp.setups == len(res.records) - 1 + (
+            res.termination == "line_search_failed")
+    nofit = NumpyLineSpace(x, 3.0, 0.2, m, n, k, fits=False)
+    res2 = DeviceLbfgs(nofit, grad_tol=1e-9, max_iter=2000, precision="fp64").run(z.copy())
+    assert nofit.line_probes == 0 and nofit.releases == 0
+    assert res2.objective == pytest.approx(direct.objective, rel=1e-10)
