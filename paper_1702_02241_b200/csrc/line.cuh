@@ -18,38 +18,50 @@ namespace spcp {
 
 // R0, D1, D2 of rows [0, m) (row-major, ld = n): 64 x 64 tiles, 4 x 4 entries
 // per thread, the three rank-k sums accumulated together from one staging of
-// U, dU, V, dV.
+// U, dU, V, dV; the next K-chunk is loaded into registers while the current
+// one is multiplied (one CTA per SM at this register count, so the loads
+// would otherwise sit exposed between the chunks).
 template <typename TX>
 __global__ void __launch_bounds__(256) line_setup_kernel(
     const double* __restrict__ z, const double* __restrict__ dz, int64_t m, int64_t n,
     int64_t k, const TX* __restrict__ x, int64_t ldx, const uint32_t* __restrict__ mbits,
     int64_t ldm, double* __restrict__ r0, double* __restrict__ d1, double* __restrict__ d2) {
   constexpr int TB = 64, KC = 8;
-  __shared__ double su[KC][TB + 1], sdu[KC][TB + 1], sv[KC][TB + 1], sdv[KC][TB + 1];
+  __shared__ double st[4][KC][TB + 1];  // U, dU (tile rows), V, dV (tile columns)
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
   const int64_t i0 = int64_t(blockIdx.y) * TB, j0 = int64_t(blockIdx.x) * TB;
-  const double *U = z, *V = z + m * k, *dU = dz, *dV = dz + m * k;
-  double p1[4][4] = {}, q1[4][4] = {}, q2[4][4] = {};
-  for (int64_t kc = 0; kc < k; kc += KC) {
-    for (int q = threadIdx.x; q < KC * TB; q += 256) {
+  const double* src[4] = {z, dz, z + m * k, dz + m * k};
+  // this thread's 8 staging slots: array a = i / 2, (row, column) from q
+  double pre[8];
+  auto gload = [&](int64_t kc) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int q = int(threadIdx.x) + 256 * (i & 1);
       const int r = q / KC, c = q % KC;
-      const int64_t gi = i0 + r, gj = j0 + r, gk = kc + c;
-      const bool ui = gi < m && gk < k, vj = gj < n && gk < k;
-      su[c][r] = ui ? U[gi * k + gk] : 0.0;
-      sdu[c][r] = ui ? dU[gi * k + gk] : 0.0;
-      sv[c][r] = vj ? V[gj * k + gk] : 0.0;
-      sdv[c][r] = vj ? dV[gj * k + gk] : 0.0;
+      const int64_t row = (i < 4 ? i0 : j0) + r, lim = i < 4 ? m : n, gk = kc + c;
+      pre[i] = (row < lim && gk < k) ? __ldg(src[i >> 1] + row * k + gk) : 0.0;
+    }
+  };
+  double p1[4][4] = {}, q1[4][4] = {}, q2[4][4] = {};
+  gload(0);
+  for (int64_t kc = 0; kc < k; kc += KC) {
+    __syncthreads();  // the previous chunk's reads are done
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int q = int(threadIdx.x) + 256 * (i & 1);
+      st[i >> 1][q % KC][q / KC] = pre[i];
     }
     __syncthreads();
+    if (kc + KC < k) gload(kc + KC);
 #pragma unroll
     for (int c = 0; c < KC; ++c) {
       double a[4], da[4], b[4], db[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        a[e] = su[c][ty * 4 + e];
-        da[e] = sdu[c][ty * 4 + e];
-        b[e] = sv[c][tx * 4 + e];
-        db[e] = sdv[c][tx * 4 + e];
+        a[e] = st[0][c][ty * 4 + e];
+        da[e] = st[1][c][ty * 4 + e];
+        b[e] = st[2][c][tx * 4 + e];
+        db[e] = st[3][c][tx * 4 + e];
       }
 #pragma unroll
       for (int e = 0; e < 4; ++e)
@@ -60,7 +72,6 @@ __global__ void __launch_bounds__(256) line_setup_kernel(
           q2[e][f] = fma(da[e], db[f], q2[e][f]);
         }
     }
-    __syncthreads();
   }
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
