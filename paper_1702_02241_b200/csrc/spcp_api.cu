@@ -301,10 +301,10 @@ static int launch_f64(spcp_problem* p, StreamParams sp, LaunchShape& shape) {
 #ifndef SPCP_F64_MMA
 #define SPCP_F64_MMA 1
 #endif
-template <int KP, bool MASK>
+template <int KP, bool MASK, bool RAW0 = false>
 static int launch_f64mma(spcp_problem* p, StreamParams sp, LaunchShape& shape) {
   using G = MmaGeom<KP>;
-  auto kern = f64_mma_kernel<KP, MASK>;
+  auto kern = f64_mma_kernel<KP, MASK, RAW0>;
   constexpr size_t smem = G::SMEM;
   static DevFlags attr = {};
   if (!attr[dev_slot(p->device)].load(std::memory_order_relaxed)) {
@@ -1260,6 +1260,76 @@ static int fetch_out(spcp_problem* p, double* out) {
 
 using namespace spcp;
 
+// k = 0 fp64 products X W_right / X^T W_left of fp32-exact X on the FP64 tensor
+// cores (f64_mma_kernel<KP, MASK, RAW0>), up to 64 columns per pass (the SIMT
+// RAW pass takes 32): the randomized SVD's sketches (linalg.py:77-106).
+static int apply0_f64mma(spcp_problem* p, int64_t b, const double* w_right, double* left_out,
+                         const double* w_left, double* right_out) {
+  int rc;
+  for (int64_t c0 = 0; c0 < b; c0 += 64) {
+    const int64_t bw = std::min<int64_t>(64, b - c0);
+    const int kp = int(round_up(bw, 8));
+    if (w_right) {
+      if ((rc = p->wr.ensure(size_t(p->n_pad) * kp * sizeof(double)))) return rc;
+      stage_cols_kernel<double><<<grid_for(p->n_pad * kp), 256, 0, p->stream>>>(
+          w_right, b, c0, bw, p->n, p->n_pad, kp, p->wr.as<double>());
+      SPCP_CHECK_LAUNCH("stage_cols");
+    }
+    if (w_left) {
+      if ((rc = p->wl.ensure(size_t(p->m_pad) * kp * sizeof(double)))) return rc;
+      stage_cols_kernel<double><<<grid_for(p->m_pad * kp), 256, 0, p->stream>>>(
+          w_left, b, c0, bw, p->m, p->m_pad, kp, p->wl.as<double>());
+      SPCP_CHECK_LAUNCH("stage_cols");
+    }
+    StreamParams sp{};
+    sp.m_pad = p->m_pad;
+    sp.n_pad = p->n_pad;
+    sp.ldx = p->ldx;
+    sp.ldm = p->ldm;
+    sp.tau = p->lambda_s;
+    sp.x = p->x32.ptr;
+    sp.mbits = p->masked ? p->mbits.as<uint32_t>() : nullptr;
+    sp.uc = p->wl.ptr;  // band operand of G^T W_left
+    sp.vc = p->wr.ptr;  // tile operand of G W_right
+    sp.do_left = w_right != nullptr;
+    sp.do_right = w_left != nullptr;
+    LaunchShape sh;
+#define SPCP_CASE(K)                                                              \
+  case K:                                                                         \
+    rc = p->masked ? launch_f64mma<K, true, true>(p, sp, sh)                      \
+                   : launch_f64mma<K, false, true>(p, sp, sh);                    \
+    break;
+    switch (kp) {
+      SPCP_CASE(8) SPCP_CASE(16) SPCP_CASE(24) SPCP_CASE(32) SPCP_CASE(40) SPCP_CASE(48)
+      SPCP_CASE(56) SPCP_CASE(64)
+      default: return fail(SPCP_ERR_UNSUPPORTED, "apply width");
+    }
+#undef SPCP_CASE
+    if (rc) return rc;
+    if ((rc = p->small.ensure(size_t(std::max(p->m, p->n)) * 64 * sizeof(double)))) return rc;
+    if (w_right) {
+      reduce_apply_kernel<double><<<grid_for(p->m * bw), 256, 0, p->stream>>>(
+          p->pleft.as<double>(), sh.nchunks, p->m, p->m_pad, kp, bw, p->small.as<double>());
+      SPCP_CHECK_LAUNCH("reduce_apply");
+      p->launches++;
+      SPCP_CUDA(cudaMemcpy2DAsync(left_out + c0, b * sizeof(double), p->small.ptr,
+                                  bw * sizeof(double), bw * sizeof(double), p->m,
+                                  cudaMemcpyDeviceToDevice, p->stream));
+    }
+    if (w_left) {
+      reduce_apply_kernel<double><<<grid_for(p->n * bw), 256, 0, p->stream>>>(
+          p->pright.as<double>(), sh.nrb, p->n, p->n_pad, kp, bw, p->small.as<double>());
+      SPCP_CHECK_LAUNCH("reduce_apply");
+      p->launches++;
+      SPCP_CUDA(cudaMemcpy2DAsync(right_out + c0, b * sizeof(double), p->small.ptr,
+                                  bw * sizeof(double), bw * sizeof(double), p->n,
+                                  cudaMemcpyDeviceToDevice, p->stream));
+    }
+  }
+  SPCP_CUDA(cudaStreamSynchronize(p->stream));
+  return SPCP_OK;
+}
+
 template <typename T>
 static int apply_impl(spcp_problem* p, int64_t k, const double* z, int64_t b,
                       const double* w_right, double* left_out, const double* w_left,
@@ -1284,6 +1354,9 @@ static int apply_impl(spcp_problem* p, int64_t k, const double* z, int64_t b,
     rc = x64 ? launch_dense<double>(p, 1, k, z, 0, p->m, gmat, nullptr, p->ldx, p->pphi.as<double>())
              : launch_dense<float>(p, 1, k, z, 0, p->m, gmat, nullptr, p->ldx, p->pphi.as<double>());
     if (rc) return rc;
+  }
+  if constexpr (sizeof(T) == 8) {
+    if (k == 0 && !x64 && p->x32.ptr && SPCP_F64_MMA) return apply0_f64mma(p, b, w_right, left_out, w_left, right_out);
   }
   for (int64_t c0 = 0; c0 < b; c0 += 32) {
     const int64_t bw = std::min<int64_t>(32, b - c0);
@@ -1435,6 +1508,26 @@ static int build_sddmm(spcp_problem* p) {
 }
 
 // ====================================================================== ABI
+template <int KP, bool MASK>
+static int launch_line_mma(spcp_problem* p, dim3 grid, int64_t chunk_cols, int64_t k,
+                           const double* z, const double* dz, const uint32_t* mb, double* r0,
+                           size_t ld) {
+  using G = LineGeom<KP, MASK>;
+  auto kern = line_setup_mma_kernel<KP, MASK>;
+  static DevFlags attr = {};
+  if (!attr[dev_slot(p->device)].load(std::memory_order_relaxed)) {
+    SPCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(G::SMEM)));
+    attr[dev_slot(p->device)].store(1, std::memory_order_relaxed);
+  }
+  kern<<<grid, 256, G::SMEM, p->stream>>>(z, dz, p->m, p->n, p->n_pad, k, p->x32.as<float>(),
+                                          p->ldx, mb, p->ldm, chunk_cols, r0, r0 + ld,
+                                          r0 + 2 * ld);
+  SPCP_CHECK_LAUNCH("line_setup_mma");
+  p->launches++;
+  return SPCP_OK;
+}
+
 extern "C" {
 
 int spcp_abi_version(void) { return SPCP_ABI_VERSION; }
@@ -1843,7 +1936,8 @@ int spcp_line_setup(spcp_problem* p, int64_t k, const double* z, const double* d
   p->line_ready = false;
   if (!p->x64.ptr && !p->x32.ptr)
     return fail(SPCP_ERR_UNSUPPORTED, "line_setup: no dense X store (sparse-observation problem)");
-  const size_t per = size_t(p->m) * size_t(p->n);
+  // rows of n_pad entries (zero pads): aligned double2 pairs for the probe
+  const size_t per = size_t(p->m) * size_t(p->n_pad);
   const size_t ld = size_t(round_up(int64_t(per), 32));  // 256-byte aligned matrices
   const size_t need = 3 * ld * sizeof(double);
   if (p->line_ws.bytes < need) {
@@ -1855,17 +1949,39 @@ int spcp_line_setup(spcp_problem* p, int64_t k, const double* z, const double* d
     if ((rc = p->line_ws.ensure(need))) return rc;
   }
   double* r0 = p->line_ws.as<double>();
-  dim3 grid(unsigned(ceil_div(p->n, 64)), unsigned(ceil_div(p->m, 64)));
   const uint32_t* mb = p->masked ? p->mbits.as<uint32_t>() : nullptr;
-  if (p->x64.ptr)
-    line_setup_kernel<double><<<grid, 256, 0, p->stream>>>(z, dz, p->m, p->n, k,
-                                                           p->x64.as<double>(), p->ldx, mb, p->ldm,
-                                                           r0, r0 + ld, r0 + 2 * ld);
-  else
-    line_setup_kernel<float><<<grid, 256, 0, p->stream>>>(z, dz, p->m, p->n, k,
-                                                          p->x32.as<float>(), p->ldx, mb, p->ldm,
-                                                          r0, r0 + ld, r0 + 2 * ld);
-  SPCP_CHECK_LAUNCH("line_setup");
+  if (!p->x64.ptr && k <= 64 && SPCP_F64_MMA) {
+    // fp32-exact X: the three products on the FP64 tensor cores
+    const int kp = int(round_up(k, 8));
+    const int64_t nrb = p->m_pad / 128, ntiles = p->n_pad / 64;
+    int64_t nch = pick_chunks(nrb, ntiles, 1, 2);
+    const int64_t tiles_per = ceil_div(ntiles, nch);
+    nch = ceil_div(ntiles, tiles_per);
+    const dim3 grid{unsigned(nch), unsigned(nrb), 1u};
+#define SPCP_CASE(K)                                                                          \
+  case K:                                                                                     \
+    rc = p->masked ? launch_line_mma<K, true>(p, grid, tiles_per * 64, k, z, dz, mb, r0, ld) \
+                   : launch_line_mma<K, false>(p, grid, tiles_per * 64, k, z, dz, mb, r0, ld); \
+    break;
+    switch (kp) {
+      SPCP_CASE(8) SPCP_CASE(16) SPCP_CASE(24) SPCP_CASE(32) SPCP_CASE(40) SPCP_CASE(48)
+      SPCP_CASE(56) SPCP_CASE(64)
+      default: return fail(SPCP_ERR_UNSUPPORTED, "line_setup width");
+    }
+#undef SPCP_CASE
+    if (rc) return rc;
+  } else {
+    dim3 grid(unsigned(p->n_pad / 64), unsigned(ceil_div(p->m, 64)));
+    if (p->x64.ptr)
+      line_setup_kernel<double><<<grid, 256, 0, p->stream>>>(
+          z, dz, p->m, p->n, p->n_pad, k, p->x64.as<double>(), p->ldx, mb, p->ldm, r0, r0 + ld,
+          r0 + 2 * ld);
+    else
+      line_setup_kernel<float><<<grid, 256, 0, p->stream>>>(
+          z, dz, p->m, p->n, p->n_pad, k, p->x32.as<float>(), p->ldx, mb, p->ldm, r0, r0 + ld,
+          r0 + 2 * ld);
+    SPCP_CHECK_LAUNCH("line_setup");
+  }
   p->launches++;
   // regulariser on the ray: |z + a dz|^2 = zz + 2 a zd + a^2 dd
   const int64_t len = (p->m + p->n) * k;
@@ -1888,7 +2004,7 @@ int spcp_line_probe(spcp_problem* p, double alpha, double* out_host) {
   if ((rc = ensure_common(p))) return rc;
   const int nb = kSMs * 4;
   if ((rc = p->line_part.ensure(size_t(2 * nb) * sizeof(double)))) return rc;
-  const size_t per = size_t(p->m) * size_t(p->n);
+  const size_t per = size_t(p->m) * size_t(p->n_pad);
   const size_t ld = size_t(round_up(int64_t(per), 32));
   const double* r0 = p->line_ws.as<double>();
   line_probe_kernel<<<nb, 256, 0, p->stream>>>(r0, r0 + ld, r0 + 2 * ld, int64_t(per), alpha,

@@ -48,7 +48,11 @@ struct MmaGeom {
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
-template <int KP, bool MASK>
+// RAW0: the k = 0 products of the randomized SVD (linalg.py:77-106 sketches
+// X W and X^T Q): phase 1 only stages the observed X tile as G (fp64), and
+// phases 2 / 3 run when p.do_left / p.do_right ask for them, with uc / vc
+// holding the staged W_left / W_right (KP columns).
+template <int KP, bool MASK, bool RAW0 = false>
 __global__ void __launch_bounds__(256, 1) f64_mma_kernel(const StreamParams p) {
   using G = MmaGeom<KP>;
   constexpr int BM = G::BM, BN = G::BN, KS = G::KS, GS = G::GS, XS = G::XS, NN = G::NN;
@@ -73,7 +77,8 @@ __global__ void __launch_bounds__(256, 1) f64_mma_kernel(const StreamParams p) {
   const double* __restrict__ Uc = reinterpret_cast<const double*>(p.uc);
   const double* __restrict__ Vc = reinterpret_cast<const double*>(p.vc);
 
-  {  // the row band's U (once)
+  const bool do_left = !RAW0 || p.do_left, do_right = !RAW0 || p.do_right;
+  if (do_right) {  // the row band's U (once)
     constexpr int CPR = KP / 2;
     for (int q = tid; q < BM * CPR; q += 256) {
       const int r = q / CPR, c = q % CPR;
@@ -96,7 +101,7 @@ __global__ void __launch_bounds__(256, 1) f64_mma_kernel(const StreamParams p) {
   auto load_v = [&](int t) {
     const int64_t c0 = c_begin + int64_t(t) * BN;
     constexpr int CPR = KP / 2;
-    for (int q = tid; q < BN * CPR; q += 256) {
+    for (int q = tid; q < (do_left ? BN * CPR : 0); q += 256) {
       const int r = q / CPR, c = q % CPR;
       cp_async16(Vs + r * KS + 2 * c, Vc + (c0 + r) * KP + 2 * c);
     }
@@ -122,7 +127,19 @@ __global__ void __launch_bounds__(256, 1) f64_mma_kernel(const StreamParams p) {
     __syncthreads();  // X, V of tile t (and U) resident
 
     // ---------------- phase 1: S = U V^T, epilogue, G tile
-    {
+    if constexpr (RAW0) {  // G = the observed X tile
+      for (int q = tid; q < BM * (BN / 2); q += 256) {
+        const int r = q / (BN / 2), c = 2 * (q % (BN / 2));
+        const float2 xv = *reinterpret_cast<const float2*>(Xs + r * XS + c);
+        double2 g = make_double2(double(xv.x), double(xv.y));
+        if constexpr (MASK) {
+          const uint32_t w = Ms[r * 2 + (c >> 5)];
+          g.x = ((w >> (c & 31)) & 1u) ? g.x : 0.0;
+          g.y = ((w >> ((c + 1) & 31)) & 1u) ? g.y : 0.0;
+        }
+        *reinterpret_cast<double2*>(Gs + r * GS + c) = g;
+      }
+    } else {
       double acc[4][4][2];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
@@ -172,7 +189,7 @@ __global__ void __launch_bounds__(256, 1) f64_mma_kernel(const StreamParams p) {
     if (t + 1 < ntiles) load_x(t + 1);
 
     // ---------------- phase 2: Lacc += G V_t   (A = G rows, B = V_t)
-    {
+    if (do_left) {
       const int wr2 = warp * 16;
 #pragma unroll 4
       for (int j0 = 0; j0 < BN; j0 += 4) {
@@ -192,7 +209,7 @@ __global__ void __launch_bounds__(256, 1) f64_mma_kernel(const StreamParams p) {
       load_v(t + 1);
     }
     // ---------------- phase 3: R_t = G^T U   (A = G^T: columns 8 w .., K = rows)
-    {
+    if (do_right) {
       double racc[NN][2];
 #pragma unroll
       for (int b = 0; b < NN; ++b) racc[b][0] = racc[b][1] = 0.0;
@@ -216,7 +233,7 @@ __global__ void __launch_bounds__(256, 1) f64_mma_kernel(const StreamParams p) {
   }
 
   // ---- flush the band's left product: pleft[chunk][r0 + row][p]
-  {
+  if (do_left) {
     const int wr2 = warp * 16;
     double* dst = reinterpret_cast<double*>(p.pleft) + (int64_t(chunk) * p.m_pad + r0) * KP;
 #pragma unroll

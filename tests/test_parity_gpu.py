@@ -195,6 +195,34 @@ def test_apply_products(api, oracle):
     assert rel(right.cpu().numpy(), obs.T @ wl) <= 1e-12
 
 
+@pytest.mark.parametrize("masked", [False, True])
+@pytest.mark.parametrize("b", [5, 30, 64, 71])
+def test_apply0_tensor_core_products(api, masked, b):
+    """k == 0 fp64 products of fp32-exact X (the rSVD sketches) on the FP64
+    tensor cores: X W and X^T W, one side or both, widths up to 64 per pass
+    (71: two passes), odd shapes, against numpy."""
+    import torch
+
+    rng = np.random.default_rng(100 + b + masked)
+    m, n = 333, 517
+    x = f32(rng.standard_normal((m, n)))
+    mask = (rng.random((m, n)) < 0.6) if masked else None
+    spec = _spec(api, x, 1.0, 0.5, mask)
+    dp = spec.device("fp64")
+    obs = x if mask is None else np.where(mask, x, 0.0)
+    wr = rng.standard_normal((n, b))
+    wl = rng.standard_normal((m, b))
+    left, right = dp.apply(0, None, w_right=torch.from_numpy(wr).cuda(),
+                           w_left=torch.from_numpy(wl).cuda())
+    assert rel(left.cpu().numpy(), obs @ wr) <= 1e-13
+    assert rel(right.cpu().numpy(), obs.T @ wl) <= 1e-13
+    left, _ = dp.apply(0, None, w_right=torch.from_numpy(wr).cuda())
+    assert rel(left.cpu().numpy(), obs @ wr) <= 1e-13
+    _, right = dp.apply(0, None, w_left=torch.from_numpy(wl).cuda())
+    assert rel(right.cpu().numpy(), obs.T @ wl) <= 1e-13
+    spec.release_device()
+
+
 def test_materialize_l_s(api, oracle):
     import torch
 
