@@ -104,10 +104,53 @@ def _device_factor_svd(dp, u, v, rank_tol, ops):
     sig = core.sigma
     r = 0 if (sig.size == 0 or sig[0] <= 0.0) else int(np.sum(sig > rank_tol * sig[0]))
     if r == 0:
-        return None, sig[:0], None, sig
+        return None, sig[:0], None, sig, None
     u1 = dp.matmul_small(qu, core.u[:, :r])
     v1 = dp.matmul_small(qv, core.v[:, :r])
-    return u1, sig[:r].copy(), v1, sig
+    # U1 = U ru^-1 core.u, V1 = V rv^-1 core.v (full column rank): the maps from
+    # the factors to the bases, for _gradient_products
+    maps = None
+    if r == u.shape[1] and ru.shape == rv.shape == (r, r):
+        cu, cv = np.linalg.cond(ru), np.linalg.cond(rv)
+        if max(cu, cv) <= GRADIENT_ROUTE_MAX_COND:
+            maps = (np.linalg.solve(ru, core.u[:, :r]), np.linalg.solve(rv, core.v[:, :r]))
+    return u1, sig[:r].copy(), v1, sig, maps
+
+
+# t1-t3 need G V1 and G^T U1.  With full-rank factors V1 = V rv^-1 core.v, so
+# G V1 = (G V) rv^-1 core.v, and G V = grad_U F - lambda U comes out of ONE fp64
+# evaluation (the FP64 tensor-core pass for fp32-exact X) instead of a separate
+# streaming product; used when the maps are this well conditioned (the products
+# keep ~cond * 1e-16 relative accuracy)
+GRADIENT_ROUTE_MAX_COND = 1e4
+
+
+def _gradient_products(dp, z, k, lam, ops):
+    """(G V, G^T U_p) at z (device, m x k and n_p x k) from one fp64
+    evaluation, or None when dp has no fp64 evaluation for this k."""
+    import torch
+
+    from ._lib import SPCP_F64
+
+    m, n = dp.m, dp.n
+    mk = m * k
+    if ops.sharded:
+        if not hasattr(dp, "eval_partial"):
+            return None
+        g = torch.empty((m + n) * k, dtype=torch.float64, device=z.device)
+        gu = torch.empty(mk, dtype=torch.float64, device=z.device)
+        scal = torch.empty(4, dtype=torch.float64, device=z.device)
+        dp.eval_partial(k, SPCP_F64, z, None, 0.0, gu, scal, g)
+        ops.dev(gu)  # G V summed over the column shards
+        gv = gu
+    else:
+        if not hasattr(dp, "eval"):
+            return None
+        g = torch.empty((m + n) * k, dtype=torch.float64, device=z.device)
+        dp.eval(k, SPCP_F64, z, None, 0.0, g)
+        gv = g[:mk] - lam * z[:mk]
+    gtu = g[mk:] - lam * z[mk:]
+    return gv.reshape(m, k), gtu.reshape(n, k)
 
 
 class _ProjectedOperator:
@@ -257,12 +300,17 @@ def certificate_core(dp, z, m, n_total, k, lam, rank_tol, f_zero, f_bound_hint, 
     against the device problem dp (a column shard when `ops` is sharded)."""
     u = z[: m * k].reshape(m, k)
     v = z[m * k:].reshape(dp.n, k)
-    u1, sig, v1, all_sig = _device_factor_svd(dp, u, v, rank_tol, ops)
+    u1, sig, v1, all_sig, maps = _device_factor_svd(dp, u, v, rank_tol, ops)
     r = sig.shape[0]
     l_norm = float(np.sqrt(np.sum(all_sig * all_sig)))  # |U V^T|_F = |R_U R_V^T|_F
     if r > 0:
-        gv1, gtu1 = dp.apply(k, z, w_right=v1, w_left=u1)
-        ops.dev(gv1)
+        prods = _gradient_products(dp, z, k, lam, ops) if maps is not None else None
+        if prods is not None:
+            gv1 = dp.matmul_small(prods[0], maps[1])
+            gtu1 = dp.matmul_small(prods[1], maps[0])
+        else:
+            gv1, gtu1 = dp.apply(k, z, w_right=v1, w_left=u1)
+            ops.dev(gv1)
         b = gv1.mul_(-1.0 / lam)  # D V1            (m x r)
         at = gtu1.mul_(-1.0 / lam)  # (U1^T D)^T     (n_p x r)
         c = ops.gram_rows(dp, at, v1)  # U1^T D V1 (r x r)

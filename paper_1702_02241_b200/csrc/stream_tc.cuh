@@ -53,6 +53,12 @@
 // slots, two named barriers per tile); 0: 128-row slots folded by the reduce.
 // Measured same-box at C2: 0.372 vs 0.348 ms (the barriers cost more than the
 // halved slot traffic saves), so 0.
+// 1: the lo piece of the G split by mixed-precision FMAs (fma.rn.f32.f16,
+// one per element) instead of fp16 -> fp32 conversions and a packed subtract
+#ifndef SPCP_TC_FHFMA
+#define SPCP_TC_FHFMA 1
+#endif
+
 #ifndef SPCP_TC_GT_FOLD
 #define SPCP_TC_GT_FOLD 0
 #endif
@@ -833,6 +839,11 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK, SEG>::NTHREADS, 1)
                                                                         (un.tc & 1) * 2 + h];
       uint32_t hi[16], lo[16];
       float2 hs2 = make_float2(0.f, 0.f);
+#ifdef SPCP_TC_EPI_PAD
+      // sensitivity probe: extra FFMA2s per pair into hs2 with a runtime zero
+      // (TcScales::pad0 = 0), no extra live registers, results unchanged
+      const float2 pad2 = make_float2(sc.pad0, sc.pad0);
+#endif
 #pragma unroll
       for (int ch = 0; ch < 2; ++ch) {
         uint32_t sv[16];
@@ -883,9 +894,17 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK, SEG>::NTHREADS, 1)
           const float2 cs2 = make_float2(fminf(fmaxf(r2.x, -tau_s), tau_s),
                                          fminf(fmaxf(r2.y, -tau_s), tau_s));
           hs2 = ffma2(cs2, ffma2(nhalf2, cs2, r2), hs2);
+#ifdef SPCP_TC_EPI_PAD
+#pragma unroll
+          for (int pp = 0; pp < SPCP_TC_EPI_PAD; ++pp) hs2 = ffma2(r2, pad2, hs2);
+#endif
           const float2 gp2 = fmul2(cs2, kap2);
           const __half2 hh2 = __float22half2_rn(gp2);
+#if SPCP_TC_FHFMA
+          const float2 lo2 = sub_half2_from(gp2, *reinterpret_cast<const uint32_t*>(&hh2));
+#else
           const float2 lo2 = fsub2(gp2, __half22float2(hh2));
+#endif
           hi[8 * ch + (e2 >> 1)] = *reinterpret_cast<const uint32_t*>(&hh2);
           lo[8 * ch + (e2 >> 1)] = pack_half2(lo2.x, lo2.y);
         }

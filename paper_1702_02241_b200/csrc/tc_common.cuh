@@ -196,6 +196,18 @@ __device__ __forceinline__ void bulk_wait_all() {
 __device__ __forceinline__ void bulk_wait_read_all() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
+// lo = g - float(h) for the two fp16 halves of h2, one mixed-precision FMA
+// each (FHFMA: h * -1 + g, a single rounding of an exact difference, so
+// bitwise the same as converting h back to fp32 and subtracting)
+__device__ __forceinline__ float2 sub_half2_from(float2 g, uint32_t h2) {
+  float2 r;
+  asm("{\n.reg .b16 l, h, m;\nmov.b32 {l, h}, %2;\nmov.b16 m, 0xBC00;\n"
+      "fma.rn.f32.f16 %0, l, m, %3;\nfma.rn.f32.f16 %1, h, m, %4;\n}\n"
+      : "=f"(r.x), "=f"(r.y)
+      : "r"(h2), "f"(g.x), "f"(g.y));
+  return r;
+}
+
 // named barrier over `count` threads (id 1..15; 0 is __syncthreads)
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");

@@ -106,6 +106,35 @@ def test_certificate_golden(api, golden):
     assert cert.e_norm == pytest.approx(float(d["zero_cert"][0]), rel=1e-12)
 
 
+def test_certificate_gradient_route(api, golden, monkeypatch):
+    """t1-t3 from one fp64 evaluation (G V1 = (grad_U F - lambda U) rv^-1
+    core.v) agree with the streaming product route, on the C1 iterates and the
+    reference's certificate goldens."""
+    import paper_1702_02241_b200.certificate as cm
+
+    from oracle import spcp_oracle as orc
+
+    d = golden("c1")
+    x, _, _ = orc.gen_low_rank_plus_sparse(1000, 1000, 10, 0.05, 1e-3, seed=0)
+    x = x.astype(np.float32).astype(np.float64)
+    spec = api.ProblemSpec(x=x, lambda_l=10.0, lambda_s=0.1)
+    for key in ("k5", "k10"):
+        fp = api.FactorPair(d[f"{key}_u"], d[f"{key}_v"])
+        monkeypatch.setattr(cm, "GRADIENT_ROUTE_MAX_COND", 1e4)
+        a = api.certificate(fp, spec)
+        monkeypatch.setattr(cm, "GRADIENT_ROUTE_MAX_COND", 0.0)  # streaming products
+        b = api.certificate(fp, spec)
+        # t1-t3 are differences of O(1) numbers (|I - U1^T D V1|^2 with c ~ 1):
+        # both routes round at ~1e-16 of c, so compare at that absolute level
+        lsq = 100.0  # lambda^2
+        np.testing.assert_allclose(np.sqrt(np.array(a.terms[:3]) / lsq),
+                                   np.sqrt(np.array(b.terms[:3]) / lsq), rtol=0, atol=1e-12)
+        ref = d[f"{key}_cert"]
+        np.testing.assert_allclose(np.sqrt(np.array(a.terms[:3]) / lsq),
+                                   np.sqrt(np.array(ref[1:4]) / lsq), rtol=0, atol=1e-12)
+        assert a.e_norm == pytest.approx(b.e_norm, rel=1e-5)
+
+
 def test_certificate_t4_routes(api, golden):
     """t4 is never a dense SVD (certificate.py:70-74 restated as streaming block
     subspace iteration on P): the under-ranked C1 iterate has several

@@ -1,0 +1,5 @@
+#!/bin/bash
+# round 2ag (v2: no extra live registers): epilogue instruction-count sensitivity (extra FFMA2 per element pair)
+mkdir -p gpurun_out
+tools/ab_run.sh gpurun_out/r2ag_ab.txt 3 p0 p1 p2
+echo done
