@@ -171,6 +171,18 @@ int spcp_apply_f32(spcp_problem* p, int64_t k, const double* z, int64_t b,
                    const double* w_right, double* left_out, const double* w_left,
                    double* right_out);
 
+/* ---- stored gradient (the certificate's repeated products, certificate.py:119)
+ * spcp_grad_store materialises G = grad phi(U V^T) on Omega (zeros elsewhere)
+ * once, float32 (dtype SPCP_F32) or float64, in device memory (m x n elements;
+ * SPCP_ERR_UNSUPPORTED when it does not fit — keep calling spcp_apply);
+ * spcp_apply_stored then gives G W_right / G^T W_left like spcp_apply from one
+ * pass over the stored G, without recomputing the rank-k residual;
+ * spcp_grad_release frees it. */
+int spcp_grad_store(spcp_problem* p, int64_t k, const double* z, int dtype);
+int spcp_apply_stored(spcp_problem* p, int64_t b, const double* w_right, double* left_out,
+                      const double* w_left, double* right_out);
+int spcp_grad_release(spcp_problem* p);
+
 /* ---- final L and S (solver.py:313-320) --------------------------------------
  * Rows [row0, row0+rows) of L = U V^T and S* = shrink(X - L) on Omega, float64,
  * written to device or host buffers (row-major, n columns); either may be NULL. */

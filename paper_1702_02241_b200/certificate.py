@@ -161,6 +161,24 @@ class _ProjectedOperator:
         self.dp, self.z, self.k, self.lam, self.u1, self.v1 = dp, z, k, lam, u1, v1
         self.ops = ops
         self.precision = precision
+        # every pass applies the same G: materialise it once (G from X and the
+        # factors in fp64, stored in the product precision) and stream the
+        # stored copy, instead of recomputing the rank-k residual per pass
+        store = getattr(dp, "grad_store", None)
+        self.stored = bool(store(k, z, precision)) if store is not None and STORE_GRADIENT \
+            else False
+        self.stored_used = self.stored
+
+    def close(self):
+        if self.stored:
+            self.dp.grad_release()
+            self.stored = False
+
+    def _apply(self, w_right=None, w_left=None):
+        if self.stored:
+            return self.dp.apply_stored(w_right=w_right, w_left=w_left)
+        return self.dp.apply(self.k, self.z, w_right=w_right, w_left=w_left,
+                             precision=self.precision)
 
     def proj_u(self, w):  # replicated m-side
         if self.u1 is None:
@@ -176,15 +194,19 @@ class _ProjectedOperator:
 
     def right(self, w):  # P w, w: n_p x b
         w = self.proj_v(w)
-        y, _ = self.dp.apply(self.k, self.z, w_right=w.contiguous(), precision=self.precision)
+        y, _ = self._apply(w_right=w.contiguous())
         self.ops.dev(y)  # sum_p D_p W_p
         return self.proj_u(y.mul_(-1.0 / self.lam))
 
     def left(self, y):  # P^T y, y: m x b (replicated)
         y = self.proj_u(y)
-        _, w = self.dp.apply(self.k, self.z, w_left=y.contiguous(), precision=self.precision)
+        _, w = self._apply(w_left=y.contiguous())
         return self.proj_v(w.mul_(-1.0 / self.lam))
 
+
+# the subspace iteration streams a stored copy of G when it fits (False: every
+# pass recomputes G from X and the factors)
+STORE_GRADIENT = True
 
 # Ritz-value convergence tolerance by product precision: fp64 streaming
 # products resolve sigma(P) to ~1e-15, the fp32 ones to ~1e-7
@@ -333,8 +355,12 @@ def certificate_core(dp, z, m, n_total, k, lam, rank_tol, f_zero, f_bound_hint, 
     precision = "fp32" if (m * n_total > FP32_PRODUCTS_MIN_ELEMS and "f32" in dp.store) \
         else "fp64"
     op = _ProjectedOperator(dp, z, k, lam, u1, v1, ops, precision)
-    sp, info = _subspace_sigmas(op, n_total, m, r)
+    try:
+        sp, info = _subspace_sigmas(op, n_total, m, r)
+    finally:
+        op.close()
     info["products"] = precision
+    info["stored_gradient"] = op.stored_used
     over = np.maximum(sp - 1.0, 0.0)
     t4 = float(np.sum(over * over))
     info["n_sigma_over_1"] = int(np.sum(sp > 1.0))

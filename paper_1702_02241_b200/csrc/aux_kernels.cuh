@@ -660,11 +660,13 @@ __global__ void reduce_apply_kernel(const T* __restrict__ part, int nparts, int6
 // L tile = U V^T for a 64x64 tile from the float64 iterate z (any k), then
 //   MODE 0: write L (ld = ldo) and S* = shrink(X - L) on Omega
 //   MODE 1: write G = -clip(X - L) on Omega (float64, ld = ldo) + phi partials
-template <typename TX, int MODE>
+//   (TO: the element type of l_out in MODE 1 — float for the certificate's
+//   stored fp32 G)
+template <typename TX, int MODE, typename TO = double>
 __global__ void __launch_bounds__(256) dense_kernel(
     const double* __restrict__ z, int64_t m, int64_t n, int64_t k, const TX* __restrict__ x,
     int64_t ldx, const uint32_t* __restrict__ mbits, int64_t ldm, double tau, int64_t row0,
-    int64_t rows, double* l_out, double* s_out, int64_t ldo, double* pphi) {
+    int64_t rows, TO* l_out, double* s_out, int64_t ldo, double* pphi) {
   constexpr int TB = 64, KC = 16;
   __shared__ double ut[KC][TB + 1];
   __shared__ double vt[KC][TB + 1];
@@ -711,7 +713,7 @@ __global__ void __launch_bounds__(256) dense_kernel(
       const bool obs = mbits == nullptr || ((mbits[gi * ldm + (gj >> 5)] >> (gj & 31)) & 1u);
       double r = obs ? double(x[gi * ldx + gj]) - l : 0.0;
       const int64_t o = (gi - row0) * ldo + gj;
-      if (MODE == 0) {
+      if constexpr (MODE == 0) {
         if (l_out) l_out[o] = l;
         if (s_out) {
           const double a = r < 0 ? -r : r;
@@ -719,7 +721,7 @@ __global__ void __launch_bounds__(256) dense_kernel(
           s_out[o] = r > 0 ? mag : (r < 0 ? -mag : 0.0);
         }
       } else {
-        l_out[o] = huber_clip<double>(r, tau, h);
+        l_out[o] = TO(huber_clip<double>(r, tau, h));
       }
     }
   }

@@ -151,6 +151,9 @@ struct spcp_problem {
   // line-restricted evaluation (line.cuh): R0, D1, D2 of one ray
   spcp::DevBuf line_ws, line_part;
   bool line_ready = false;
+  // stored G of one iterate (spcp_grad_store): the certificate's products
+  spcp::DevBuf gstore;
+  int gstore_type = -1;
   double line_zz = 0.0, line_zd = 0.0, line_dd = 0.0;
 };
 
@@ -1330,15 +1333,17 @@ static int apply0_f64mma(spcp_problem* p, int64_t b, const double* w_right, doub
   return SPCP_OK;
 }
 
+// gstored: products with a stored G (spcp_grad_store, element type T, the X
+// layout, zeros off Omega) as RAW passes instead of G from X and the factors
 template <typename T>
 static int apply_impl(spcp_problem* p, int64_t k, const double* z, int64_t b,
                       const double* w_right, double* left_out, const double* w_left,
-                      double* right_out) {
+                      double* right_out, const void* gstored = nullptr) {
   int rc;
   if (k < 0 || b < 1) return fail(SPCP_ERR_DIMENSION, "bad apply shape");
   SPCP_CUDA(cudaSetDevice(p->device));
   const bool x64 = p->x64.ptr != nullptr;
-  int kr = std::is_same<T, float>::value ? apply_kr32(k) : apply_kr64(k);
+  int kr = gstored ? 0 : (std::is_same<T, float>::value ? apply_kr32(k) : apply_kr64(k));
   // residual operands (T)
   if (kr > 0) {
     if ((rc = prep<T>(p, k, kr, z, nullptr, 0.0))) return rc;
@@ -1356,7 +1361,8 @@ static int apply_impl(spcp_problem* p, int64_t k, const double* z, int64_t b,
     if (rc) return rc;
   }
   if constexpr (sizeof(T) == 8) {
-    if (k == 0 && !x64 && p->x32.ptr && SPCP_F64_MMA) return apply0_f64mma(p, b, w_right, left_out, w_left, right_out);
+    if (!gstored && k == 0 && !x64 && p->x32.ptr && SPCP_F64_MMA)
+      return apply0_f64mma(p, b, w_right, left_out, w_left, right_out);
   }
   for (int64_t c0 = 0; c0 < b; c0 += 32) {
     const int64_t bw = std::min<int64_t>(32, b - c0);
@@ -1388,7 +1394,11 @@ static int apply_impl(spcp_problem* p, int64_t k, const double* z, int64_t b,
     sp.do_left = w_right != nullptr;
     sp.do_right = w_left != nullptr;
     LaunchShape sh;
-    if (kr < 0) {
+    if (gstored) {
+      sp.x = gstored;
+      sp.mbits = nullptr;
+      rc = dispatch_apply<T, T, false>(p, 0, pw, sp, sh);
+    } else if (kr < 0) {
       sp.x = p->gu_tmp.ptr;
       sp.mbits = nullptr;
       rc = pw == 8 ? launch_stream<double, double, 0, 8, MODE_RAW, false>(p, sp, sh, false)
@@ -1693,7 +1703,7 @@ int spcp_problem_destroy(spcp_problem* p) {
                     &p->scal, &p->gu_tmp, &p->vec_part, &p->small, &p->csr_ptr, &p->csr_idx,
                     &p->csr_v32, &p->csr_v64, &p->csc_ptr, &p->csc_idx, &p->csc_v32,
                     &p->csc_v64, &p->tc_units, &p->tc_begin, &p->tc_csr, &p->tc_uimg,
-                    &p->tc_vimg, &p->tc_scales, &p->tc_bmax, &p->line_ws, &p->line_part})
+                    &p->tc_vimg, &p->tc_scales, &p->tc_bmax, &p->line_ws, &p->line_part, &p->gstore})
     b->release();
   if (p->host_out) cudaFreeHost(p->host_out);
   for (int i = 0; i < spcp_problem::kEvRing; ++i) {
@@ -1861,6 +1871,69 @@ int spcp_apply(spcp_problem* p, int64_t k, const double* z, int64_t b, const dou
                double* left_out, const double* w_left, double* right_out) {
   if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
   return apply_impl<double>(p, k, z, b, w_right, left_out, w_left, right_out);
+}
+
+int spcp_grad_store(spcp_problem* p, int64_t k, const double* z, int dtype) {
+  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
+  if (k < 1) return fail(SPCP_ERR_DIMENSION, "k must be >= 1");
+  if (dtype != SPCP_F32 && dtype != SPCP_F64) return fail(SPCP_ERR_VALUE, "dtype");
+  int rc;
+  SPCP_CUDA(cudaSetDevice(p->device));
+  p->gstore_type = -1;
+  if (!p->x64.ptr && !p->x32.ptr)
+    return fail(SPCP_ERR_UNSUPPORTED, "grad_store: no dense X store (sparse-observation problem)");
+  const size_t es = dtype == SPCP_F32 ? 4 : 8;
+  const size_t need = size_t(p->m_pad) * size_t(p->ldx) * es;
+  if (p->gstore.bytes < need) {
+    p->gstore.release();
+    size_t free_b = 0, total_b = 0;
+    SPCP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    if (need + (size_t(1) << 30) > free_b)
+      return fail(SPCP_ERR_UNSUPPORTED, "grad_store: the m x n gradient does not fit");
+    if ((rc = p->gstore.ensure(need))) return rc;
+  }
+  SPCP_CUDA(cudaMemsetAsync(p->gstore.ptr, 0, need, p->stream));  // pads and off-Omega rows
+  const int64_t nbx = ceil_div(p->n, 64), nby = ceil_div(p->m, 64);
+  if ((rc = p->pphi.ensure(size_t(nbx * nby) * sizeof(double)))) return rc;
+  const dim3 grid{unsigned(nbx), unsigned(nby), 1u};
+  const uint32_t* mb = p->masked ? p->mbits.as<uint32_t>() : nullptr;
+#define SPCP_GS(TX, XP, TO)                                                                \
+  dense_kernel<TX, 1, TO><<<grid, 256, 0, p->stream>>>(z, p->m, p->n, k, XP, p->ldx, mb,    \
+                                                       p->ldm, p->lambda_s, 0, p->m,        \
+                                                       p->gstore.as<TO>(), nullptr, p->ldx, \
+                                                       p->pphi.as<double>())
+  if (p->x64.ptr) {
+    if (dtype == SPCP_F32) SPCP_GS(double, p->x64.as<double>(), float);
+    else SPCP_GS(double, p->x64.as<double>(), double);
+  } else {
+    if (dtype == SPCP_F32) SPCP_GS(float, p->x32.as<float>(), float);
+    else SPCP_GS(float, p->x32.as<float>(), double);
+  }
+#undef SPCP_GS
+  SPCP_CHECK_LAUNCH("grad_store");
+  p->launches++;
+  p->gstore_type = dtype;
+  return SPCP_OK;
+}
+
+int spcp_apply_stored(spcp_problem* p, int64_t b, const double* w_right, double* left_out,
+                      const double* w_left, double* right_out) {
+  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
+  if (p->gstore_type < 0) return fail(SPCP_ERR_VALUE, "apply_stored before grad_store");
+  return p->gstore_type == SPCP_F32
+             ? apply_impl<float>(p, 0, nullptr, b, w_right, left_out, w_left, right_out,
+                                 p->gstore.ptr)
+             : apply_impl<double>(p, 0, nullptr, b, w_right, left_out, w_left, right_out,
+                                  p->gstore.ptr);
+}
+
+int spcp_grad_release(spcp_problem* p) {
+  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
+  SPCP_CUDA(cudaSetDevice(p->device));
+  if (p->stream) SPCP_CUDA(cudaStreamSynchronize(p->stream));
+  p->gstore.release();
+  p->gstore_type = -1;
+  return SPCP_OK;
 }
 
 int spcp_apply_f32(spcp_problem* p, int64_t k, const double* z, int64_t b,

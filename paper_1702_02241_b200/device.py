@@ -247,6 +247,35 @@ class DeviceProblem:
                  dptr(right)))
         return left, right
 
+    # ------------------------------------------------------------ stored gradient
+    def grad_store(self, k, z, precision="fp32"):
+        """Materialise G = grad phi(U V^T) once (float32 or float64) for
+        apply_stored; False when it does not fit (or X is sparse-only)."""
+        rc = lib.spcp_grad_store(self.h, int(k), dptr(z), SPCP_F32 if precision == "fp32"
+                                 else SPCP_F64)
+        if rc == SPCP_ERR_UNSUPPORTED:
+            return False
+        check(rc)
+        return True
+
+    def apply_stored(self, w_right=None, w_left=None):
+        """(G @ w_right, G^T @ w_left) from the stored G (float64 device matrices)."""
+        torch = torch_mod()
+        b = int((w_right if w_right is not None else w_left).shape[1])
+        left = right = None
+        if w_right is not None:
+            w_right = w_right.contiguous()
+            left = torch.empty((self.m, b), dtype=torch.float64, device=self.device)
+        if w_left is not None:
+            w_left = w_left.contiguous()
+            right = torch.empty((self.n, b), dtype=torch.float64, device=self.device)
+        check(lib.spcp_apply_stored(self.h, b, dptr(w_right), dptr(left), dptr(w_left),
+                                    dptr(right)))
+        return left, right
+
+    def grad_release(self):
+        check(lib.spcp_grad_release(self.h))
+
     # ------------------------------------------------------------ line probes
     def line_setup(self, k, z, dz):
         """Store R0, D1, D2 of the ray z + a dz (csrc/line.cuh).  False when the

@@ -1,6 +1,6 @@
-"""Where the certificate's time goes at C5 (200000 x 20000, k = 50) on one GPU:
+"""Where the certificate's time goes at C5 (200000 x 20000, k = 50; or c2) on one GPU:
 every DeviceProblem product it calls, by kind, plus the total.
-python tools/cert_c5_probe.py"""
+python tools/cert_c5_probe.py [c5|c2]"""
 import collections
 import sys
 import time
@@ -39,15 +39,21 @@ def apply_key(a, kw):
 
 
 wrap("apply", apply_key)
+wrap("apply_stored", lambda a, kw: "apply_stored " + ("R" if kw.get("w_right") is not None
+                                                       else "L"))
+wrap("grad_store", lambda a, kw: "grad_store")
+wrap("eval", lambda a, kw: "eval (fp64, t1-t3 route)")
 wrap("gram", lambda a, kw: "gram")
 wrap("matmul_small", lambda a, kw: "matmul_small")
 
-m, n, k = 200000, 20000, 50
+CASES = {"c5": (200000, 20000, 50, 100.0), "c2": (20000, 20000, 20, 40.0)}
+m, n, k, lam = CASES[sys.argv[1] if len(sys.argv) > 1 else "c5"]
 x = gen_low_rank_plus_sparse_device(m, n, k, 0.05, 1e-3, seed=0)
-spec = ProblemSpec(x=x, lambda_l=100.0, lambda_s=0.1)
+spec = ProblemSpec(x=x, lambda_l=lam, lambda_s=0.1)
 spec.device("mixed")
 rep = solve_split_spcp(spec, k, SolverConfig())
-for r in range(2):
+wrap("grad_release", lambda a, kw: "grad_release")
+for r in range(3):
     STAT.clear()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
