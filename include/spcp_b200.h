@@ -177,11 +177,15 @@ int spcp_apply_f32(spcp_problem* p, int64_t k, const double* z, int64_t b,
  * SPCP_ERR_UNSUPPORTED when it does not fit — keep calling spcp_apply);
  * spcp_apply_stored then gives G W_right / G^T W_left like spcp_apply from one
  * pass over the stored G, without recomputing the rank-k residual;
- * spcp_grad_release frees it. */
+ * spcp_grad_release ends its use.  The stored G and the stored ray below share
+ * one workspace that stays with the problem between uses (allocating and
+ * freeing tens of GB costs 25-500 ms per call); spcp_workspace_trim frees it,
+ * spcp_problem_destroy too. */
 int spcp_grad_store(spcp_problem* p, int64_t k, const double* z, int dtype);
 int spcp_apply_stored(spcp_problem* p, int64_t b, const double* w_right, double* left_out,
                       const double* w_left, double* right_out);
 int spcp_grad_release(spcp_problem* p);
+int spcp_workspace_trim(spcp_problem* p);
 
 /* ---- final L and S (solver.py:313-320) --------------------------------------
  * Rows [row0, row0+rows) of L = U V^T and S* = shrink(X - L) on Omega, float64,
@@ -204,9 +208,10 @@ int spcp_materialize_grad(spcp_problem* p, int64_t k, const double* z, double* g
  * spcp_eval).  spcp_line_probe(a) returns out_host[8] = [F, phi, reg,
  * grad F . dz, 0, 0, 0, 0] at z + a dz (float64, fixed-order sums) from one
  * pass over the stored matrices, without the gradient; spcp_line_release
- * frees them.  Replaces the per-probe fun(x) calls of the reference's
- * strong-Wolfe search (spcp/lbfgs.py:64-99) for the probes that are not
- * accepted; the accepted point is re-evaluated with spcp_eval. */
+ * ends their use (the memory stays for the next search: spcp_workspace_trim).
+ * Replaces the per-probe fun(x) calls of the reference's strong-Wolfe search
+ * (spcp/lbfgs.py:64-99) for the probes that are not accepted; the accepted
+ * point is re-evaluated with spcp_eval. */
 int spcp_line_setup(spcp_problem* p, int64_t k, const double* z, const double* dz);
 int spcp_line_probe(spcp_problem* p, double alpha, double* out_host);
 int spcp_line_release(spcp_problem* p);

@@ -58,6 +58,7 @@ EXPORTS = {
     "spcp_grad_store": [_vp, _i64, _vp, _i32],
     "spcp_apply_stored": [_vp, _i64, _vp, _vp, _vp, _vp],
     "spcp_grad_release": [_vp],
+    "spcp_workspace_trim": [_vp],
     "spcp_line_setup": [_vp, _i64, _vp, _vp],
     "spcp_line_probe": [_vp, _d, _dp],
     "spcp_line_release": [_vp],

@@ -148,11 +148,13 @@ struct spcp_problem {
   bool sddmm = false, sddmm32 = false;  // built; used by fp32 evaluations too
   int64_t nnz = 0;
   spcp::DevBuf csr_ptr, csr_idx, csr_v32, csr_v64, csc_ptr, csc_idx, csc_v32, csc_v64;
-  // line-restricted evaluation (line.cuh): R0, D1, D2 of one ray
-  spcp::DevBuf line_ws, line_part;
+  // one large workspace shared by the stored ray (line.cuh: R0, D1, D2) and the
+  // stored gradient (spcp_grad_store); kept between uses (cudaMalloc / cudaFree
+  // of tens of GB measured 25-500 ms each), freed by spcp_workspace_trim or
+  // spcp_problem_destroy
+  spcp::DevBuf big, line_part;
   bool line_ready = false;
   // stored G of one iterate (spcp_grad_store): the certificate's products
-  spcp::DevBuf gstore;
   int gstore_type = -1;
   double line_zz = 0.0, line_zd = 0.0, line_dd = 0.0;
 };
@@ -304,10 +306,10 @@ static int launch_f64(spcp_problem* p, StreamParams sp, LaunchShape& shape) {
 #ifndef SPCP_F64_MMA
 #define SPCP_F64_MMA 1
 #endif
-template <int KP, bool MASK, bool RAW0 = false>
+template <int KP, bool MASK, bool RAW0 = false, int GOUT = 0>
 static int launch_f64mma(spcp_problem* p, StreamParams sp, LaunchShape& shape) {
   using G = MmaGeom<KP>;
-  auto kern = f64_mma_kernel<KP, MASK, RAW0>;
+  auto kern = f64_mma_kernel<KP, MASK, RAW0, GOUT>;
   constexpr size_t smem = G::SMEM;
   static DevFlags attr = {};
   if (!attr[dev_slot(p->device)].load(std::memory_order_relaxed)) {
@@ -325,12 +327,14 @@ static int launch_f64mma(spcp_problem* p, StreamParams sp, LaunchShape& shape) {
   shape.nrb = int(nrb);
   shape.chunk_cols = sp.chunk_cols;
   int rc;
-  if ((rc = p->pleft.ensure(size_t(nch) * p->m_pad * KP * sizeof(double)))) return rc;
-  if ((rc = p->pright.ensure(size_t(nrb) * p->n_pad * KP * sizeof(double)))) return rc;
   if ((rc = p->pphi.ensure(size_t(nrb * nch) * sizeof(double)))) return rc;
-  sp.pleft = p->pleft.ptr;
-  sp.pright = p->pright.ptr;
   sp.pphi = p->pphi.as<double>();
+  if constexpr (GOUT == 0) {
+    if ((rc = p->pleft.ensure(size_t(nch) * p->m_pad * KP * sizeof(double)))) return rc;
+    if ((rc = p->pright.ensure(size_t(nrb) * p->n_pad * KP * sizeof(double)))) return rc;
+    sp.pleft = p->pleft.ptr;
+    sp.pright = p->pright.ptr;
+  }  // GOUT: sp.pleft is the caller's G destination
   dim3 grid{unsigned(nch), unsigned(nrb), 1u};
   if (p->prof && prof_begin(p)) return SPCP_ERR_CUDA;
   kern<<<grid, G::NT, smem, p->stream>>>(sp);
@@ -1703,7 +1707,7 @@ int spcp_problem_destroy(spcp_problem* p) {
                     &p->scal, &p->gu_tmp, &p->vec_part, &p->small, &p->csr_ptr, &p->csr_idx,
                     &p->csr_v32, &p->csr_v64, &p->csc_ptr, &p->csc_idx, &p->csc_v32,
                     &p->csc_v64, &p->tc_units, &p->tc_begin, &p->tc_csr, &p->tc_uimg,
-                    &p->tc_vimg, &p->tc_scales, &p->tc_bmax, &p->line_ws, &p->line_part, &p->gstore})
+                    &p->tc_vimg, &p->tc_scales, &p->tc_bmax, &p->big, &p->line_part})
     b->release();
   if (p->host_out) cudaFreeHost(p->host_out);
   for (int i = 0; i < spcp_problem::kEvRing; ++i) {
@@ -1884,15 +1888,51 @@ int spcp_grad_store(spcp_problem* p, int64_t k, const double* z, int dtype) {
     return fail(SPCP_ERR_UNSUPPORTED, "grad_store: no dense X store (sparse-observation problem)");
   const size_t es = dtype == SPCP_F32 ? 4 : 8;
   const size_t need = size_t(p->m_pad) * size_t(p->ldx) * es;
-  if (p->gstore.bytes < need) {
-    p->gstore.release();
+  p->line_ready = false;  // the workspace is shared with the stored ray
+  if (p->big.bytes < need) {
+    p->big.release();
     size_t free_b = 0, total_b = 0;
     SPCP_CUDA(cudaMemGetInfo(&free_b, &total_b));
     if (need + (size_t(1) << 30) > free_b)
       return fail(SPCP_ERR_UNSUPPORTED, "grad_store: the m x n gradient does not fit");
-    if ((rc = p->gstore.ensure(need))) return rc;
+    if ((rc = p->big.ensure(need))) return rc;
   }
-  SPCP_CUDA(cudaMemsetAsync(p->gstore.ptr, 0, need, p->stream));  // pads and off-Omega rows
+  if (!p->x64.ptr && k <= 64 && SPCP_F64_MMA) {
+    // fp32-exact X: G from the FP64 tensor-core pass's phase 1 (every entry of
+    // the padded array written: pads and off-Omega entries are zeros)
+    if ((rc = prep<double>(p, k, int(round_up(k, 8)), z, nullptr, 0.0))) return rc;
+    StreamParams sp{};
+    sp.m_pad = p->m_pad;
+    sp.n_pad = p->n_pad;
+    sp.ldx = p->ldx;
+    sp.ldm = p->ldm;
+    sp.tau = p->lambda_s;
+    sp.x = p->x32.ptr;
+    sp.mbits = p->masked ? p->mbits.as<uint32_t>() : nullptr;
+    sp.uc = p->uc.ptr;
+    sp.vc = p->vc.ptr;
+    sp.pleft = p->big.ptr;
+    LaunchShape sh;
+    const int kp = int(round_up(k, 8));
+#define SPCP_CASE(K)                                                                        \
+  case K:                                                                                   \
+    rc = dtype == SPCP_F32                                                                  \
+             ? (p->masked ? launch_f64mma<K, true, false, 4>(p, sp, sh)                     \
+                          : launch_f64mma<K, false, false, 4>(p, sp, sh))                   \
+             : (p->masked ? launch_f64mma<K, true, false, 8>(p, sp, sh)                     \
+                          : launch_f64mma<K, false, false, 8>(p, sp, sh));                  \
+    break;
+    switch (kp) {
+      SPCP_CASE(8) SPCP_CASE(16) SPCP_CASE(24) SPCP_CASE(32) SPCP_CASE(40) SPCP_CASE(48)
+      SPCP_CASE(56) SPCP_CASE(64)
+      default: return fail(SPCP_ERR_UNSUPPORTED, "grad_store width");
+    }
+#undef SPCP_CASE
+    if (rc) return rc;
+    p->gstore_type = dtype;
+    return SPCP_OK;
+  }
+  SPCP_CUDA(cudaMemsetAsync(p->big.ptr, 0, need, p->stream));  // pads and off-Omega rows
   const int64_t nbx = ceil_div(p->n, 64), nby = ceil_div(p->m, 64);
   if ((rc = p->pphi.ensure(size_t(nbx * nby) * sizeof(double)))) return rc;
   const dim3 grid{unsigned(nbx), unsigned(nby), 1u};
@@ -1900,7 +1940,7 @@ int spcp_grad_store(spcp_problem* p, int64_t k, const double* z, int dtype) {
 #define SPCP_GS(TX, XP, TO)                                                                \
   dense_kernel<TX, 1, TO><<<grid, 256, 0, p->stream>>>(z, p->m, p->n, k, XP, p->ldx, mb,    \
                                                        p->ldm, p->lambda_s, 0, p->m,        \
-                                                       p->gstore.as<TO>(), nullptr, p->ldx, \
+                                                       p->big.as<TO>(), nullptr, p->ldx,     \
                                                        p->pphi.as<double>())
   if (p->x64.ptr) {
     if (dtype == SPCP_F32) SPCP_GS(double, p->x64.as<double>(), float);
@@ -1922,17 +1962,24 @@ int spcp_apply_stored(spcp_problem* p, int64_t b, const double* w_right, double*
   if (p->gstore_type < 0) return fail(SPCP_ERR_VALUE, "apply_stored before grad_store");
   return p->gstore_type == SPCP_F32
              ? apply_impl<float>(p, 0, nullptr, b, w_right, left_out, w_left, right_out,
-                                 p->gstore.ptr)
+                                 p->big.ptr)
              : apply_impl<double>(p, 0, nullptr, b, w_right, left_out, w_left, right_out,
-                                  p->gstore.ptr);
+                                  p->big.ptr);
 }
 
 int spcp_grad_release(spcp_problem* p) {
   if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
+  p->gstore_type = -1;  // the memory stays with the problem (spcp_workspace_trim)
+  return SPCP_OK;
+}
+
+int spcp_workspace_trim(spcp_problem* p) {
+  if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
   SPCP_CUDA(cudaSetDevice(p->device));
   if (p->stream) SPCP_CUDA(cudaStreamSynchronize(p->stream));
-  p->gstore.release();
+  p->big.release();
   p->gstore_type = -1;
+  p->line_ready = false;
   return SPCP_OK;
 }
 
@@ -2013,15 +2060,16 @@ int spcp_line_setup(spcp_problem* p, int64_t k, const double* z, const double* d
   const size_t per = size_t(p->m) * size_t(p->n_pad);
   const size_t ld = size_t(round_up(int64_t(per), 32));  // 256-byte aligned matrices
   const size_t need = 3 * ld * sizeof(double);
-  if (p->line_ws.bytes < need) {
-    p->line_ws.release();
+  p->gstore_type = -1;  // the workspace is shared with the stored gradient
+  if (p->big.bytes < need) {
+    p->big.release();
     size_t free_b = 0, total_b = 0;
     SPCP_CUDA(cudaMemGetInfo(&free_b, &total_b));
     if (need + (size_t(1) << 30) > free_b)
       return fail(SPCP_ERR_UNSUPPORTED, "line_setup: the three m x n float64 matrices do not fit");
-    if ((rc = p->line_ws.ensure(need))) return rc;
+    if ((rc = p->big.ensure(need))) return rc;
   }
-  double* r0 = p->line_ws.as<double>();
+  double* r0 = p->big.as<double>();
   const uint32_t* mb = p->masked ? p->mbits.as<uint32_t>() : nullptr;
   if (!p->x64.ptr && k <= 64 && SPCP_F64_MMA) {
     // fp32-exact X: the three products on the FP64 tensor cores
@@ -2079,7 +2127,7 @@ int spcp_line_probe(spcp_problem* p, double alpha, double* out_host) {
   if ((rc = p->line_part.ensure(size_t(2 * nb) * sizeof(double)))) return rc;
   const size_t per = size_t(p->m) * size_t(p->n_pad);
   const size_t ld = size_t(round_up(int64_t(per), 32));
-  const double* r0 = p->line_ws.as<double>();
+  const double* r0 = p->big.as<double>();
   line_probe_kernel<<<nb, 256, 0, p->stream>>>(r0, r0 + ld, r0 + 2 * ld, int64_t(per), alpha,
                                                p->lambda_s, p->line_part.as<double>());
   SPCP_CHECK_LAUNCH("line_probe");
@@ -2104,9 +2152,7 @@ int spcp_line_probe(spcp_problem* p, double alpha, double* out_host) {
 int spcp_line_release(spcp_problem* p) {
   if (!p) return fail(SPCP_ERR_VALUE, "null problem handle");
   SPCP_CUDA(cudaSetDevice(p->device));
-  if (p->stream) SPCP_CUDA(cudaStreamSynchronize(p->stream));
-  p->line_ws.release();
-  p->line_ready = false;
+  p->line_ready = false;  // the memory stays with the problem (spcp_workspace_trim)
   return SPCP_OK;
 }
 

@@ -19,6 +19,8 @@
 // accumulators measured 3.35 vs 3.25 ms, so the single-warp K loops stay.)
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "stream_simt.cuh"
 
@@ -52,7 +54,9 @@ struct MmaGeom {
 // X W and X^T Q): phase 1 only stages the observed X tile as G (fp64), and
 // phases 2 / 3 run when p.do_left / p.do_right ask for them, with uc / vc
 // holding the staged W_left / W_right (KP columns).
-template <int KP, bool MASK, bool RAW0 = false>
+// GOUT (4 / 8): phase 1 only, the G tile written to p.pleft as float / double
+// [m_pad][ldx] (spcp_grad_store: the certificate's stored gradient).
+template <int KP, bool MASK, bool RAW0 = false, int GOUT = 0>
 __global__ void __launch_bounds__(256, 1) f64_mma_kernel(const StreamParams p) {
   using G = MmaGeom<KP>;
   constexpr int BM = G::BM, BN = G::BN, KS = G::KS, GS = G::GS, XS = G::XS, NN = G::NN;
@@ -77,8 +81,9 @@ __global__ void __launch_bounds__(256, 1) f64_mma_kernel(const StreamParams p) {
   const double* __restrict__ Uc = reinterpret_cast<const double*>(p.uc);
   const double* __restrict__ Vc = reinterpret_cast<const double*>(p.vc);
 
-  const bool do_left = !RAW0 || p.do_left, do_right = !RAW0 || p.do_right;
-  if (do_right) {  // the row band's U (once)
+  const bool need_u = !RAW0 || p.do_right, need_v = !RAW0 || p.do_left;
+  const bool do_left = GOUT == 0 && need_v, do_right = GOUT == 0 && need_u;
+  if (need_u) {  // the row band's U (once)
     constexpr int CPR = KP / 2;
     for (int q = tid; q < BM * CPR; q += 256) {
       const int r = q / CPR, c = q % CPR;
@@ -101,7 +106,7 @@ __global__ void __launch_bounds__(256, 1) f64_mma_kernel(const StreamParams p) {
   auto load_v = [&](int t) {
     const int64_t c0 = c_begin + int64_t(t) * BN;
     constexpr int CPR = KP / 2;
-    for (int q = tid; q < (do_left ? BN * CPR : 0); q += 256) {
+    for (int q = tid; q < (need_v ? BN * CPR : 0); q += 256) {
       const int r = q / CPR, c = q % CPR;
       cp_async16(Vs + r * KS + 2 * c, Vc + (c0 + r) * KP + 2 * c);
     }
@@ -187,6 +192,20 @@ __global__ void __launch_bounds__(256, 1) f64_mma_kernel(const StreamParams p) {
     }
     __syncthreads();  // G tile complete; X and the mask free
     if (t + 1 < ntiles) load_x(t + 1);
+    if constexpr (GOUT != 0) {
+      using TO = typename std::conditional<GOUT == 4, float, double>::type;
+      if (t + 1 < ntiles) load_v(t + 1);  // V_t consumed by phase 1
+      const int64_t c0 = c_begin + int64_t(t) * BN;
+      TO* dst = reinterpret_cast<TO*>(p.pleft);
+      for (int q = tid; q < BM * (BN / 2); q += 256) {
+        const int r = q / (BN / 2), c = 2 * (q % (BN / 2));
+        const double2 g = *reinterpret_cast<const double2*>(Gs + r * GS + c);
+        TO* o = dst + (r0 + r) * p.ldx + c0 + c;
+        o[0] = TO(g.x);
+        o[1] = TO(g.y);
+      }
+      continue;
+    }
 
     // ---------------- phase 2: Lacc += G V_t   (A = G rows, B = V_t)
     if (do_left) {

@@ -276,6 +276,11 @@ class DeviceProblem:
     def grad_release(self):
         check(lib.spcp_grad_release(self.h))
 
+    def trim_workspace(self):
+        """Free the large workspace shared by the stored ray and the stored
+        gradient (kept between uses; also freed by close())."""
+        check(lib.spcp_workspace_trim(self.h))
+
     # ------------------------------------------------------------ line probes
     def line_setup(self, k, z, dz):
         """Store R0, D1, D2 of the ray z + a dz (csrc/line.cuh).  False when the
