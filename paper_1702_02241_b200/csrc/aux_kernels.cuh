@@ -794,13 +794,20 @@ struct GramPtrs {
   const double* a[kGramNA];
   const double* b[4];
 };
+// a-vectors in groups of kGramGA over blockIdx.y: every accumulator index is a
+// compile-time constant, so acc[][] lives in registers (indexing it with the
+// runtime count put the whole array in local memory: a local read-modify-write
+// per FMA); each group re-reads the NB b-vectors
+constexpr int kGramGA = 8;
 template <int NB>
 __global__ void __launch_bounds__(256) vec_gram_kernel(GramPtrs gp, int na, int64_t len,
                                                        double* part) {
   __shared__ double scratch[32];
-  double acc[kGramNA][NB];
+  const int i0 = int(blockIdx.y) * kGramGA;
+  const int nga = na - i0 < kGramGA ? na - i0 : kGramGA;  // block-uniform
+  double acc[kGramGA][NB];
 #pragma unroll
-  for (int i = 0; i < kGramNA; ++i)
+  for (int i = 0; i < kGramGA; ++i)
 #pragma unroll
     for (int j = 0; j < NB; ++j) acc[i][j] = 0.0;
   for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < len;
@@ -809,19 +816,22 @@ __global__ void __launch_bounds__(256) vec_gram_kernel(GramPtrs gp, int na, int6
 #pragma unroll
     for (int j = 0; j < NB; ++j) bv[j] = gp.b[j][q];
 #pragma unroll
-    for (int i = 0; i < kGramNA; ++i) {
-      if (i < na) {
-        const double av = gp.a[i][q];
+    for (int i = 0; i < kGramGA; ++i) {
+      if (i < nga) {
+        const double av = gp.a[i0 + i][q];
 #pragma unroll
         for (int j = 0; j < NB; ++j) acc[i][j] = fma(av, bv[j], acc[i][j]);
       }
     }
   }
-  for (int i = 0; i < na; ++i)
 #pragma unroll
-    for (int j = 0; j < NB; ++j) {
-      const double s = block_sum(acc[i][j], scratch);
-      if (threadIdx.x == 0) part[(int64_t(blockIdx.x) * kGramNA + i) * NB + j] = s;
+  for (int i = 0; i < kGramGA; ++i)
+    if (i < nga) {
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        const double s = block_sum(acc[i][j], scratch);
+        if (threadIdx.x == 0) part[(int64_t(blockIdx.x) * kGramNA + i0 + i) * NB + j] = s;
+      }
     }
 }
 

@@ -2209,19 +2209,33 @@ static int vec_gram_impl(spcp_problem* p, int64_t len, int na, const double* con
   SPCP_CUDA(cudaSetDevice(p->device));
   if (nb < 1 || nb > 4 || na < 1) return fail(SPCP_ERR_VALUE, "vec_gram: need 1<=nb<=4, na>=1");
   if ((rc = ensure_common(p))) return rc;
-  const int nblk = grid_for(len, 256, 148 * 2);
+  // one wave: the (column block x a-group) grid fills the resident slots of
+  // the kernel's register budget (more blocks only add a partial second wave)
+  static DevFlags occ[4] = {};
+  int per_sm = occ[nb - 1][dev_slot(p->device)].load(std::memory_order_relaxed);
+  if (!per_sm) {
+    cudaError_t e = nb == 1 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vec_gram_kernel<1>, 256, 0)
+                  : nb == 2 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vec_gram_kernel<2>, 256, 0)
+                  : nb == 3 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vec_gram_kernel<3>, 256, 0)
+                            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vec_gram_kernel<4>, 256, 0);
+    if (e != cudaSuccess || per_sm < 1) per_sm = 2;
+    occ[nb - 1][dev_slot(p->device)].store(per_sm, std::memory_order_relaxed);
+  }
   for (int a0 = 0; a0 < na; a0 += kGramNA) {
     const int cnt = std::min(kGramNA, na - a0);
+    const int ngroups = int(ceil_div(cnt, kGramGA));
+    const int nblk = grid_for(len, 256, std::max<int64_t>(kSMs, int64_t(kSMs) * per_sm / ngroups));
     GramPtrs gp{};
     for (int i = 0; i < cnt; ++i) gp.a[i] = a[a0 + i];
     for (int j = 0; j < nb; ++j) gp.b[j] = b[j];
     if ((rc = p->vec_part.ensure(size_t(nblk) * kGramNA * 4 * sizeof(double)))) return rc;
     double* part = p->vec_part.as<double>();
+    const dim3 grid{unsigned(nblk), unsigned(ceil_div(cnt, kGramGA)), 1u};
     switch (nb) {
-      case 1: vec_gram_kernel<1><<<nblk, 256, 0, p->stream>>>(gp, cnt, len, part); break;
-      case 2: vec_gram_kernel<2><<<nblk, 256, 0, p->stream>>>(gp, cnt, len, part); break;
-      case 3: vec_gram_kernel<3><<<nblk, 256, 0, p->stream>>>(gp, cnt, len, part); break;
-      default: vec_gram_kernel<4><<<nblk, 256, 0, p->stream>>>(gp, cnt, len, part); break;
+      case 1: vec_gram_kernel<1><<<grid, 256, 0, p->stream>>>(gp, cnt, len, part); break;
+      case 2: vec_gram_kernel<2><<<grid, 256, 0, p->stream>>>(gp, cnt, len, part); break;
+      case 3: vec_gram_kernel<3><<<grid, 256, 0, p->stream>>>(gp, cnt, len, part); break;
+      default: vec_gram_kernel<4><<<grid, 256, 0, p->stream>>>(gp, cnt, len, part); break;
     }
     SPCP_CHECK_LAUNCH("vec_gram");
     double* dst = out_dev ? out_dev + size_t(a0) * nb : p->out_dev.as<double>();
