@@ -696,7 +696,8 @@ static int tc_launch(spcp_problem* p, int64_t k) {
   tp.pleft = p->pleft.as<float>();
   tp.pright = p->pright.as<float>();
   tp.pphi = p->pphi.as<double>();
-  tp.kstore = int(round_up(k, 4));
+  // partial row stride: the K-concatenated drains write SEG columns
+  tp.kstore = SEG > 0 ? SEG : int(round_up(k, 4));
 #ifdef SPCP_TC_TIMESTAMPS
   static long long* dbg = nullptr;
   if (!dbg) SPCP_CUDA(cudaMalloc(&dbg, 64 * 32 * sizeof(long long)));
@@ -781,19 +782,20 @@ static int tc_prep_kc(spcp_problem* p, int64_t k, const double* z, const double*
   return SPCP_OK;
 }
 
-// K-concatenated layout (k <= 20): SEG = round_up(k, 4).  The two-atom rows of
-// k = 21..32 (SEG 24-32) build and are exact, but their shared-memory budget
-// leaves two X stages and one U buffer: measured at C4 (k = 30, mask) 0.68 ms
-// against 0.59 ms for the split-image layout, so they stay off.
+// K-concatenated layout (k <= 32): SEG = round_up(k, 4) up to 20; k = 21..32
+// take SEG = 32 with one-atom rows (TcCfg::REUSE: the third K-segment re-reads
+// the stored ones).  (Storing the third segment as a second atom left two X
+// stages and one U buffer in shared memory: 0.68 vs 0.59 ms at C4.)
 static bool tc_use_kc(int64_t k) {
   static const bool split = env_str("SPCP_TC_LAYOUT") == "split";
-  return k <= 20 && !split;
+  return k <= 32 && !split;
 }
+static int kc_seg(int64_t k) { return k <= 20 ? int(round_up(k, 4)) : 32; }
 
-#define SPCP_KC_SEGS(X) X(4) X(8) X(12) X(16) X(20)
+#define SPCP_KC_SEGS(X) X(4) X(8) X(12) X(16) X(20) X(32)
 template <bool MASK>
 static int tc_launch_kc(spcp_problem* p, int64_t k) {
-  switch (int(round_up(k, 4))) {
+  switch (kc_seg(k)) {
 #define SPCP_KC_CASE(S) \
     case S: return tc_launch<16, MASK, S>(p, k);
     SPCP_KC_SEGS(SPCP_KC_CASE)
@@ -808,7 +810,7 @@ static int tc_eval(spcp_problem* p, int64_t k, const double* z, const double* dz
   if ((rc = tc_build(p))) return rc;
   if (tc_use_kc(k)) {
 #if SPCP_TC_PREP_FUSED
-    switch (int(round_up(k, 4))) {
+    switch (kc_seg(k)) {
 #define SPCP_KC_CASE(S) \
       case S: rc = tc_prep_kc<S>(p, k, z, dz, alpha); break;
       SPCP_KC_SEGS(SPCP_KC_CASE)
@@ -822,7 +824,7 @@ static int tc_eval(spcp_problem* p, int64_t k, const double* z, const double* dz
                          nu, nv, p->tc_bmax.as<unsigned long long>()));
     SPCP_CHECK_LAUNCH("tc_max");
     p->launches += 1;
-    switch (int(round_up(k, 4))) {
+    switch (kc_seg(k)) {
 #define SPCP_KC_CASE(S) \
       case S: rc = tc_images_kc<S>(p, k, z, dz, alpha); break;
       SPCP_KC_SEGS(SPCP_KC_CASE)
@@ -831,9 +833,9 @@ static int tc_eval(spcp_problem* p, int64_t k, const double* z, const double* dz
     }
 #endif
     if (rc) return rc;
-    const int kst = int(round_up(k, 4));
+    const int kst = kc_seg(k);  // slot row stride: the drains write SEG columns
     if ((rc = p->pleft.ensure(size_t(p->tc_runs) * 128 * kst * sizeof(float)))) return rc;
-    constexpr int gt_rows = SPCP_TC_GT_FOLD ? 64 : 128;
+    const int gt_rows = (SPCP_TC_GT_FOLD || kc_seg(k) == 32) ? 64 : 128;  // TcCfg::GT_FOLD
     if ((rc = p->pright.ensure(size_t(p->tc_slots) * gt_rows * kst * sizeof(float)))) return rc;
     if ((rc = p->pphi.ensure(size_t(p->tc_grid) * sizeof(double)))) return rc;
     rc = p->masked ? tc_launch_kc<true>(p, k) : tc_launch_kc<false>(p, k);

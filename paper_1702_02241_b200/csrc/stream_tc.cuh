@@ -117,7 +117,16 @@ struct TcCfg {
   //   reductions only read atom 0.  SEG == 0: two split images [uh|um], [vh|vm].
   static constexpr bool KC = SEG > 0;
   static constexpr int KE = 3 * SEG;
-  static constexpr int NA = KC ? (KE * 2 + 127) / 128 : 1;  // K-atoms per image row
+  // REUSE (SEG = 32, k = 21..32): rows store only the first two segments,
+  // U = [um | uh], V = [vh | vm] (one 128-byte atom); the residual's third
+  // K-segment re-reads uh (TMEM copies) and vh (B descriptors) instead of a
+  // stored duplicate, so these ranks keep the one-atom pipeline depths
+  static constexpr bool REUSE = KC && SEG % 16 == 0 && 3 * SEG > 64 && 2 * SEG <= 64;
+  static constexpr int NA = KC ? (REUSE ? 1 : (KE * 2 + 127) / 128) : 1;  // K-atoms per row
+  // gh / gl parts of G^T U summed in the drain (64-row slots): measured a win
+  // for the wide REUSE rows (C4: step 0.697 -> 0.661 ms), a loss for SEG <= 20
+  // (C2 kernel 0.333 -> 0.365 ms)
+  static constexpr bool GT_FOLD = KC && (SPCP_TC_GT_FOLD || REUSE);
   static constexpr int RB = KC ? (NA > 1 ? 128 : (KE <= 16 ? 32 : (KE <= 32 ? 64 : 128)))
                                : KP16 * 2;
   static constexpr uint32_t SWK = RB == 128 ? tc::SW_128 : (RB == 64 ? tc::SW_64 : tc::SW_32);
@@ -310,10 +319,17 @@ __device__ __noinline__ void tc_residual_issuer(unsigned char* sm, TcBarriers* b
         tc_fence_after();
         const uint64_t du = dU_k + uint64_t(ubuf * (C::U_BYTES >> 4));
         if (do_mma && !(SPCP_TC_DEBUG_BITS & 64)) {
-          static_for<C::NKS>([&](auto I) {  // K-step I: atom I / 4, 32 B step I % 4
-            tmem_cp_128x256b_w(tm + C::T_U + 8 * I,
-                               du + uint64_t((I / 4) * (C::U_ATOM >> 4) + 2 * (I % 4)));
-          });
+          if constexpr (C::REUSE) {
+            static_for<C::NKS>([&](auto I) {  // K-steps 4, 5 repeat uh (steps 2, 3)
+              constexpr int src = I < 4 ? int(I) : int(I) - 2;
+              tmem_cp_128x256b_w(tm + C::T_U + 8 * I, du + uint64_t(2 * src));
+            });
+          } else {
+            static_for<C::NKS>([&](auto I) {  // K-step I: atom I / 4, 32 B step I % 4
+              tmem_cp_128x256b_w(tm + C::T_U + 8 * I,
+                                 du + uint64_t((I / 4) * (C::U_ATOM >> 4) + 2 * (I % 4)));
+            });
+          }
         }
       }
     }
@@ -337,8 +353,9 @@ __device__ __noinline__ void tc_residual_issuer(unsigned char* sm, TcBarriers* b
           mma_ts_batch<C::NKS, 2>(dt, tm + C::T_U, db, ID_RES, 0u);
         } else {
           mma_ts_batch<4, 2>(dt, tm + C::T_U, db, ID_RES, 0u);
-          mma_ts_batch<C::NKS - 4, 2>(dt, tm + C::T_U + 32, db + uint64_t(C::V_ATOM >> 4),
-                                      ID_RES, 1u);
+          // K-steps 4..: atom 1 of the rows, or (REUSE) vh again
+          mma_ts_batch<C::NKS - 4, 2>(dt, tm + C::T_U + 32,
+                                      db + uint64_t(C::REUSE ? 0 : (C::V_ATOM >> 4)), ID_RES, 1u);
         }
       } else {
         static_for<3 * KS>([&](auto I) {
@@ -643,7 +660,7 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK, SEG>::NTHREADS, 1)
       tc_fence_after();
       if constexpr (C::KC) {
         if (!(SPCP_TC_DEBUG_BITS & 1)) {
-#if SPCP_TC_GT_FOLD
+          if constexpr (C::GT_FOLD) {
           // M = 128 stacked accumulator: lanes 0..63 hold the gh part of tile
           // columns 0..63, lanes 64..127 the gl part; output column c = D[c]
           // (um) + D[SEG + c] (uh).  Quarters 2, 3 park their gl part in the
@@ -695,7 +712,7 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK, SEG>::NTHREADS, 1)
             });
           }
           named_bar_sync(1 + grp, 32 * C::NEG);  // read before G(t) reuses the image
-#else
+} else {
           // M = 128 stacked accumulator: lane = slot row (0..63 gh part, 64..127 gl
           // part), kept as separate 128-row slots (summed by the reduce kernel);
           // output column c = D[c] (um) + D[SEG + c] (uh)
@@ -722,7 +739,7 @@ __global__ void __launch_bounds__(TcCfg<KP16, MASK, SEG>::NTHREADS, 1)
                            __float_as_uint(o.w));
             }
           });
-#endif
+}
         }
       } else if (!(SPCP_TC_DEBUG_BITS & 1)) {
         // chunked slot [kst / 4][64 rows][4] (coalesced float4 stores)
@@ -1212,10 +1229,10 @@ __device__ __forceinline__ void tc_images_kc_body(const double* __restrict__ z,
       *reinterpret_cast<__half*>(base + (e / EPA) * atom +
                                  tc::Swz<RB>::offset(rr, (e % EPA) * 2)) = val;
     };
-    // U: segments (m, h, h); V: (h, m, h)
+    // U: segments (m, h, h); V: (h, m, h) (REUSE: the first two only)
     put(c, is_u ? lo : hh);
     put(SEG + c, is_u ? hh : lo);
-    put(2 * SEG + c, hh);
+    if constexpr (!C::REUSE) put(2 * SEG + c, hh);
     for (int e = 3 * SEG + c; e < NE; e += SEG) put(e, __half(0.f));
   }
 }

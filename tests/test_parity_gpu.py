@@ -92,6 +92,9 @@ SHAPES = [  # m, n, k, masked — multiple tiles / chunks / bands, ragged edges
     (900, 700, 5, True),    # K-concatenated images, SEG = 8 (two K-steps)
     (700, 1100, 16, False),  # SEG = 16
     (5000, 260, 12, True),  # SEG = 12, tall-skinny (C3 shape class)
+    (1100, 900, 21, False),  # SEG = 32 one-atom rows (k = 21..32), padded ranks
+    (600, 1300, 27, True),
+    (2000, 700, 30, False),  # C4's rank
 ]
 
 
