@@ -63,6 +63,10 @@
 #define SPCP_TC_GT_FOLD 0
 #endif
 
+#ifndef SPCP_TC_GV_FIRST
+#define SPCP_TC_GV_FIRST 1
+#endif
+
 #ifndef SPCP_TC_XPF
 #define SPCP_TC_XPF 0  // X tiles prefetched into L2 ahead of the stage ring (measured: no gain)
 #endif
@@ -415,6 +419,7 @@ __device__ __noinline__ void tc_reduction_issuer(unsigned char* sm, TcBarriers* 
     tc_fence_after();
     const uint64_t dUn = dUn0 + uint64_t(ubuf * (C::U_BYTES >> 4));
     const uint64_t goff = uint64_t((C::GB == 1 ? 0 : b) * (C::G_BYTES >> 4));
+    auto issue_gt = [&]() {
     const uint32_t gt = tm + C::T_GT + gtb * C::GTW;
     if (C::KC && ROLE != 2 && do_mma && !(SPCP_TC_DEBUG_BITS & 16)) {
       // stacked [gh; gl]^T U: 8 K-steps of 16 tile rows (A += 2048 B, B += 16 RB)
@@ -440,6 +445,8 @@ __device__ __noinline__ void tc_reduction_issuer(unsigned char* sm, TcBarriers* 
     if (ROLE != 2) tc_commit<C::KC>(&bar->gt_full[gtb]);
     if (C::KC && ROLE != 2) tc_commit<C::KC>(&bar->gs_empty[b]);  // G image: G^T U's operand only
     TC_TS(t, ROLE == 2 ? 29 : 25);
+    };
+    auto issue_gv = [&]() {
     const uint64_t dVn = dVn0 + uint64_t(st * (C::V_BYTES >> 4));
     const uint32_t gv = tm + C::T_GV + gvb * C::GVW;
     if (C::KC && ROLE != 1 && do_mma && !(SPCP_TC_DEBUG_BITS & 32)) {
@@ -469,6 +476,16 @@ __device__ __noinline__ void tc_reduction_issuer(unsigned char* sm, TcBarriers* 
     if (!C::KC) mma_commit(&bar->gs_empty[b]);  // per tile parity (see the epilogue's wait)
     else if (ROLE != 1) tc_commit<C::KC>(&bar->s_empty[t % C::NSB]);  // S / G columns
     if (ROLE != 1) tc_commit<C::KC>(&bar->v_empty[st]);
+    };
+    // KC + SPCP_TC_GV_FIRST: G.V first (its completion frees the tile's S
+    // columns for the residual of tile t + NSB), then G^T U (frees the G image)
+    if constexpr (C::KC && SPCP_TC_GV_FIRST) {
+      issue_gv();
+      issue_gt();
+    } else {
+      issue_gt();
+      issue_gv();
+    }
     if (un.flags & TCU_LAST_OF_RUN) {
       if (ROLE != 1) tc_commit<C::KC>(&bar->gv_full[gvb]);
       if (ROLE != 2) tc_commit<C::KC>(&bar->u_empty[ubuf]);
