@@ -183,7 +183,7 @@ struct TcCfg {
 #ifndef SPCP_TC_NSB
 #define SPCP_TC_NSB 3  // measured: 3 (0.339 ms) beats 4 with two G^T U buffers (0.347 ms)
 #endif
-  static constexpr int NSB = KC ? SPCP_TC_NSB : 2;
+  static constexpr int NSB = KC ? ((2 * SEG + 15) / 16 * 16 > 48 ? 3 : SPCP_TC_NSB) : 2;
   static_assert(NSB <= 4, "TcBarriers holds four S buffers");
   static constexpr uint32_t T_S = 0, T_GV = 64 * NSB;
   static constexpr uint32_t T_GT = T_GV + 2 * GVW;
