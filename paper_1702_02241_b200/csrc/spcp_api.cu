@@ -1186,11 +1186,15 @@ static int run_reduce(spcp_problem* p, int64_t k, int kp, int part_dtype, const 
     rp.chunked = sh.chunked;
     rp.tc_unscale = &p->tc_scales.as<TcScales>()->gv_unscale;
   }
-  // SPCP_TC_FOLD=1: one block per sub-band / column tile (tc_fold_kernel).
-  // Measured same-box against the LPI kernel: C2 step 0.412 vs 0.415 ms, C4
-  // 0.678 vs 0.701, C3 (k = 5) 0.223 vs 0.213, C1 0.034 vs 0.032 — a wash, so
-  // the LPI kernel stays the default.
-  static const bool fold_env = env_str("SPCP_TC_FOLD") == "1";
+  // One block per sub-band / column tile (tc_fold_kernel) vs the LPI kernel.
+  // First measured mid-round (C2 step 0.412 vs 0.415 ms, C4 0.678 vs 0.701, C3
+  // k = 5 0.223 vs 0.213, C1 0.034 vs 0.032).
+  // Re-measured with the final fused kernel (`gpurun_out/r2bf_configs.txt`,
+  // same box, two rounds): C2 step 0.391 vs 0.395 ms, C4 0.620 vs 0.643, C3 and
+  // C5 within noise, C1 0.034 vs 0.032 — on by default above 2^24 entries
+  // (SPCP_TC_FOLD=0 / 1 forces it off / on).
+  static const std::string fold_s = env_str("SPCP_TC_FOLD");
+  const bool fold_env = fold_s == "1" || (fold_s != "0" && p->m * p->n >= (int64_t(1) << 24));
   if (sh.tc && sh.chunked && (u_mode == U_FULL || u_mode == U_PARTIAL) && v_mode && fold_env &&
       p->tc_max_u_src <= kFoldMaxSrc && p->tc_max_v_src <= kFoldMaxSrc) {
     // one block per sub-band / column tile (tc_fold_kernel)
